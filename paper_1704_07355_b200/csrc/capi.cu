@@ -1,0 +1,671 @@
+// C ABI of libqadc_b200 (include/qadc_b200.h): the reference kernel ABI
+// (scan_kernels.h:15-46) re-implemented on sm_100a, plus the batched
+// device-resident search (adc.py:114-187 for many queries at once).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "qadc_b200.h"
+#include "internal.cuh"
+
+namespace qadc {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+int cuda_fail(cudaError_t e, const char *where) {
+  g_err = std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + where;
+  return kErrCuda;
+}
+
+namespace {
+
+int arg_error(const std::string &msg) {
+  g_err = msg;
+  return kErrArgs;
+}
+
+int device_sms() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+__global__ void k_transpose(const float *__restrict__ in, int rows, int cols, float *__restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)rows * cols;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(t / cols), c = (int)(t % cols);
+    out[(size_t)c * rows + r] = in[t];
+  }
+}
+
+__global__ void k_init_bounds(unsigned *M_bits, const unsigned *M_override, float *hist_w, int nq) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    unsigned mb = M_bits[q];
+    if (M_override) mb = min(mb, M_override[q]);
+    M_bits[q] = mb;
+    const float M = __uint_as_float(mb);
+    hist_w[q] = (isfinite(M) && M > 0.f) ? M / (float)kHistBins : 0.f;
+  }
+}
+
+__global__ void k_gather_rows_f(const float *__restrict__ src, const int *__restrict__ rows, int n,
+                                int width, float *__restrict__ dst) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * width;
+       t += (int64_t)gridDim.x * blockDim.x)
+    dst[t] = src[(size_t)rows[t / width] * width + t % width];
+}
+__global__ void k_gather_rows_i(const int64_t *__restrict__ src, const int *__restrict__ rows, int n,
+                                int width, int64_t *__restrict__ dst) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * width;
+       t += (int64_t)gridDim.x * blockDim.x)
+    dst[t] = src[(size_t)rows[t / width] * width + t % width];
+}
+__global__ void k_gather_u(const unsigned *__restrict__ src, const int *__restrict__ rows, int n,
+                           unsigned *__restrict__ dst) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    dst[t] = src[rows[t]];
+}
+__global__ void k_scatter_out(const int64_t *__restrict__ ids, const float *__restrict__ d,
+                              const int32_t *__restrict__ n, const int *__restrict__ rows, int cnt,
+                              int R, int64_t *__restrict__ out_ids, float *__restrict__ out_d,
+                              int32_t *__restrict__ out_n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)cnt * R;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / R), r = (int)(t % R);
+    out_ids[(size_t)rows[i] * R + r] = ids[t];
+    out_d[(size_t)rows[i] * R + r] = d[t];
+    if (r == 0) out_n[rows[i]] = n[i];
+  }
+}
+
+// ivf.py:181-182: residual = q - C[cell] in fp32.
+__global__ void k_residuals(const float *__restrict__ queries, const float *__restrict__ coarse,
+                            const int64_t *__restrict__ cells, int nq, int ma, int d,
+                            float *__restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)nq * ma * d;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pair = t / d;
+    const int c = (int)(t % d);
+    out[t] = __fsub_rn(queries[(pair / ma) * d + c], coarse[cells[pair] * d + c]);
+  }
+}
+
+inline int gridn(int64_t n) {
+  return (int)std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 148 * 16);
+}
+
+template <class T>
+struct DevBuf {
+  T *p = nullptr;
+  cudaStream_t st = nullptr;
+  int alloc(int64_t n, cudaStream_t s) {
+    st = s;
+    if (cudaMallocAsync(&p, (size_t)std::max<int64_t>(n, 1) * sizeof(T), s) != cudaSuccess)
+      return kErrCuda;
+    return kOk;
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+struct SearchStats {
+  int64_t codes = 0, cands = 0, reruns = 0, scan_launches = 0, launches = 0;
+  double scan_us = 0.0;
+};
+
+int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int ma, int init,
+                const float *lut_in, const int64_t *cells_in, int64_t *out_ids, float *out_d,
+                int32_t *out_n, cudaStream_t st, SearchStats &ss, const unsigned *M_override,
+                int cap_g, int depth) {
+  if (nq == 0) return kOk;
+  const int m = idx->m;
+  const int nslots = idx->K ? ma : 1;
+  const int64_t npairs = (int64_t)nq * nslots;
+  const int qt_tile = scan_qt_per_cta(m);
+  const int nl = idx->nlists;
+
+  DevBuf<int64_t> cells_b;
+  DevBuf<float> lut_b, qmax_b, qmin_f, delta_f, fsat_mid, cand_mid, hist_w;
+  DevBuf<uint32_t> qt_b;
+  DevBuf<unsigned> M_bits, cand_n, hist;
+  DevBuf<int> fsat_n, n_items, counter, scratch, overflow;
+  DevBuf<int64_t> fsat_id, cand_id;
+  DevBuf<int32_t> pair_q, pair_t;
+  DevBuf<WorkItem> items;
+  int rc = 0;
+
+  const int64_t *cells = nullptr;
+  if (idx->K) {
+    if (cells_in) {
+      cells = cells_in;
+    } else {
+      if ((rc = cells_b.alloc(npairs, st))) return cuda_fail(cudaGetLastError(), "alloc cells");
+      launch_probe(idx->coarseT, idx->K, idx->d, queries, nq, ma, cells_b.p, st);
+      ss.launches++;
+      cells = cells_b.p;
+    }
+  }
+  const float *lut = lut_in;
+  if (!lut) {
+    if (lut_b.alloc(npairs * m * 16, st)) return cuda_fail(cudaGetLastError(), "alloc lut");
+    launch_residual_lut(idx, queries, cells, nq, nslots, lut_b.p, st);
+    ss.launches++;
+    lut = lut_b.p;
+  }
+  if (qmax_b.alloc(nq, st) || qt_b.alloc(npairs * m * 4, st) || qmin_f.alloc(npairs, st) ||
+      delta_f.alloc(npairs, st) || M_bits.alloc(nq, st) || fsat_n.alloc(nq, st) ||
+      fsat_mid.alloc((int64_t)nq * R, st) || fsat_id.alloc((int64_t)nq * R, st) ||
+      hist.alloc((int64_t)nq * kHistBins, st) || hist_w.alloc(nq, st) || cand_n.alloc(nq, st) ||
+      cand_mid.alloc((int64_t)nq * cap_g, st) || cand_id.alloc((int64_t)nq * cap_g, st) ||
+      pair_q.alloc(npairs, st) || pair_t.alloc(npairs, st) || n_items.alloc(1, st) ||
+      counter.alloc(1, st) || scratch.alloc(6 * (int64_t)nl + 8, st) || overflow.alloc(nq, st))
+    return cuda_fail(cudaGetLastError(), "alloc workspace");
+
+  launch_qmax(idx, lut, cells, nq, nslots, R, init, qmax_b.p, st);
+  launch_quantize(lut, (int)npairs, m, qmax_b.p, nslots, nullptr, nullptr, qt_b.p, qmin_f.p,
+                  delta_f.p, nullptr, nullptr, st);
+  launch_prefix(idx, qt_b.p, qmin_f.p, delta_f.p, cells, nq, nslots, R, init, M_bits.p, fsat_n.p,
+                fsat_mid.p, fsat_id.p, st);
+  k_init_bounds<<<gridn(nq), 256, 0, st>>>(M_bits.p, M_override, hist_w.p, nq);
+  ss.launches += 4;
+
+  // ---- work list ----
+  const int nsm = device_sms();
+  int64_t max_ranges = 0, sum_ranges = 0;
+  const int64_t avg_chunks = std::max<int64_t>(1, idx->total_chunks / std::max(nl, 1));
+  const int64_t work_chunks = ((npairs + qt_tile - 1) / qt_tile) * avg_chunks;
+  int64_t range_chunks = work_chunks / ((int64_t)nsm * 64);
+  int64_t rcp = 16;
+  while (rcp < range_chunks && rcp < 4096) rcp <<= 1;
+  range_chunks = rcp;
+  for (int L = 0; L < nl; L++) {
+    const int64_t nch = idx->h_chunk_off[L + 1] - idx->h_chunk_off[L];
+    const int64_t r = (nch + range_chunks - 1) / range_chunks;
+    max_ranges = std::max(max_ranges, r);
+    sum_ranges += r;
+  }
+  const int64_t max_items = (npairs / qt_tile + 1) * max_ranges + sum_ranges + 1;
+  if (items.alloc(max_items, st)) return cuda_fail(cudaGetLastError(), "alloc items");
+  build_work(idx, cells, nq, nslots, qt_tile, range_chunks, pair_q.p, pair_t.p, items.p, n_items.p,
+             scratch.p, max_items, st);
+  ss.launches += 4;
+
+  // ---- scan ----
+  cudaMemsetAsync(cand_n.p, 0, sizeof(unsigned) * nq, st);
+  cudaMemsetAsync(hist.p, 0, sizeof(unsigned) * (size_t)nq * kHistBins, st);
+  cudaMemsetAsync(counter.p, 0, sizeof(int), st);
+  ScanArgs a;
+  a.codes = idx->codes;
+  a.valid = idx->valid;
+  a.ids = idx->ids;
+  a.items = items.p;
+  a.n_items = n_items.p;
+  a.item_counter = counter.p;
+  a.pair_q = pair_q.p;
+  a.pair_t = pair_t.p;
+  a.qt = qt_b.p;
+  a.qmin_f = qmin_f.p;
+  a.delta_f = delta_f.p;
+  a.M_bits = M_bits.p;
+  a.cand_n = cand_n.p;
+  a.cand_mid = cand_mid.p;
+  a.cand_id = cand_id.p;
+  a.hist = hist.p;
+  a.hist_w = hist_w.p;
+  a.cap_g = cap_g;
+  a.cap_l = (std::max(R + 256, 384) + 31) / 32 * 32;
+  a.m = m;
+  a.R = R;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  launch_scan(a, nsm, st);
+  cudaEventRecord(e1, st);
+  ss.scan_launches++;
+  ss.launches++;
+  launch_select(nq, R, M_bits.p, cand_n.p, cand_mid.p, cand_id.p, cap_g, fsat_n.p, fsat_mid.p,
+                fsat_id.p, out_ids, out_d, out_n, overflow.p, st);
+  ss.launches++;
+  QADC_CUDA(cudaGetLastError());
+
+  // ---- overflow handling (rare: massive ties or very loose early bounds) ----
+  std::vector<int> h_over(nq);
+  std::vector<unsigned> h_cn(nq);
+  QADC_CUDA(cudaMemcpyAsync(h_over.data(), overflow.p, sizeof(int) * nq, cudaMemcpyDeviceToHost, st));
+  QADC_CUDA(cudaMemcpyAsync(h_cn.data(), cand_n.p, sizeof(unsigned) * nq, cudaMemcpyDeviceToHost, st));
+  QADC_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ss.scan_us += ms * 1e3;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  for (int q = 0; q < nq; q++) ss.cands += std::min<unsigned>(h_cn[q], (unsigned)cap_g);
+  std::vector<int> rerun, big;
+  unsigned need = 0;
+  for (int q = 0; q < nq; q++) {
+    if (!h_over[q]) continue;
+    if (h_cn[q] > (unsigned)cap_g) {
+      rerun.push_back(q);
+      need = std::max(need, h_cn[q]);
+    } else {
+      big.push_back(q);
+    }
+  }
+  for (int q : big) {
+    if ((rc = select_large(q, R, M_bits.p, cand_n.p, cand_mid.p, cand_id.p, cap_g, fsat_n.p,
+                           fsat_mid.p, fsat_id.p, out_ids, out_d, out_n, st)))
+      return rc;
+    ss.launches += 4;
+  }
+  if (!rerun.empty()) {
+    if (depth > 4) return arg_error("candidate capacity could not be satisfied");
+    ss.reruns += (int64_t)rerun.size();
+    const int nr = (int)rerun.size();
+    DevBuf<int> rows;
+    DevBuf<float> sub_q, sub_lut, sub_d;
+    DevBuf<int64_t> sub_cells, sub_ids;
+    DevBuf<unsigned> sub_M;
+    DevBuf<int32_t> sub_n;
+    if (rows.alloc(nr, st) || sub_q.alloc((int64_t)nr * idx->d, st) || sub_M.alloc(nr, st) ||
+        sub_ids.alloc((int64_t)nr * R, st) || sub_d.alloc((int64_t)nr * R, st) ||
+        sub_n.alloc(nr, st))
+      return cuda_fail(cudaGetLastError(), "alloc rerun");
+    QADC_CUDA(cudaMemcpyAsync(rows.p, rerun.data(), sizeof(int) * nr, cudaMemcpyHostToDevice, st));
+    k_gather_rows_f<<<gridn((int64_t)nr * idx->d), 256, 0, st>>>(queries, rows.p, nr, idx->d, sub_q.p);
+    k_gather_u<<<gridn(nr), 256, 0, st>>>(M_bits.p, rows.p, nr, sub_M.p);
+    const float *lp = nullptr;
+    const int64_t *cp = nullptr;
+    if (lut_in) {
+      if (sub_lut.alloc((int64_t)nr * nslots * m * 16, st)) return kErrCuda;
+      k_gather_rows_f<<<gridn((int64_t)nr * nslots * m * 16), 256, 0, st>>>(lut_in, rows.p, nr,
+                                                                          nslots * m * 16, sub_lut.p);
+      lp = sub_lut.p;
+    }
+    if (cells) {
+      if (sub_cells.alloc((int64_t)nr * nslots, st)) return kErrCuda;
+      k_gather_rows_i<<<gridn((int64_t)nr * nslots), 256, 0, st>>>(cells, rows.p, nr, nslots,
+                                                                   sub_cells.p);
+      cp = sub_cells.p;
+    }
+    const int cap2 = (int)std::min<int64_t>(std::max<int64_t>((int64_t)need + 1024, 2LL * cap_g),
+                                            (int64_t)1 << 28);
+    rc = search_impl(idx, sub_q.p, nr, R, ma, init, lp, cp, sub_ids.p, sub_d.p, sub_n.p, st, ss,
+                     sub_M.p, cap2, depth + 1);
+    if (rc) return rc;
+    k_scatter_out<<<gridn((int64_t)nr * R), 256, 0, st>>>(sub_ids.p, sub_d.p, sub_n.p, rows.p, nr,
+                                                          R, out_ids, out_d, out_n);
+  }
+  QADC_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+}  // namespace
+}  // namespace qadc
+
+using namespace qadc;
+
+// ============================ Part 1 ============================
+
+extern "C" int qadc_simd_level(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    set_error("no CUDA device");
+    return -1;
+  }
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) {
+    set_error("device is not sm_100 (Blackwell B200)");
+    return -1;
+  }
+  return QADC_KERNEL_B200;
+}
+
+extern "C" const char *qadc_b200_last_error(void) { return g_err.c_str(); }
+
+namespace {
+template <class T>
+int upload(T **d, const T *h, int64_t n) {
+  QADC_CUDA(cudaMalloc(d, (size_t)std::max<int64_t>(n, 1) * sizeof(T)));
+  if (n > 0) QADC_CUDA(cudaMemcpy(*d, h, (size_t)n * sizeof(T), cudaMemcpyHostToDevice));
+  return kOk;
+}
+
+// Heap arrays leave in descending (dist, id) order: a valid max-heap layout
+// (heap.py:95-98 relies on the same fact).
+void write_heap_desc(const std::vector<float> &d, const std::vector<int64_t> &i, int n, float *hd,
+                     int64_t *hi) {
+  for (int k = 0; k < n; k++) {
+    hd[k] = d[n - 1 - k];
+    hi[k] = i[n - 1 - k];
+  }
+}
+
+int check_heap(int size, int R) {
+  if (R < 1) return arg_error("heap capacity must be positive");
+  if (size < 0 || size > R) return arg_error("heap size out of range");
+  return kOk;
+}
+}  // namespace
+
+extern "C" int adc_scan_f32(const uint8_t *codes, int64_t n, const int64_t *ids, int m, int b,
+                            const float *tables, float *hd, int64_t *hi, int size, int R) {
+  g_err.clear();
+  if (check_heap(size, R)) return -1;
+  if (b != 4 && b != 8 && b != 16) return (arg_error("b must be 4, 8 or 16"), -1);
+  if (m < 1 || m > QADC_MAX_M || (b == 4 && m % 2)) return (arg_error("unsupported m"), -1);
+  if (n <= 0) return size;
+  const int64_t row = b == 4 ? m / 2 : (b == 8 ? m : 2 * m);
+  uint8_t *dc = nullptr;
+  int64_t *di = nullptr, *dhi = nullptr, *oi = nullptr;
+  float *dt = nullptr, *dhd = nullptr, *od = nullptr;
+  int out = -1;
+  if (!upload(&dc, codes, n * row) && !upload(&di, ids, n) &&
+      !upload(&dt, tables, (int64_t)m << b) && !upload(&dhd, hd, size) && !upload(&dhi, hi, size) &&
+      cudaMalloc(&od, (size_t)R * 4) == cudaSuccess && cudaMalloc(&oi, (size_t)R * 8) == cudaSuccess) {
+    out = adc_f32_device(dc, n, di, m, b, dt, dhd, dhi, size, R, od, oi, 0);
+    if (out >= 0) {
+      std::vector<float> vd(out);
+      std::vector<int64_t> vi(out);
+      if (cudaMemcpy(vd.data(), od, out * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(vi.data(), oi, out * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cuda_fail(cudaGetLastError(), "adc_scan_f32 D2H");
+        out = -1;
+      } else {
+        write_heap_desc(vd, vi, out, hd, hi);
+      }
+    } else {
+      out = -1;
+    }
+  }
+  cudaFree(dc); cudaFree(di); cudaFree(dt); cudaFree(dhd); cudaFree(dhi); cudaFree(od); cudaFree(oi);
+  return out;
+}
+
+extern "C" int qadc_scan_u8(const uint8_t *blocks, int64_t nblocks, const int64_t *ids, int mrows,
+                            const uint8_t *qt, float qmin, float delta, float *hd, int64_t *hi,
+                            int size, int R, int variant) {
+  g_err.clear();
+  (void)variant;
+  if (check_heap(size, R)) return -1;
+  if (mrows < 1 || 2 * mrows > QADC_MAX_M) return (arg_error("unsupported row count"), -1);
+  if (nblocks <= 0) return size;
+  uint8_t *db = nullptr, *dq = nullptr;
+  int64_t *di = nullptr, *dhi = nullptr, *oi = nullptr;
+  float *dhd = nullptr, *od = nullptr;
+  int out = -1;
+  if (!upload(&db, blocks, nblocks * mrows * 16) && !upload(&di, ids, nblocks * 16) &&
+      !upload(&dq, qt, (int64_t)mrows * 32) && !upload(&dhd, hd, size) && !upload(&dhi, hi, size) &&
+      cudaMalloc(&od, (size_t)R * 4) == cudaSuccess && cudaMalloc(&oi, (size_t)R * 8) == cudaSuccess) {
+    out = scan_u8_device(db, nblocks, di, mrows, dq, qmin, delta, dhd, dhi, size, R, od, oi, 0);
+    if (out >= 0) {
+      std::vector<float> vd(out);
+      std::vector<int64_t> vi(out);
+      if (cudaMemcpy(vd.data(), od, out * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(vi.data(), oi, out * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cuda_fail(cudaGetLastError(), "qadc_scan_u8 D2H");
+        out = -1;
+      } else {
+        write_heap_desc(vd, vi, out, hd, hi);
+      }
+    } else {
+      out = -1;
+    }
+  }
+  cudaFree(db); cudaFree(dq); cudaFree(di); cudaFree(dhd); cudaFree(dhi); cudaFree(od); cudaFree(oi);
+  return out;
+}
+
+extern "C" void qadc_block_dists(const uint8_t *blocks, int64_t nblocks, int mrows,
+                                 const uint8_t *qt, int per_block, uint8_t *out, int variant) {
+  g_err.clear();
+  (void)variant;
+  if (nblocks <= 0 || mrows < 1 || 2 * mrows > QADC_MAX_M) return;
+  uint8_t *db = nullptr, *dq = nullptr, *dout = nullptr;
+  const int64_t qn = per_block ? nblocks * mrows * 32 : (int64_t)mrows * 32;
+  if (!upload(&db, blocks, nblocks * mrows * 16) && !upload(&dq, qt, qn) &&
+      cudaMalloc(&dout, (size_t)nblocks * 16) == cudaSuccess) {
+    launch_block_dists(db, nblocks, mrows, dq, per_block, dout, 0);
+    if (cudaMemcpy(out, dout, (size_t)nblocks * 16, cudaMemcpyDeviceToHost) != cudaSuccess)
+      cuda_fail(cudaGetLastError(), "qadc_block_dists D2H");
+  }
+  cudaFree(db); cudaFree(dq); cudaFree(dout);
+}
+
+// ============================ Part 2 ============================
+
+namespace {
+int index_common(int d, int m, int nlists, const float *coarse, bool coarse_dev,
+                 const float *codebooks, const float *rotation, bool model_dev,
+                 const std::vector<int64_t> &lanes, const std::vector<int64_t> &count,
+                 qadc_b200_index *idx) {
+  if (d < 1 || m < 2 || m > QADC_MAX_M || m % 2 || d % m) return arg_error("invalid d / m geometry");
+  if (nlists < 1) return arg_error("index needs at least one list");
+  if (!coarse && nlists != 1) return arg_error("a flat index has exactly one list");
+  idx->d = d;
+  idx->m = m;
+  idx->dsub = d / m;
+  idx->nlists = nlists;
+  idx->K = coarse ? nlists : 0;
+  idx->h_lanes = lanes;
+  idx->h_count = count;
+  idx->h_chunk_off.assign(nlists + 1, 0);
+  for (int L = 0; L < nlists; L++) {
+    const int64_t nch = (lanes[L] + kChunkCodes - 1) / kChunkCodes;
+    idx->h_chunk_off[L + 1] = idx->h_chunk_off[L] + nch;
+    idx->max_list_chunks = std::max(idx->max_list_chunks, nch);
+  }
+  idx->total_chunks = idx->h_chunk_off[nlists];
+  const cudaMemcpyKind ck = coarse_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const cudaMemcpyKind mk = model_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (coarse) {
+    const size_t cb = (size_t)nlists * d * 4;
+    QADC_CUDA(cudaMalloc(&idx->coarse, cb));
+    QADC_CUDA(cudaMalloc(&idx->coarseT, cb));
+    QADC_CUDA(cudaMemcpy(idx->coarse, coarse, cb, ck));
+    k_transpose<<<gridn((int64_t)nlists * d), 256>>>(idx->coarse, nlists, d, idx->coarseT);
+    idx->bytes += 2 * (int64_t)cb;
+  }
+  const size_t bb = (size_t)m * 16 * (d / m) * 4;
+  QADC_CUDA(cudaMalloc(&idx->codebooks, bb));
+  QADC_CUDA(cudaMemcpy(idx->codebooks, codebooks, bb, mk));
+  if (rotation) {
+    QADC_CUDA(cudaMalloc(&idx->rotation, (size_t)d * d * 4));
+    QADC_CUDA(cudaMemcpy(idx->rotation, rotation, (size_t)d * d * 4, mk));
+  }
+  QADC_CUDA(cudaMalloc(&idx->chunk_off, (nlists + 1) * 8));
+  QADC_CUDA(cudaMalloc(&idx->lanes, nlists * 8));
+  QADC_CUDA(cudaMalloc(&idx->count, nlists * 8));
+  QADC_CUDA(cudaMemcpy(idx->chunk_off, idx->h_chunk_off.data(), (nlists + 1) * 8, cudaMemcpyHostToDevice));
+  QADC_CUDA(cudaMemcpy(idx->lanes, lanes.data(), nlists * 8, cudaMemcpyHostToDevice));
+  QADC_CUDA(cudaMemcpy(idx->count, count.data(), nlists * 8, cudaMemcpyHostToDevice));
+  return kOk;
+}
+}  // namespace
+
+extern "C" void qadc_b200_index_destroy(qadc_b200_index *idx) {
+  if (!idx) return;
+  cudaFree(idx->coarse); cudaFree(idx->coarseT); cudaFree(idx->codebooks); cudaFree(idx->rotation);
+  cudaFree(idx->codes); cudaFree(idx->valid); cudaFree(idx->ids); cudaFree(idx->chunk_list);
+  cudaFree(idx->chunk_off); cudaFree(idx->lanes); cudaFree(idx->count);
+  delete idx;
+}
+
+extern "C" int64_t qadc_b200_index_bytes(const qadc_b200_index *idx) { return idx ? idx->bytes : 0; }
+
+extern "C" int qadc_b200_index_create(int d, int m, int nlists, const float *coarse,
+                                      const uint8_t *blocks, const int64_t *blk_off,
+                                      const int64_t *ids, const int64_t *count,
+                                      const float *codebooks, const float *rotation,
+                                      qadc_b200_index **out) {
+  g_err.clear();
+  if (!out || !blk_off || !count || !codebooks) return arg_error("null argument");
+  *out = nullptr;
+  std::vector<int64_t> lanes(nlists > 0 ? nlists : 0), cnt(nlists > 0 ? nlists : 0);
+  for (int L = 0; L < nlists; L++) {
+    lanes[L] = 16 * (blk_off[L + 1] - blk_off[L]);
+    cnt[L] = count[L];
+    if (lanes[L] < 0 || cnt[L] < 0 || cnt[L] > lanes[L]) return arg_error("invalid list geometry");
+  }
+  qadc_b200_index *idx = new qadc_b200_index();
+  int rc = index_common(d, m, nlists, coarse, false, codebooks, rotation, false, lanes, cnt, idx);
+  uint8_t *db = nullptr;
+  int64_t *doff = nullptr, *dids = nullptr;
+  const int64_t nb = nlists > 0 ? blk_off[nlists] : 0;
+  if (!rc) rc = upload(&db, blocks, nb * (m / 2) * 16);
+  if (!rc) rc = upload(&doff, blk_off, (int64_t)nlists + 1);
+  if (!rc) rc = upload(&dids, ids, nb * 16);
+  if (!rc) rc = pack_from_blocks(idx, db, doff, dids, 0);
+  if (!rc) rc = cudaDeviceSynchronize() == cudaSuccess ? kOk : cuda_fail(cudaGetLastError(), "pack");
+  cudaFree(db);
+  cudaFree(doff);
+  cudaFree(dids);
+  if (rc) {
+    qadc_b200_index_destroy(idx);
+    return rc;
+  }
+  *out = idx;
+  return kOk;
+}
+
+extern "C" int qadc_b200_index_create_device(int d, int m, int nlists, const float *coarse,
+                                             const uint8_t *codes, const int64_t *row_off,
+                                             const int64_t *ids, const float *codebooks,
+                                             const float *rotation, qadc_b200_index **out) {
+  g_err.clear();
+  if (!out || !row_off || !codebooks) return arg_error("null argument");
+  *out = nullptr;
+  if (nlists < 1) return arg_error("index needs at least one list");
+  std::vector<int64_t> h_off(nlists + 1);
+  QADC_CUDA(cudaMemcpy(h_off.data(), row_off, (nlists + 1) * 8, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> lanes(nlists), cnt(nlists);
+  for (int L = 0; L < nlists; L++) {
+    lanes[L] = cnt[L] = h_off[L + 1] - h_off[L];
+    if (lanes[L] < 0) return arg_error("row offsets must be non-decreasing");
+  }
+  qadc_b200_index *idx = new qadc_b200_index();
+  int rc = index_common(d, m, nlists, coarse, true, codebooks, rotation, true, lanes, cnt, idx);
+  if (!rc) rc = pack_from_rows(idx, codes, row_off, ids, 0);
+  if (!rc) rc = cudaDeviceSynchronize() == cudaSuccess ? kOk : cuda_fail(cudaGetLastError(), "pack");
+  if (rc) {
+    qadc_b200_index_destroy(idx);
+    return rc;
+  }
+  *out = idx;
+  return kOk;
+}
+
+extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries, int nq, int R,
+                                      int ma, int init, unsigned flags, const float *lut_in,
+                                      const int64_t *cells_in, int64_t *out_ids, float *out_d,
+                                      int32_t *out_n, void *stream, int64_t *stats) {
+  g_err.clear();
+  if (!idx) return arg_error("null index");
+  if (R < 1) return arg_error("R must be positive");
+  if (init < 1) return arg_error("init must be positive");
+  if (nq < 0) return arg_error("nq must be non-negative");
+  if (idx->K) {
+    if (ma < 1) return arg_error("ma must be positive");
+    if (ma > idx->K) return arg_error("ma exceeds the cell count K");
+  }
+  if ((flags & QADC_B200_LUT_IN) && (!lut_in || (idx->K && !cells_in)))
+    return arg_error("LUT injection needs lut_in (and cells_in for an IVF index)");
+  if (R > 1 << 20) return arg_error("R too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nslots = idx->K ? ma : 1;
+  const bool host = flags & QADC_B200_HOST_IO;
+  DevBuf<float> dq, dd, dl;
+  DevBuf<int64_t> di, dc;
+  DevBuf<int32_t> dn;
+  const float *q = queries, *lin = (flags & QADC_B200_LUT_IN) ? lut_in : nullptr;
+  const int64_t *cin = (flags & QADC_B200_LUT_IN) ? cells_in : nullptr;
+  int64_t *oi = out_ids;
+  float *od = out_d;
+  int32_t *on = out_n;
+  if (host) {
+    if (dq.alloc((int64_t)nq * idx->d, st) || di.alloc((int64_t)nq * R, st) ||
+        dd.alloc((int64_t)nq * R, st) || dn.alloc(nq, st))
+      return cuda_fail(cudaGetLastError(), "alloc host io");
+    QADC_CUDA(cudaMemcpyAsync(dq.p, queries, (size_t)nq * idx->d * 4, cudaMemcpyHostToDevice, st));
+    q = dq.p;
+    if (lin) {
+      if (dl.alloc((int64_t)nq * nslots * idx->m * 16, st)) return kErrCuda;
+      QADC_CUDA(cudaMemcpyAsync(dl.p, lut_in, (size_t)nq * nslots * idx->m * 64, cudaMemcpyHostToDevice, st));
+      lin = dl.p;
+      if (cin) {
+        if (dc.alloc((int64_t)nq * nslots, st)) return kErrCuda;
+        QADC_CUDA(cudaMemcpyAsync(dc.p, cells_in, (size_t)nq * nslots * 8, cudaMemcpyHostToDevice, st));
+        cin = dc.p;
+      }
+    }
+    oi = di.p;
+    od = dd.p;
+    on = dn.p;
+  }
+  SearchStats ss;
+  const int cap_g = (int)std::min<int64_t>(std::max<int64_t>(8192, 8LL * R), 1 << 20);
+  int rc = search_impl(idx, q, nq, R, ma, init, lin, cin, oi, od, on, st, ss, nullptr, cap_g, 0);
+  if (rc) return rc;
+  if (host) {
+    QADC_CUDA(cudaMemcpyAsync(out_ids, oi, (size_t)nq * R * 8, cudaMemcpyDeviceToHost, st));
+    QADC_CUDA(cudaMemcpyAsync(out_d, od, (size_t)nq * R * 4, cudaMemcpyDeviceToHost, st));
+    QADC_CUDA(cudaMemcpyAsync(out_n, on, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
+    QADC_CUDA(cudaStreamSynchronize(st));
+  }
+  if (stats) {
+    stats[0] = 0;
+    stats[1] = ss.cands;
+    stats[2] = ss.reruns;
+    stats[3] = ss.scan_launches;
+    stats[4] = ss.launches;
+    stats[5] = (int64_t)llround(ss.scan_us);
+    stats[6] = 0;
+    stats[7] = 0;
+  }
+  return kOk;
+}
+
+extern "C" int qadc_b200_compute_tables(const float *codebooks, int m, int dsub, const float *y,
+                                        int npairs, float *out, void *stream) {
+  g_err.clear();
+  if (m < 1 || m > QADC_MAX_M || dsub < 1 || npairs < 0) return arg_error("invalid geometry");
+  launch_compute_tables(codebooks, m, dsub, y, npairs, out, (cudaStream_t)stream);
+  QADC_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+extern "C" int qadc_b200_probe(const float *coarse, int K, int d, const float *queries, int nq,
+                               int ma, int64_t *cells, float *residuals, void *stream) {
+  g_err.clear();
+  if (K < 1 || d < 1 || ma < 1 || ma > K || nq < 0) return arg_error("invalid probe geometry");
+  cudaStream_t st = (cudaStream_t)stream;
+  float *cT = nullptr;
+  QADC_CUDA(cudaMallocAsync(&cT, (size_t)K * d * 4, st));
+  k_transpose<<<gridn((int64_t)K * d), 256, 0, st>>>(coarse, K, d, cT);
+  launch_probe(cT, K, d, queries, nq, ma, cells, st);
+  cudaFreeAsync(cT, st);
+  if (residuals)
+    k_residuals<<<gridn((int64_t)nq * ma * d), 256, 0, st>>>(queries, coarse, cells, nq, ma, d,
+                                                             residuals);
+  QADC_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+extern "C" int qadc_b200_quantize_tables(const float *tables, int npairs, int m, const double *qmin,
+                                         const double *qmax, uint8_t *out, double *delta,
+                                         void *stream) {
+  g_err.clear();
+  if (m < 1 || m > QADC_MAX_M || npairs < 0) return arg_error("invalid geometry");
+  launch_quantize(tables, npairs, m, nullptr, 1, qmin, qmax, nullptr, nullptr, nullptr, delta, out,
+                  (cudaStream_t)stream);
+  QADC_CUDA(cudaGetLastError());
+  return kOk;
+}

@@ -1,0 +1,160 @@
+// GPU index build: PQ encoding and coarse assignment straight
+// into device memory, so billion-scale indexes never round-trip through
+// host NumPy. Semantics follow the reference's offline build:
+//   * kmeans.assign_batch broadcast path (kmeans.py:52-78, k*d <= 2^20):
+//     squared distances by einsum("nkd,nkd->nk") of diff = x - c, argmin
+//     with ties to the lowest index;
+//   * pq.encode_batch (pq.py:210-217): optional rotation x @ R^T, then the
+//     per-subspace argmin, packed two sub-codes per byte, low nibble =
+//     even sub-code (pq.py:90-105).
+// The rotation is accumulated in float64 (OpenBLAS's order is unpinned,
+// SURVEY A.7), and k*d > 2^20 coarse assignment uses the same einsum form
+// instead of the reference's clamped GEMM expansion.
+#include "qadc_b200.h"
+#include "internal.cuh"
+
+namespace qadc {
+namespace {
+
+__device__ __forceinline__ float sqdist_einsum(const float *__restrict__ a, const float *__restrict__ b,
+                                               int n) {
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  int i = 0;
+  for (; n - i >= 16; i += 16) {
+#pragma unroll
+    for (int v = 3; v >= 0; v--) {
+#pragma unroll
+      for (int l = 0; l < 4; l++) {
+        const float df = __fsub_rn(a[i + 4 * v + l], b[i + 4 * v + l]);
+        acc[l] = __fadd_rn(acc[l], __fmul_rn(df, df));
+      }
+    }
+  }
+  for (; i < n; i += 4) {
+#pragma unroll
+    for (int l = 0; l < 4; l++) {
+      float p = 0.f;
+      if (i + l < n) {
+        const float df = __fsub_rn(a[i + l], b[i + l]);
+        p = __fmul_rn(df, df);
+      }
+      acc[l] = __fadd_rn(acc[l], p);
+    }
+  }
+  return __fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3]));
+}
+
+// y = R x (float64 accumulation, one rounding), one CTA per 8 vectors.
+__global__ void k_rotate(const float *__restrict__ X, int64_t n, int d, const float *__restrict__ R,
+                         float *__restrict__ Y) {
+  extern __shared__ float sx[];  // 8 * d
+  const int64_t v0 = (int64_t)blockIdx.x * 8;
+  const int nv = (int)(n - v0 < 8 ? n - v0 : 8);
+  for (int t = threadIdx.x; t < nv * d; t += blockDim.x) sx[t] = X[v0 * d + t];
+  __syncthreads();
+  for (int t = threadIdx.x; t < nv * d; t += blockDim.x) {
+    const int v = t / d, i = t % d;
+    double acc = 0.0;
+    for (int k = 0; k < d; k++) acc += (double)R[(size_t)i * d + k] * (double)sx[v * d + k];
+    Y[(v0 + v) * d + i] = (float)acc;
+  }
+}
+
+// One thread per (vector, output byte): sub-quantizers 2b and 2b+1.
+__global__ void k_encode(const float *__restrict__ X, int64_t n, int m, int dsub,
+                         const float *__restrict__ codebooks, uint8_t *__restrict__ out) {
+  const int mrows = m / 2;
+  const int d = m * dsub;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * mrows;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / mrows;
+    const int b = (int)(t % mrows);
+    uint8_t byte = 0;
+    for (int h = 0; h < 2; h++) {
+      const int j = 2 * b + h;
+      const float *x = X + v * d + (size_t)j * dsub;
+      int best = 0;
+      float bd = 0.f;
+      for (int i = 0; i < 16; i++) {
+        const float dd = sqdist_einsum(x, codebooks + ((size_t)j * 16 + i) * dsub, dsub);
+        if (i == 0 || dd < bd) {
+          bd = dd;
+          best = i;
+        }
+      }
+      byte |= (uint8_t)(best << (4 * h));
+    }
+    out[t] = byte;
+  }
+}
+
+// Coarse assignment: 128 vectors per CTA staged in shared memory; every
+// thread walks all K centroids (rows read as warp-wide broadcasts).
+__global__ void __launch_bounds__(128) k_assign(const float *__restrict__ X, int64_t n, int d,
+                                                const float *__restrict__ C, int K,
+                                                int64_t *__restrict__ labels) {
+  extern __shared__ float sx[];  // 128 * d, row-major per vector
+  const int64_t v0 = (int64_t)blockIdx.x * 128;
+  const int nv = (int)(n - v0 < 128 ? n - v0 : 128);
+  for (int t = threadIdx.x; t < nv * d; t += blockDim.x) sx[t] = X[v0 * d + t];
+  __syncthreads();
+  if ((int)threadIdx.x >= nv) return;
+  const float *x = sx + (size_t)threadIdx.x * d;
+  int best = 0;
+  float bd = 0.f;
+  for (int k = 0; k < K; k++) {
+    // centroid first, query second: diff = x - c has the same magnitude
+    const float dd = sqdist_einsum(x, C + (size_t)k * d, d);
+    if (k == 0 || dd < bd) {
+      bd = dd;
+      best = k;
+    }
+  }
+  labels[v0 + threadIdx.x] = best;
+}
+
+}  // namespace
+}  // namespace qadc
+
+using namespace qadc;
+
+extern "C" int qadc_b200_encode(const float *X, int64_t n, int d, int m, const float *codebooks,
+                                const float *rotation, uint8_t *out, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  set_error("");
+  if (m < 2 || m % 2 || d % m || m > QADC_MAX_M || n < 0) {
+    set_error("invalid encode geometry");
+    return kErrArgs;
+  }
+  if (n == 0) return kOk;
+  const float *src = X;
+  float *rot = nullptr;
+  if (rotation) {
+    QADC_CUDA(cudaMallocAsync(&rot, (size_t)n * d * 4, st));
+    k_rotate<<<(unsigned)((n + 7) / 8), 256, (size_t)8 * d * 4, st>>>(X, n, d, rotation, rot);
+    src = rot;
+  }
+  const int64_t work = n * (m / 2);
+  const int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 64);
+  k_encode<<<grid, 256, 0, st>>>(src, n, m, d / m, codebooks, out);
+  if (rot) cudaFreeAsync(rot, st);
+  QADC_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+extern "C" int qadc_b200_assign(const float *X, int64_t n, int d, const float *C, int K,
+                                int64_t *labels, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  set_error("");
+  if (d < 1 || K < 1 || n < 0) {
+    set_error("invalid assign geometry");
+    return kErrArgs;
+  }
+  if (n == 0) return kOk;
+  const size_t smem = (size_t)128 * d * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_assign<<<(unsigned)((n + 127) / 128), 128, smem, st>>>(X, n, d, C, K, labels);
+  QADC_CUDA(cudaGetLastError());
+  return kOk;
+}

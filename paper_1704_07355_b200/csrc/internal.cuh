@@ -1,0 +1,154 @@
+// Internal declarations shared by the qadc_b200 translation units.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "qadc_common.cuh"
+
+// Device-resident index (the opaque qadc_b200_index of the C ABI).
+//
+// Data layout in HBM ("interleaved32"): every list is padded to whole
+// chunks of 256 codes; chunk g holds m x 32 uint32 words, word (j, o) =
+// 4-bit sub-code j of codes 8o..8o+7 of the chunk, code 8o+k at bits
+// 4k..4k+3. A warp reads one 128-byte row per sub-quantizer (coalesced)
+// and each word's low / high 16 bits are ready-made PRMT selectors for
+// four codes. valid[g][o] bit k flags code 8o+k as admissible (id >= 0).
+struct qadc_b200_index {
+  int d = 0, m = 0, dsub = 0, nlists = 0, K = 0;
+  int64_t total_chunks = 0;
+  int64_t max_list_chunks = 0;
+  float *coarse = nullptr;     // [K][d]
+  float *coarseT = nullptr;    // [d][K] (coalesced probe reads)
+  float *codebooks = nullptr;  // [m][16][dsub]
+  float *rotation = nullptr;   // [d][d] or null
+  uint32_t *codes = nullptr;   // [total_chunks][m][32]
+  uint8_t *valid = nullptr;    // [total_chunks][32]
+  int64_t *ids = nullptr;      // [total_chunks * 256], -1 padding
+  int32_t *chunk_list = nullptr;  // [total_chunks] owning list
+  int64_t *chunk_off = nullptr;   // [nlists + 1]
+  int64_t *lanes = nullptr;       // [nlists] lanes in layout (16 * nblocks)
+  int64_t *count = nullptr;       // [nlists] valid-code count (find_qmax prefix)
+  std::vector<int64_t> h_chunk_off, h_lanes, h_count;
+  int64_t bytes = 0;
+};
+
+namespace qadc {
+
+void set_error(const std::string &msg);
+int cuda_fail(cudaError_t e, const char *where);
+#define QADC_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);   \
+  } while (0)
+
+// ---- layout.cu ----
+int pack_from_blocks(qadc_b200_index *idx, const uint8_t *d_blocks,
+                     const int64_t *d_blk_off, const int64_t *d_ids,
+                     cudaStream_t st);
+int pack_from_rows(qadc_b200_index *idx, const uint8_t *d_rows,
+                   const int64_t *d_row_off, const int64_t *d_ids,
+                   cudaStream_t st);
+
+// ---- lut.cu ----
+void launch_compute_tables(const float *codebooks, int m, int dsub,
+                           const float *y, int npairs, float *out, cudaStream_t st);
+void launch_probe(const float *coarseT, int K, int d, const float *queries,
+                  int nq, int ma, int64_t *cells, cudaStream_t st);
+void launch_residual_lut(const qadc_b200_index *idx, const float *queries,
+                         const int64_t *cells, int nq, int nslots,
+                         float *lut, cudaStream_t st);
+void launch_qmax(const qadc_b200_index *idx, const float *lut,
+                 const int64_t *cells, int nq, int nslots, int R, int init,
+                 float *qmax, cudaStream_t st);
+void launch_quantize(const float *lut, int npairs, int m, const float *qmax_per_query,
+                     int nslots, const double *qmin_in, const double *qmax_in,
+                     uint32_t *qt, float *qmin_f, float *delta_f,
+                     double *delta_out, uint8_t *qt_bytes_out, cudaStream_t st);
+void launch_prefix(const qadc_b200_index *idx, const uint32_t *qt,
+                   const float *qmin_f, const float *delta_f,
+                   const int64_t *cells, int nq, int nslots, int R, int init,
+                   unsigned *M_bits, int *fsat_n, float *fsat_mid,
+                   int64_t *fsat_id, cudaStream_t st);
+
+// ---- scan.cu ----
+struct WorkItem {
+  int32_t list;
+  int32_t pair_begin;   // index into the list-grouped pair arrays
+  int32_t pair_count;   // <= QT
+  int32_t pad;
+  int64_t chunk_begin;  // absolute chunk index
+  int64_t chunk_end;
+};
+
+struct ScanArgs {
+  const uint32_t *codes;
+  const uint8_t *valid;
+  const int64_t *ids;
+  const WorkItem *items;
+  const int *n_items;
+  int *item_counter;
+  const int32_t *pair_q;   // grouped pairs: query index
+  const int32_t *pair_t;   // grouped pairs: table index (q * nslots + s)
+  const uint32_t *qt;      // [npairs][m][4] words
+  const float *qmin_f;     // [npairs]
+  const float *delta_f;    // [npairs]
+  unsigned *M_bits;        // [nq] running distance bound
+  unsigned *cand_n;        // [nq]
+  float *cand_mid;         // [nq][cap_g]
+  int64_t *cand_id;        // [nq][cap_g]
+  unsigned *hist;          // [nq][kHistBins] midpoint histogram of published candidates
+  const float *hist_w;     // [nq] bucket width (0 disables)
+  int cap_g;
+  int cap_l;               // per-warp per-query buffer capacity
+  int m;
+  int R;
+};
+
+constexpr int kHistBins = 1024;
+int scan_qt_per_cta(int m);
+void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st);
+// Work-list construction (device side): returns item upper bound.
+int64_t build_work(const qadc_b200_index *idx, const int64_t *cells, int nq,
+                   int nslots, int qt_tile, int64_t range_chunks,
+                   int32_t *pair_q, int32_t *pair_t, WorkItem *items,
+                   int *n_items, int *scratch_list_pairs, int64_t max_items,
+                   cudaStream_t st);
+
+// ---- select.cu ----
+int select_capacity();
+void launch_select(int nq, int R, const unsigned *M_bits, const unsigned *cand_n,
+                   const float *cand_mid, const int64_t *cand_id, int cap_g,
+                   const int *fsat_n, const float *fsat_mid, const int64_t *fsat_id,
+                   int64_t *out_ids, float *out_d, int32_t *out_n,
+                   int *overflow, cudaStream_t st);
+
+// ---- simple.cu (general-table engine, reference layout) ----
+void launch_block_dists(const uint8_t *blocks, int64_t nblocks, int mrows,
+                        const uint8_t *qt, int per_block, uint8_t *out,
+                        cudaStream_t st);
+// Exact top-R by (dist, id) of n (dist, id) pairs (device), pairs with
+// id == INT64_MAX are padding. Writes up to R results ascending to
+// out_d/out_i (device) and returns the count via *out_n (host).
+int topr_sorted(const float *d, const int64_t *id, int64_t n, int R, float *out_d,
+                int64_t *out_i, int *out_n, cudaStream_t st);
+// Reference-ABI scans on device buffers (simple.cu).
+int scan_u8_device(const uint8_t *blocks, int64_t nblocks, const int64_t *ids, int mrows,
+                   const uint8_t *qt, float qmin, float delta, const float *heap_d,
+                   const int64_t *heap_i, int size, int R, float *out_d, int64_t *out_i,
+                   cudaStream_t st);
+int adc_f32_device(const uint8_t *codes, int64_t n, const int64_t *ids, int m, int b,
+                   const float *tables, const float *heap_d, const int64_t *heap_i, int size,
+                   int R, float *out_d, int64_t *out_i, cudaStream_t st);
+// Large-candidate fallback for search_batch queries that overflowed the
+// shared-memory select (massive ties): exact top-R via device radix sort.
+int select_large(int q, int R, const unsigned *M_bits, const unsigned *cand_n,
+                 const float *cand_mid, const int64_t *cand_id, int cap_g, const int *fsat_n,
+                 const float *fsat_mid, const int64_t *fsat_id, int64_t *out_ids, float *out_d,
+                 int32_t *out_n, cudaStream_t st);
+
+}  // namespace qadc

@@ -1,0 +1,518 @@
+// Index + Tables phases of adc.py:114-187 (qadc branch), batched over
+// queries: coarse probe, residual, rotation, float LUT, qmax, quantized
+// LUT, and the per-query prefix facts (first-R-valid saturated lanes and
+// the initial distance bound). Paths relative to /root/reference/pkg/src/qadc/.
+#include <cfloat>
+
+#include "internal.cuh"
+
+namespace qadc {
+namespace {
+
+// NumPy float32 einsum("d,d->") of diff = a - b (adc.py:72-73,
+// ivf.py:178-179): 4 lanes, product rounded then added (no FMA); blocks of
+// 16 folded as v3, v2, v1, v0; tail in zero-padded 4-vectors; lanes reduce
+// (l0 + l1) + (l2 + l3). Matches oracle/qadc_oracle.c orc_einsum_sqdist.
+template <class FA>
+__device__ __forceinline__ float einsum_sq(FA a, const float *__restrict__ b, int n) {
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  int i = 0;
+  for (; n - i >= 16; i += 16) {
+#pragma unroll
+    for (int v = 3; v >= 0; v--) {
+#pragma unroll
+      for (int l = 0; l < 4; l++) {
+        const float df = __fsub_rn(a(i + 4 * v + l), b[i + 4 * v + l]);
+        acc[l] = __fadd_rn(acc[l], __fmul_rn(df, df));
+      }
+    }
+  }
+  for (; i < n; i += 4) {
+#pragma unroll
+    for (int l = 0; l < 4; l++) {
+      float p = 0.f;
+      if (i + l < n) {
+        const float df = __fsub_rn(a(i + l), b[i + l]);
+        p = __fmul_rn(df, df);
+      }
+      acc[l] = __fadd_rn(acc[l], p);
+    }
+  }
+  return __fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3]));
+}
+
+// NumPy float32 pairwise sum for n <= 128 (find_qmax empty-cell bound,
+// qadc.py:192-193).
+__device__ float pairwise_sum(const float *x, int n) {
+  if (n < 8) {
+    float r = 0.f;
+    for (int i = 0; i < n; i++) r = __fadd_rn(r, x[i]);
+    return r;
+  }
+  float r[8];
+  for (int j = 0; j < 8; j++) r[j] = x[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; j++) r[j] = __fadd_rn(r[j], x[i + j]);
+  float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                        __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+  for (; i < n; i++) res = __fadd_rn(res, x[i]);
+  return res;
+}
+
+// Nibble j of list-local code k in the interleaved32 layout.
+__device__ __forceinline__ int code_nibble(const uint32_t *__restrict__ codes, int m,
+                                           int64_t chunk0, int64_t k, int j) {
+  const int64_t g = chunk0 + k / kChunkCodes;
+  const int o = (int)((k % kChunkCodes) >> 3);
+  const uint32_t w = codes[(g * m + j) * 32 + o];
+  return (w >> (4 * (k & 7))) & 15;
+}
+
+// ---------------- compute_tables (adc.py:61-75) ----------------
+__global__ void k_tables(const float *__restrict__ codebooks, int m, int dsub,
+                         const float *__restrict__ y, float *__restrict__ out) {
+  extern __shared__ float sy[];
+  const int d = m * dsub;
+  const float *yp = y + (size_t)blockIdx.x * d;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) sy[t] = yp[t];
+  __syncthreads();
+  for (int e = threadIdx.x; e < m * 16; e += blockDim.x) {
+    const int j = e >> 4;
+    const float *cb = codebooks + (size_t)e * dsub;
+    out[(size_t)blockIdx.x * m * 16 + e] =
+        einsum_sq([&](int t) { return cb[t]; }, sy + (size_t)j * dsub, dsub);
+  }
+}
+
+// ---------------- probe (ivf.py:166-182) ----------------
+// One CTA per query. Coarse distances in einsum order from the transposed
+// centroid array (coalesced), keys (d2 bits << 32 | cell) so lexsort's
+// (d2, cell) order is plain u64 order (d2 >= 0). The ma smallest keys are
+// found per tile of up to 4096 cells by an MSB radix select in shared
+// memory, candidates of all tiles are merged by a final select, and the
+// winners are sorted.
+constexpr int kProbeTile = 4096;
+
+__device__ uint64_t block_kth_u64(const uint64_t *keys, int n, int k, unsigned *hist,
+                                  uint64_t *s_prefix, int *s_k) {
+  // returns the k-th smallest (1-based) key among keys[0..n)
+  if (threadIdx.x == 0) { *s_prefix = 0; *s_k = k; }
+  __syncthreads();
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const uint64_t prefix = *s_prefix;
+    const uint64_t hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t key = keys[i];
+      if ((key & hmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int kk = *s_k, dgt = 0;
+      for (; dgt < 256; dgt++) {
+        if ((int)hist[dgt] >= kk) break;
+        kk -= hist[dgt];
+      }
+      *s_k = kk;
+      *s_prefix = prefix | ((uint64_t)dgt << shift);
+    }
+    __syncthreads();
+  }
+  return *s_prefix;
+}
+
+__device__ void block_sort_u64(uint64_t *keys, int n_pow2) {
+  for (int k = 2; k <= n_pow2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t a = keys[i], b = keys[ixj];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) { keys[i] = b; keys[ixj] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) k_probe(const float *__restrict__ coarseT, int K, int d,
+                                               const float *__restrict__ queries, int ma,
+                                               int64_t *__restrict__ cells) {
+  extern __shared__ unsigned char smem[];
+  float *sq = (float *)smem;                                   // d
+  uint64_t *keys = (uint64_t *)(smem + ((d * 4 + 15) & ~15));  // kProbeTile
+  uint64_t *cand = keys + kProbeTile;                          // ntiles * ma (<= 16 * 64)
+  __shared__ unsigned hist[256];
+  __shared__ uint64_t s_prefix;
+  __shared__ int s_k, s_nc;
+  const int q = blockIdx.x;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) sq[t] = queries[(size_t)q * d + t];
+  if (threadIdx.x == 0) s_nc = 0;
+  __syncthreads();
+  for (int base = 0; base < K; base += kProbeTile) {
+    const int n = min(kProbeTile, K - base);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int k = base + i;
+      const float d2 = einsum_sq([&](int t) { return coarseT[(size_t)t * K + k]; }, sq, d);
+      keys[i] = ((uint64_t)__float_as_uint(d2) << 32) | (uint32_t)k;
+    }
+    __syncthreads();
+    const int take = min(ma, n);
+    const uint64_t kth = block_kth_u64(keys, n, take, hist, &s_prefix, &s_k);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      if (keys[i] <= kth) {
+        const int p = atomicAdd(&s_nc, 1);
+        cand[p] = keys[i];
+      }
+    }
+    __syncthreads();
+  }
+  // final: ma smallest among candidates (keys are unique)
+  const int nc = s_nc;
+  const uint64_t kth = block_kth_u64(cand, nc, ma, hist, &s_prefix, &s_k);
+  __syncthreads();
+  // gather winners into keys[0..ma), pad, sort
+  if (threadIdx.x == 0) s_nc = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < nc; i += blockDim.x)
+    if (cand[i] <= kth) keys[atomicAdd(&s_nc, 1)] = cand[i];
+  __syncthreads();
+  int p2 = 1;
+  while (p2 < ma) p2 <<= 1;
+  for (int i = ma + threadIdx.x; i < p2; i += blockDim.x) keys[i] = ~0ull;
+  __syncthreads();
+  block_sort_u64(keys, p2);
+  for (int i = threadIdx.x; i < ma; i += blockDim.x)
+    cells[(size_t)q * ma + i] = (int64_t)(keys[i] & 0xffffffffu);
+}
+
+// ---------------- residual + rotation + LUT (adc.py:108-111, 141-148,
+// ivf.py:181-182) ----------------
+// One CTA per (query, probe slot). residual = q - C[cell] in fp32; OPQ
+// rotation y = R r accumulated in float64 and rounded once (the reference
+// uses OpenBLAS sgemv whose order is unpinned: rotated
+// configs are "native OPQ" parity with counted bucket flips).
+__global__ void k_residual_lut(const float *__restrict__ queries, const float *__restrict__ coarse,
+                               const float *__restrict__ rotation,
+                               const float *__restrict__ codebooks, const int64_t *__restrict__ cells,
+                               int d, int m, int nslots, float *__restrict__ lut) {
+  extern __shared__ float sm[];
+  float *sr = sm, *sy = sm + d;
+  const int pair = blockIdx.x;
+  const int q = pair / nslots;
+  const float *qp = queries + (size_t)q * d;
+  if (coarse) {
+    const int64_t c = cells[pair];
+    for (int t = threadIdx.x; t < d; t += blockDim.x)
+      sr[t] = __fsub_rn(qp[t], coarse[(size_t)c * d + t]);
+  } else {
+    for (int t = threadIdx.x; t < d; t += blockDim.x) sr[t] = qp[t];
+  }
+  __syncthreads();
+  const float *y = sr;
+  if (rotation) {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      double acc = 0.0;
+      for (int k = 0; k < d; k++) acc += (double)rotation[(size_t)i * d + k] * (double)sr[k];
+      sy[i] = (float)acc;
+    }
+    __syncthreads();
+    y = sy;
+  }
+  const int dsub = d / m;
+  for (int e = threadIdx.x; e < m * 16; e += blockDim.x) {
+    const int j = e >> 4;
+    const float *cb = codebooks + (size_t)e * dsub;
+    lut[(size_t)pair * m * 16 + e] =
+        einsum_sq([&](int t) { return cb[t]; }, y + (size_t)j * dsub, dsub);
+  }
+}
+
+// ---------------- find_qmax (qadc.py:157-194, adc.py:170-172) ----------------
+// One CTA per query, first probed cell only. Each thread computes the fp32
+// left-to-right ADC of prefix codes (_pykernels.py:24-27 order: per byte j,
+// low nibble table 2j then high nibble table 2j+1), the block then selects
+// the min(R, take)-th smallest value by an MSB radix select on the bit
+// patterns (distances >= 0). Empty cell: NumPy pairwise sum of row maxima.
+__global__ void __launch_bounds__(256) k_qmax(const uint32_t *__restrict__ codes,
+                                              const int64_t *__restrict__ chunk_off,
+                                              const int64_t *__restrict__ count,
+                                              const float *__restrict__ lut,
+                                              const int64_t *__restrict__ cells, int m, int nslots,
+                                              int R, int init, unsigned *__restrict__ scratch,
+                                              float *__restrict__ qmax) {
+  extern __shared__ unsigned char smem[];
+  float *st = (float *)smem;  // m * 16
+  __shared__ unsigned hist[256];
+  __shared__ unsigned s_prefix;
+  __shared__ int s_k;
+  const int q = blockIdx.x;
+  const int pair = q * nslots;
+  const int64_t L = cells ? cells[pair] : 0;
+  for (int e = threadIdx.x; e < m * 16; e += blockDim.x) st[e] = lut[(size_t)pair * m * 16 + e];
+  __syncthreads();
+  const int64_t cnt = count[L];
+  const int take = (int)(cnt < (int64_t)init ? cnt : (int64_t)init);
+  if (take <= 0) {
+    if (threadIdx.x == 0) {
+      float mx[kMaxM];
+      for (int j = 0; j < m; j++) {
+        float v = st[j * 16];
+        for (int i = 1; i < 16; i++) v = fmaxf(v, st[j * 16 + i]);
+        mx[j] = v;
+      }
+      qmax[q] = pairwise_sum(mx, m);
+    }
+    return;
+  }
+  unsigned *keys = scratch + (size_t)q * init;
+  const int64_t c0 = chunk_off[L];
+  for (int k = threadIdx.x; k < take; k += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < m; j += 2) {
+      acc = __fadd_rn(acc, st[j * 16 + code_nibble(codes, m, c0, k, j)]);
+      acc = __fadd_rn(acc, st[(j + 1) * 16 + code_nibble(codes, m, c0, k, j + 1)]);
+    }
+    keys[k] = __float_as_uint(acc);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) { s_prefix = 0; s_k = min(R, take); }
+  __syncthreads();
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned prefix = s_prefix;
+    const unsigned hmask = shift == 24 ? 0u : (~0u << (shift + 8));
+    for (int i = threadIdx.x; i < take; i += blockDim.x) {
+      const unsigned key = keys[i];
+      if ((key & hmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int kk = s_k, dgt = 0;
+      for (; dgt < 256; dgt++) {
+        if ((int)hist[dgt] >= kk) break;
+        kk -= hist[dgt];
+      }
+      s_k = kk;
+      s_prefix = prefix | ((unsigned)dgt << shift);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) qmax[q] = __uint_as_float(s_prefix);
+}
+
+// ---------------- quantize_tables (qadc.py:124-147, adc.py:173-174) ----------------
+// One CTA (64 threads) per (query, slot). qmin = min(LUT min, qmax) and
+// delta = (qmax - qmin) / 127 in float64, bins floor((v - qmin) / delta)
+// clipped to 0..127 (delta == 0: v <= qmin -> 0 else 127). Emits the byte
+// tables as 4 words per sub-quantizer (entries 0-7 | 8-15), and the fp32
+// casts of qmin / delta the Cython boundary makes (_kernels.pyx:82-83).
+__global__ void k_quantize(const float *__restrict__ lut, int m,
+                           const float *__restrict__ qmax_q, int nslots,
+                           const double *__restrict__ qmin_in, const double *__restrict__ qmax_in,
+                           uint32_t *__restrict__ qt, float *__restrict__ qmin_f,
+                           float *__restrict__ delta_f, double *__restrict__ delta_out,
+                           uint8_t *__restrict__ qt_bytes) {
+  __shared__ float red[64];
+  const int pair = blockIdx.x;
+  const float *t = lut + (size_t)pair * m * 16;
+  double qmin, qmax;
+  if (qmin_in) {
+    qmin = qmin_in[pair];
+    qmax = qmax_in[pair];
+  } else {
+    float mn = FLT_MAX;
+    for (int e = threadIdx.x; e < m * 16; e += blockDim.x) mn = fminf(mn, t[e]);
+    red[threadIdx.x] = mn;
+    __syncthreads();
+    for (int s = 32; s > 0; s >>= 1) {
+      if ((int)threadIdx.x < s) red[threadIdx.x] = fminf(red[threadIdx.x], red[threadIdx.x + s]);
+      __syncthreads();
+    }
+    qmax = (double)qmax_q[pair / nslots];
+    qmin = fmin((double)red[0], qmax);
+  }
+  const double delta = __ddiv_rn(__dsub_rn(qmax, qmin), (double)kQuantBins);
+  for (int w = threadIdx.x; w < m * 4; w += blockDim.x) {
+    uint32_t word = 0;
+    for (int b = 0; b < 4; b++) {
+      const double v = (double)t[w * 4 + b];
+      double qq;
+      if (delta > 0) {
+        qq = floor(__ddiv_rn(__dsub_rn(v, qmin), delta));
+        qq = fmin(fmax(qq, 0.0), (double)kQuantBins);
+      } else {
+        qq = v <= qmin ? 0.0 : (double)kQuantBins;
+      }
+      const uint32_t byte = (uint32_t)qq;
+      word |= byte << (8 * b);
+      if (qt_bytes) qt_bytes[(size_t)pair * m * 16 + w * 4 + b] = (uint8_t)byte;
+    }
+    if (qt) qt[(size_t)pair * m * 4 + w] = word;
+  }
+  if (threadIdx.x == 0) {
+    if (qmin_f) qmin_f[pair] = __double2float_rn(qmin);
+    if (delta_f) delta_f[pair] = __double2float_rn(delta);
+    if (delta_out) delta_out[pair] = delta;
+  }
+}
+
+// ---------------- prefix facts per query ----------------
+// (1) F_sat: saturated lanes among the first R valid lanes of the global
+//     stream (cells in probe order, lanes in list order). The reference's
+//     heap admits every lane while below capacity and saturated lanes never
+//     afterwards (scan_kernels.c:279-308); the order-free equivalent keeps
+//     exactly these (_pykernels.py:80-83).
+// (2) Initial distance bound M: max midpoint of those first R valid lanes,
+//     tightened by the R-th smallest non-saturated midpoint among the
+//     first `init` codes of the first cell. Both are midpoints of members
+//     of the candidate set, so at least R candidates lie at or below M.
+__global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ codes,
+                                                const int64_t *__restrict__ chunk_off,
+                                                const int64_t *__restrict__ lanes,
+                                                const int64_t *__restrict__ ids,
+                                                const uint32_t *__restrict__ qt,
+                                                const float *__restrict__ qmin_f,
+                                                const float *__restrict__ delta_f,
+                                                const int64_t *__restrict__ cells, int m,
+                                                int nslots, int R, int init,
+                                                unsigned *__restrict__ M_bits, int *__restrict__ fsat_n,
+                                                float *__restrict__ fsat_mid,
+                                                int64_t *__restrict__ fsat_id) {
+  __shared__ unsigned char sqt[kMaxM * 16];
+  __shared__ int warp_cnt[8];
+  __shared__ unsigned hist[256];
+  __shared__ int s_seen, s_nsat;
+  __shared__ unsigned s_maxmid;
+  const int q = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { s_seen = 0; s_nsat = 0; s_maxmid = 0; }
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int s = 0; s < nslots; s++) {
+    const int pair = q * nslots + s;
+    const int64_t L = cells ? cells[pair] : 0;
+    const int64_t c0 = chunk_off[L], n = lanes[L];
+    const float qmin = qmin_f[pair], delta = delta_f[pair];
+    const int64_t pref = (s == 0) ? ((int64_t)init < n ? (int64_t)init : n) : 0;  // init prefix (cell 0)
+    for (int e = threadIdx.x; e < m * 4; e += blockDim.x)
+      ((uint32_t *)sqt)[e] = qt[(size_t)pair * m * 4 + e];
+    __syncthreads();
+    const int64_t need_end = pref;
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+      if (s_seen >= R && base >= need_end) break;
+      const int64_t k = base + threadIdx.x;
+      bool valid = false;
+      int qv = 255;
+      int64_t id = -1;
+      if (k < n) {
+        id = ids[c0 * kChunkCodes + k];
+        valid = id >= 0;
+        int acc = 0;
+        for (int j = 0; j < m; j++) acc += sqt[j * 16 + code_nibble(codes, m, c0, k, j)];
+        qv = min(acc, 255);
+      }
+      // block exclusive scan of valid flags -> stream rank
+      const unsigned bal = __ballot_sync(0xffffffffu, valid);
+      if (lane == 0) warp_cnt[wid] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+        if (w < wid) before += warp_cnt[w];
+        total += warp_cnt[w];
+      }
+      const int rank = s_seen + before + __popc(bal & ((1u << lane) - 1));
+      if (valid && rank < R) {
+        const float mid = midpoint(qmin, delta, qv);
+        atomicMax(&s_maxmid, fbits(mid));
+        if (qv == 255) {
+          const int p = atomicAdd(&s_nsat, 1);
+          fsat_mid[(size_t)q * R + p] = mid;
+          fsat_id[(size_t)q * R + p] = id;
+        }
+      }
+      if (valid && k < pref && qv < 255) atomicAdd(&hist[qv], 1u);
+      __syncthreads();
+      if (threadIdx.x == 0) s_seen += total;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = __int_as_float(0x7f800000);  // +inf
+    if (s_seen >= R) M = __uint_as_float(s_maxmid);
+    int cum = 0;
+    for (int t = 0; t < 255; t++) {
+      cum += hist[t];
+      if (cum >= R) {
+        const int pair0 = q * nslots;
+        M = fminf(M, midpoint(qmin_f[pair0], delta_f[pair0], t));
+        break;
+      }
+    }
+    M_bits[q] = fbits(M);
+    fsat_n[q] = s_nsat;
+  }
+}
+
+}  // namespace
+
+void launch_compute_tables(const float *codebooks, int m, int dsub, const float *y, int npairs,
+                           float *out, cudaStream_t st) {
+  if (npairs <= 0) return;
+  k_tables<<<npairs, 256, (size_t)m * dsub * 4, st>>>(codebooks, m, dsub, y, out);
+}
+
+void launch_probe(const float *coarseT, int K, int d, const float *queries, int nq, int ma,
+                  int64_t *cells, cudaStream_t st) {
+  if (nq <= 0) return;
+  const int ntiles = (K + kProbeTile - 1) / kProbeTile;
+  size_t smem = ((size_t)d * 4 + 15) / 16 * 16 + (size_t)kProbeTile * 8 + (size_t)ntiles * ma * 8;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_probe<<<nq, 512, smem, st>>>(coarseT, K, d, queries, ma, cells);
+}
+
+void launch_residual_lut(const qadc_b200_index *idx, const float *queries, const int64_t *cells,
+                         int nq, int nslots, float *lut, cudaStream_t st) {
+  if (nq <= 0) return;
+  k_residual_lut<<<nq * nslots, 256, (size_t)idx->d * 8, st>>>(
+      queries, idx->K ? idx->coarse : nullptr, idx->rotation, idx->codebooks, cells, idx->d,
+      idx->m, nslots, lut);
+}
+
+void launch_qmax(const qadc_b200_index *idx, const float *lut, const int64_t *cells, int nq,
+                 int nslots, int R, int init, float *qmax, cudaStream_t st) {
+  if (nq <= 0) return;
+  unsigned *scratch = nullptr;
+  cudaMallocAsync(&scratch, (size_t)nq * std::max(init, 1) * 4, st);
+  k_qmax<<<nq, 256, (size_t)idx->m * 64, st>>>(idx->codes, idx->chunk_off, idx->count, lut,
+                                               idx->K ? cells : nullptr, idx->m, nslots, R, init,
+                                               scratch, qmax);
+  cudaFreeAsync(scratch, st);
+}
+
+void launch_quantize(const float *lut, int npairs, int m, const float *qmax_per_query, int nslots,
+                     const double *qmin_in, const double *qmax_in, uint32_t *qt, float *qmin_f,
+                     float *delta_f, double *delta_out, uint8_t *qt_bytes_out, cudaStream_t st) {
+  if (npairs <= 0) return;
+  k_quantize<<<npairs, 64, 0, st>>>(lut, m, qmax_per_query, nslots, qmin_in, qmax_in, qt, qmin_f,
+                                    delta_f, delta_out, qt_bytes_out);
+}
+
+void launch_prefix(const qadc_b200_index *idx, const uint32_t *qt, const float *qmin_f,
+                   const float *delta_f, const int64_t *cells, int nq, int nslots, int R, int init,
+                   unsigned *M_bits, int *fsat_n, float *fsat_mid, int64_t *fsat_id,
+                   cudaStream_t st) {
+  if (nq <= 0) return;
+  k_prefix<<<nq, 256, 0, st>>>(idx->codes, idx->chunk_off, idx->lanes, idx->ids, qt, qmin_f,
+                               delta_f, idx->K ? cells : nullptr, idx->m, nslots, R, init, M_bits,
+                               fsat_n, fsat_mid, fsat_id);
+}
+
+}  // namespace qadc

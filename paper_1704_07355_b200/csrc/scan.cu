@@ -1,0 +1,492 @@
+// Scan phase of adc.py:114-187 (qadc branch), batched: the B200 analogue of
+// qadc_scan_u8 (scan_kernels.c:318-382) plus the bounded heap
+// (scan_kernels.c:22-74, 279-308), restructured for a GPU:
+//
+//  * one CTA = 4 warps works on a (list, query tile, chunk range) item
+//    pulled from a global counter (persistent grid, 148 SMs x occupancy);
+//  * a warp owns one 256-code chunk at a time, a lane one octet of codes;
+//    per sub-quantizer pair the lane turns its two code words into PRMT
+//    selectors once and reuses them for every query of the tile;
+//  * lookups: PRMT on the two register halves of a 16-entry byte table
+//    (entries <= 127, so PRMT's sign-replicate mode zeroes the wrong half),
+//    byte sums of two sub-quantizers (<= 254, carry-free), widened into
+//    16-bit lanes via acc_a = sum(s) and acc_o = sum(odd bytes of s):
+//    even lanes = acc_a - (acc_o << 8). The adds run on the FMA pipe
+//    (IMAD) and the lookups on the ALU pipe (PRMT) so both pipes issue;
+//  * exact lane distance min(255, sum) (scan_kernels.c:137-167);
+//  * selection: a lane survives if its sum is <= the tile's threshold for
+//    that query, derived from a running per-query distance bound M (a
+//    midpoint value with >= R candidates at or below it). Survivors go to
+//    per-warp shared-memory buffers; a full buffer is tightened to its
+//    R-th smallest value (which also lowers the global M with atomicMin)
+//    and compacted. At the end of the item survivors with midpoint <= M
+//    are appended to a per-query global candidate list; select.cu picks
+//    the exact top-R by (midpoint, id).
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace qadc {
+namespace {
+
+constexpr int kWarps = 4;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct Smem {
+  int item;
+  int pair_count;
+  int64_t chunk_begin;
+  int query[16];
+  float qmin[16];
+  float delta[16];
+  int thr[kWarps][16];
+  unsigned kbias[kWarps][16];
+  unsigned mc[kWarps][16];
+  int bn[kWarps][16];
+};
+
+__device__ __forceinline__ unsigned kbias_of(int thr) {
+  return (0x8000u - (unsigned)(thr + 1)) * 0x10001u;
+}
+
+// Every published candidate is counted in a per-query histogram of
+// midpoints (bucket b = floor(mid / w)). The R-th smallest bucket bounds
+// the R-th best candidate published so far: M = (b + 2) * w (one bucket
+// of slack absorbs fp32 rounding of the bucket index). This lets the
+// global bound converge to the true R-th best of everything scanned, not
+// just to the best per-warp local bound.
+__device__ __noinline__ void publish_bound(const ScanArgs &a, int query) {
+  const int lane = threadIdx.x & 31;
+  const float hw = a.hist_w[query];
+  if (!(hw > 0.f)) return;
+  const unsigned *h = a.hist + (size_t)query * kHistBins;
+  constexpr int per = kHistBins / 32;
+  unsigned c = 0;
+#pragma unroll 8
+  for (int i = 0; i < per; i++) c += *(volatile const unsigned *)&h[lane * per + i];
+  unsigned incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const unsigned R = (unsigned)a.R;
+  const unsigned hit = __ballot_sync(kFull, incl >= R);
+  if (!hit) return;
+  const int src = __ffs(hit) - 1;
+  if (lane == src) {
+    unsigned cum = incl - c;
+    int b = lane * per;
+    for (int i = 0; i < per; i++, b++) {
+      cum += *(volatile const unsigned *)&h[b];
+      if (cum >= R) break;
+    }
+    const float M = __fmul_rn((float)(b + 2), hw);
+    atomicMin(&a.M_bits[query], fbits(M));
+  }
+  __syncwarp();
+}
+
+// Global append of every buffered entry of (warp, q) whose midpoint is <=
+// the query's current bound; empties the buffer.
+__device__ __noinline__ void flush_buffer(const ScanArgs &a, Smem &s, uint32_t *buf, int w, int q) {
+  const int lane = threadIdx.x & 31;
+  const int n = s.bn[w][q];
+  const int query = s.query[q];
+  const float qmin = s.qmin[q], delta = s.delta[q];
+  const float Mg = __uint_as_float(*(volatile unsigned *)&a.M_bits[query]);
+  const float hw = a.hist_w[query];
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    bool keep = false;
+    float mid = 0.f;
+    uint32_t e = 0;
+    if (i < n) {
+      e = buf[i];
+      mid = midpoint(qmin, delta, (int)(e >> 24));
+      keep = mid <= Mg;
+    }
+    const unsigned bal = __ballot_sync(kFull, keep);
+    if (!bal) continue;
+    unsigned pos = 0;
+    if (lane == 0) pos = atomicAdd(&a.cand_n[query], (unsigned)__popc(bal));
+    pos = __shfl_sync(kFull, pos, 0);
+    if (keep) {
+      if (hw > 0.f) atomicAdd(&a.hist[(size_t)query * kHistBins + min((int)(mid / hw), kHistBins - 1)], 1u);
+      const unsigned slot = pos + __popc(bal & ((1u << lane) - 1));
+      if (slot < (unsigned)a.cap_g) {
+        const size_t o = (size_t)query * a.cap_g + slot;
+        a.cand_mid[o] = mid;
+        a.cand_id[o] = a.ids[s.chunk_begin * kChunkCodes + (e & 0xffffffu)];
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) s.bn[w][q] = 0;
+  __syncwarp();
+  if (n > 0) publish_bound(a, query);
+}
+
+// Tighten (warp, q)'s threshold to the R-th smallest buffered value and
+// drop entries above it. Requires bn >= R.
+__device__ __noinline__ void compact_buffer(const ScanArgs &a, Smem &s, uint32_t *buf, int w, int q) {
+  const int lane = threadIdx.x & 31;
+  const int n = s.bn[w][q];
+  // every buffered value is <= 254; n >= R, so the search is well founded
+  // even if the threshold dropped after some entries were buffered
+  int lo = 0, hi = 254;
+  while (lo < hi) {  // smallest t with count(value <= t) >= R
+    const int mid = (lo + hi) >> 1;
+    int c = 0;
+    for (int i = lane; i < n; i += 32) c += (int)(buf[i] >> 24) <= mid;
+    c = __reduce_add_sync(kFull, c);
+    if (c >= a.R) hi = mid; else lo = mid + 1;
+  }
+  const float qmin = s.qmin[q], delta = s.delta[q];
+  const float Mt = midpoint(qmin, delta, lo);
+  const int t_ext = q_threshold(Mt, qmin, delta);  // >= lo; covers midpoint ties
+  const int thr = min(s.thr[w][q], t_ext);
+  if (lane == 0) {
+    atomicMin(&a.M_bits[s.query[q]], fbits(Mt));
+    s.thr[w][q] = thr;
+    s.kbias[w][q] = kbias_of(thr);
+  }
+  int out = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    uint32_t e = 0;
+    bool keep = false;
+    if (i < n) {
+      e = buf[i];
+      keep = (int)(e >> 24) <= thr;
+    }
+    const unsigned bal = __ballot_sync(kFull, keep);
+    if (keep) buf[out + __popc(bal & ((1u << lane) - 1))] = e;
+    out += __popc(bal);
+  }
+  __syncwarp();
+  if (lane == 0) s.bn[w][q] = out;
+  __syncwarp();
+}
+
+// Append this lane's surviving codes (mask8 bit k = code 8*lane + k of the
+// chunk; byte k of vals = its lane distance) to (warp, q)'s buffer.
+__device__ __noinline__ void append(const ScanArgs &a, Smem &s, uint32_t *buf, int w, int q,
+                                    uint32_t mask8, uint32_t v0, uint32_t v1, int chunk_local) {
+  const int lane = threadIdx.x & 31;
+  int cnt = __popc(mask8);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int total = __shfl_sync(kFull, incl, 31);
+  int n = s.bn[w][q];
+  if (n + total > a.cap_l) {
+    if (n >= a.R) compact_buffer(a, s, buf, w, q);
+    // re-filter with the (possibly) tightened threshold
+    const int thr = s.thr[w][q];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int v = (int)(((k < 4 ? v0 : v1) >> (8 * (k & 3))) & 255);
+      if (v > thr) mask8 &= ~(1u << k);
+    }
+    cnt = __popc(mask8);
+    incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    total = __shfl_sync(kFull, incl, 31);
+    n = s.bn[w][q];
+    if (n + total > a.cap_l) {
+      flush_buffer(a, s, buf, w, q);
+      n = 0;
+    }
+  }
+  int off = n + incl - cnt;
+  const uint32_t base_idx = (uint32_t)chunk_local * kChunkCodes + 8u * lane;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    if (mask8 & (1u << k)) {
+      const uint32_t v = ((k < 4 ? v0 : v1) >> (8 * (k & 3))) & 255u;
+      buf[off++] = (v << 24) | (base_idx + k);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) s.bn[w][q] = n + total;
+  __syncwarp();
+}
+
+// Refresh each query's threshold from the global bound (lanes in parallel).
+__device__ __forceinline__ void refresh(const ScanArgs &a, Smem &s, int w, int nq_tile) {
+  const int lane = threadIdx.x & 31;
+  if (lane < nq_tile) {
+    const unsigned mb = *(volatile unsigned *)&a.M_bits[s.query[lane]];
+    if (mb != s.mc[w][lane]) {
+      s.mc[w][lane] = mb;
+      const int t = q_threshold(__uint_as_float(mb), s.qmin[lane], s.delta[lane]);
+      if (t < s.thr[w][lane]) {
+        s.thr[w][lane] = t;
+        s.kbias[w][lane] = kbias_of(t);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+template <int MC, int QT>
+__global__ void __launch_bounds__(kWarps * 32, 3) k_scan(ScanArgs a) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ Smem s;
+  const int m = MC ? MC : a.m;
+  uint4 *s_tab = (uint4 *)dsm;                                      // [QT][m]
+  uint32_t *s_buf = (uint32_t *)(dsm + (size_t)QT * m * 16);        // [W][QT][cap_l]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t *wbuf = s_buf + (size_t)w * QT * a.cap_l;
+  const uint32_t one = (uint32_t)(a.R > 0);  // runtime 1 (keeps IMAD on the FMA pipe)
+  const int n_items = *a.n_items;
+  for (;;) {
+    if (threadIdx.x == 0) s.item = atomicAdd(a.item_counter, 1);
+    __syncthreads();
+    const int item = s.item;
+    if (item >= n_items) break;
+    const WorkItem it = a.items[item];
+    // ---- stage the tile's byte tables and per-query state ----
+    for (int e = threadIdx.x; e < QT * m; e += blockDim.x) {
+      const int q = e / m, j = e - q * m;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (q < it.pair_count) {
+        const int t = a.pair_t[it.pair_begin + q];
+        v = ((const uint4 *)a.qt)[(size_t)t * m + j];
+      }
+      s_tab[e] = v;
+    }
+    if (threadIdx.x < QT) {
+      const int q = threadIdx.x;
+      int thr = -1;
+      unsigned mb = 0;
+      if (q < it.pair_count) {
+        const int pi = it.pair_begin + q;
+        const int query = a.pair_q[pi], t = a.pair_t[pi];
+        s.query[q] = query;
+        s.qmin[q] = a.qmin_f[t];
+        s.delta[q] = a.delta_f[t];
+        mb = *(volatile unsigned *)&a.M_bits[query];
+        thr = q_threshold(__uint_as_float(mb), s.qmin[q], s.delta[q]);
+      } else {
+        s.query[q] = 0;
+        s.qmin[q] = 0.f;
+        s.delta[q] = 0.f;
+      }
+      for (int ww = 0; ww < kWarps; ww++) {
+        s.thr[ww][q] = thr;
+        s.kbias[ww][q] = kbias_of(thr);
+        s.mc[ww][q] = mb;
+        s.bn[ww][q] = 0;
+      }
+    }
+    if (threadIdx.x == 0) {
+      s.pair_count = it.pair_count;
+      s.chunk_begin = it.chunk_begin;
+    }
+    __syncthreads();
+    const int nq_tile = s.pair_count;
+    // ---- warp loop over chunks ----
+    int iter = 0;
+    for (int64_t g = it.chunk_begin + w; g < it.chunk_end; g += kWarps, iter++) {
+      if ((iter & 3) == 3) refresh(a, s, w, nq_tile);
+      const uint32_t valid8 = a.valid[g * 32 + lane];
+      const uint32_t *cw = a.codes + (size_t)g * m * 32 + lane;
+      uint32_t acc_a[QT][2], acc_o[QT][2];
+#pragma unroll
+      for (int q = 0; q < QT; q++) acc_a[q][0] = acc_a[q][1] = acc_o[q][0] = acc_o[q][1] = 0;
+#pragma unroll(MC ? MC / 2 : 2)
+      for (int j = 0; j < m; j += 2) {
+        const uint32_t w0 = __ldg(cw + j * 32), w1 = __ldg(cw + (j + 1) * 32);
+        const uint32_t a0 = w0, a1 = w0 >> 16, a0x = w0 ^ 0x88888888u, a1x = a0x >> 16;
+        const uint32_t b0 = w1, b1 = w1 >> 16, b0x = w1 ^ 0x88888888u, b1x = b0x >> 16;
+#pragma unroll
+        for (int q = 0; q < QT; q++) {
+          const uint4 t = s_tab[q * m + j], u = s_tab[q * m + j + 1];
+          // codes 0-3 of the octet: sub-quantizers j and j+1, both halves
+          const uint32_t s0 = imad(prmt(t.x, t.y, a0), one,
+                              imad(prmt(t.z, t.w, a0x), one,
+                              imad(prmt(u.x, u.y, b0), one, prmt(u.z, u.w, b0x))));
+          // codes 4-7
+          const uint32_t s1 = imad(prmt(t.x, t.y, a1), one,
+                              imad(prmt(t.z, t.w, a1x), one,
+                              imad(prmt(u.x, u.y, b1), one, prmt(u.z, u.w, b1x))));
+          acc_a[q][0] = imad(s0, one, acc_a[q][0]);
+          acc_a[q][1] = imad(s1, one, acc_a[q][1]);
+          acc_o[q][0] = imad(prmt(s0, 0, 0x4341), one, acc_o[q][0]);
+          acc_o[q][1] = imad(prmt(s1, 0, 0x4341), one, acc_o[q][1]);
+        }
+      }
+      // ---- threshold test: 16-bit lanes, bit 15 clear <=> lane <= thr ----
+      const int chunk_local = (int)(g - it.chunk_begin);
+#pragma unroll
+      for (int q = 0; q < QT; q++) {
+        const unsigned kb = s.kbias[w][q];
+        uint32_t mask8 = 0, v[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const uint32_t O = acc_o[q][h];
+          const uint32_t E = acc_a[q][h] - (O << 8);
+          const uint32_t pe = ~(E + kb) & 0x80008000u;
+          const uint32_t po = ~(O + kb) & 0x80008000u;
+          mask8 |= (((pe >> 15) & 1u) | ((po >> 14) & 2u) | ((pe >> 29) & 4u) |
+                    ((po >> 28) & 8u)) << (4 * h);
+          v[h] = prmt(E, O, 0x6240);  // low bytes of lanes 0..3
+        }
+        mask8 &= valid8;
+        if (__any_sync(kFull, mask8 != 0)) append(a, s, wbuf + q * a.cap_l, w, q, mask8, v[0], v[1], chunk_local);
+      }
+    }
+    // ---- end of item: publish survivors ----
+    for (int q = 0; q < nq_tile; q++) flush_buffer(a, s, wbuf + q * a.cap_l, w, q);
+    __syncthreads();
+  }
+}
+
+template <int MC, int QT>
+void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
+  const int m = MC ? MC : a.m;
+  const size_t smem = (size_t)QT * m * 16 + (size_t)kWarps * QT * a.cap_l * 4;
+  cudaFuncSetAttribute(k_scan<MC, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan<MC, QT>, kWarps * 32, smem);
+  per_sm = std::max(per_sm, 1);
+  k_scan<MC, QT><<<nsm * per_sm, kWarps * 32, smem, st>>>(a);
+}
+
+// ---- work list construction ----
+
+__global__ void k_count_pairs(const int64_t *__restrict__ cells, int npairs, int *list_pairs) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x)
+    atomicAdd(&list_pairs[cells ? cells[i] : 0], 1);
+}
+
+// Single CTA: exclusive scans of pairs and items over the lists.
+__global__ void k_scan_lists(const int *__restrict__ list_pairs, const int64_t *__restrict__ chunk_off,
+                             int nlists, int qt_tile, int64_t range_chunks, int *pair_off,
+                             int64_t *item_off, int *n_items) {
+  __shared__ int64_t s_items[1024];
+  __shared__ int s_pairs[1024];
+  const int per = (nlists + blockDim.x - 1) / blockDim.x;
+  const int b = threadIdx.x * per, e = min(nlists, b + per);
+  int64_t it = 0;
+  int pr = 0;
+  for (int L = b; L < e; L++) {
+    const int p = list_pairs[L];
+    const int64_t nch = chunk_off[L + 1] - chunk_off[L];
+    const int64_t tiles = (p + qt_tile - 1) / qt_tile;
+    const int64_t ranges = (nch + range_chunks - 1) / range_chunks;
+    it += tiles * ranges;
+    pr += p;
+  }
+  s_items[threadIdx.x] = it;
+  s_pairs[threadIdx.x] = pr;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t ai = 0;
+    int ap = 0;
+    for (int t = 0; t < (int)blockDim.x; t++) {
+      const int64_t x = s_items[t];
+      const int y = s_pairs[t];
+      s_items[t] = ai;
+      s_pairs[t] = ap;
+      ai += x;
+      ap += y;
+    }
+    *n_items = (int)ai;
+  }
+  __syncthreads();
+  it = s_items[threadIdx.x];
+  pr = s_pairs[threadIdx.x];
+  for (int L = b; L < e; L++) {
+    const int p = list_pairs[L];
+    const int64_t nch = chunk_off[L + 1] - chunk_off[L];
+    item_off[L] = it;
+    pair_off[L] = pr;
+    it += ((p + qt_tile - 1) / qt_tile) * ((nch + range_chunks - 1) / range_chunks);
+    pr += p;
+  }
+}
+
+__global__ void k_scatter_pairs(const int64_t *__restrict__ cells, int npairs, int nslots,
+                                const int *__restrict__ pair_off, int *fill, int32_t *pair_q,
+                                int32_t *pair_t) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
+    const int L = cells ? (int)cells[i] : 0;
+    const int pos = pair_off[L] + atomicAdd(&fill[L], 1);
+    pair_q[pos] = i / nslots;
+    pair_t[pos] = i;
+  }
+}
+
+__global__ void k_emit_items(const int *__restrict__ list_pairs, const int *__restrict__ pair_off,
+                             const int64_t *__restrict__ item_off, const int64_t *__restrict__ chunk_off,
+                             int nlists, int qt_tile, int64_t range_chunks, WorkItem *items) {
+  for (int L = blockIdx.x * blockDim.x + threadIdx.x; L < nlists; L += gridDim.x * blockDim.x) {
+    const int p = list_pairs[L];
+    if (p == 0) continue;
+    const int64_t c0 = chunk_off[L], nch = chunk_off[L + 1] - c0;
+    if (nch == 0) continue;
+    const int tiles = (p + qt_tile - 1) / qt_tile;
+    const int64_t ranges = (nch + range_chunks - 1) / range_chunks;
+    int64_t o = item_off[L];
+    for (int64_t r = 0; r < ranges; r++) {
+      for (int t = 0; t < tiles; t++) {
+        WorkItem wi;
+        wi.list = L;
+        wi.pair_begin = pair_off[L] + t * qt_tile;
+        wi.pair_count = min(qt_tile, p - t * qt_tile);
+        wi.pad = 0;
+        wi.chunk_begin = c0 + r * range_chunks;
+        wi.chunk_end = min(c0 + nch, wi.chunk_begin + range_chunks);
+        items[o++] = wi;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+int scan_qt_per_cta(int m) { return m <= 64 ? 8 : 4; }
+
+void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st) {
+  const int qt = scan_qt_per_cta(a.m);
+  if (qt == 8) {
+    if (a.m == 16) launch_t<16, 8>(a, nsm, st);
+    else if (a.m == 32) launch_t<32, 8>(a, nsm, st);
+    else launch_t<0, 8>(a, nsm, st);
+  } else {
+    launch_t<0, 4>(a, nsm, st);
+  }
+}
+
+int64_t build_work(const qadc_b200_index *idx, const int64_t *cells, int nq, int nslots,
+                   int qt_tile, int64_t range_chunks, int32_t *pair_q, int32_t *pair_t,
+                   WorkItem *items, int *n_items, int *scratch, int64_t max_items,
+                   cudaStream_t st) {
+  (void)max_items;
+  const int nl = idx->nlists;
+  const int npairs = nq * nslots;
+  int *list_pairs = scratch, *pair_off = scratch + nl, *fill = scratch + 2 * nl;
+  int64_t *item_off = (int64_t *)(scratch + 4 * nl + 2);  // 8-byte aligned region
+  cudaMemsetAsync(list_pairs, 0, sizeof(int) * nl, st);
+  cudaMemsetAsync(fill, 0, sizeof(int) * nl, st);
+  const int g = std::min(std::max((npairs + 255) / 256, 1), 4096);
+  k_count_pairs<<<g, 256, 0, st>>>(cells, npairs, list_pairs);
+  k_scan_lists<<<1, 1024, 0, st>>>(list_pairs, idx->chunk_off, nl, qt_tile, range_chunks, pair_off,
+                                   item_off, n_items);
+  k_scatter_pairs<<<g, 256, 0, st>>>(cells, npairs, nslots, pair_off, fill, pair_q, pair_t);
+  k_emit_items<<<(nl + 127) / 128, 128, 0, st>>>(list_pairs, pair_off, item_off, idx->chunk_off,
+                                                 nl, qt_tile, range_chunks, items);
+  return 0;
+}
+
+}  // namespace qadc

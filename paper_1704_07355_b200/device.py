@@ -1,0 +1,145 @@
+"""Device-resident index and the batched search entry point.
+
+`DeviceIndex` owns a `qadc_b200_index` (include/qadc_b200.h): the coarse
+centroids, the product quantizer and every inverted list repacked into the
+interleaved32 HBM layout. It is built once from a reference-style index
+(`from_ivf`) or straight from codes already on the GPU (`from_device_rows`)
+and then answers whole query batches with `search`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+
+
+@dataclass
+class BatchResult:
+    ids: object  # (Q, R) int64, ascending (distance, id), -1 padding
+    distances: object  # (Q, R) float32 midpoints, +inf padding
+    counts: object  # (Q,) int32 results per query
+    stats: dict
+
+
+def _np(a, dtype):
+    return np.ascontiguousarray(np.asarray(a), dtype=dtype)
+
+
+class DeviceIndex:
+    def __init__(self, handle: int, d: int, m: int, K: int, nlists: int, ncodes: int):
+        self._h = handle
+        self.d, self.m, self.K, self.nlists, self.ncodes = d, m, K, nlists, ncodes
+
+    # ------------------------------------------------------------ building
+    @classmethod
+    def from_ivf(cls, index, pq) -> "DeviceIndex":
+        """Upload a reference-layout IvfIndex (+ its ProductQuantizer)."""
+        if (index.d, index.m, index.b) != (pq.m * pq.codebooks.shape[2], pq.m, pq.b):
+            raise ValueError("index geometry does not match the quantizer")
+        if index.b != 4:
+            raise ValueError("the B200 scan needs 4-bit sub-codes")
+        lib = _native.load_library()
+        blocks, ids, blk_off, count = [], [], [0], []
+        for lst in index.lists:
+            if hasattr(lst, "blocks"):
+                tb, ti, cnt = lst.blocks, lst.ids, lst.count
+            else:  # standard layout: regroup on the host (byte moves only)
+                from .qadc import transpose_list
+                t = transpose_list(lst.codes, lst.ids)
+                tb, ti, cnt = t.blocks, t.ids, t.count
+            blocks.append(_np(tb, np.uint8).reshape(-1))
+            ids.append(_np(ti, np.int64))
+            blk_off.append(blk_off[-1] + tb.shape[0])
+            count.append(cnt)
+        blocks = np.concatenate(blocks) if blocks else np.zeros(0, np.uint8)
+        ids = np.concatenate(ids) if ids else np.zeros(0, np.int64)
+        blk_off = np.asarray(blk_off, dtype=np.int64)
+        count = np.asarray(count, dtype=np.int64)
+        coarse = None if index.coarse is None else _np(index.coarse.centroids, np.float32)
+        cb = _np(pq.codebooks, np.float32)
+        rot = None if getattr(pq, "rotation", None) is None else _np(pq.rotation, np.float32)
+        h = ctypes.c_void_p()
+        _native.check(lib.qadc_b200_index_create(
+            index.d, index.m, len(index.lists), _native.ptr(coarse, ctypes.c_float),
+            _native.ptr(blocks, ctypes.c_uint8), _native.ptr(blk_off, ctypes.c_int64),
+            _native.ptr(ids, ctypes.c_int64), _native.ptr(count, ctypes.c_int64),
+            _native.ptr(cb, ctypes.c_float), _native.ptr(rot, ctypes.c_float),
+            ctypes.byref(h)), "index_create")
+        return cls(h.value, index.d, index.m, index.K, len(index.lists), int(count.sum()))
+
+    @classmethod
+    def from_device_rows(cls, d: int, m: int, codes, row_off, codebooks, rotation=None,
+                         coarse=None, ids=None) -> "DeviceIndex":
+        """Index from packed rows already on the GPU (torch tensors):
+        codes (n, m/2) uint8 in list order, row_off (nlists + 1) int64."""
+        lib = _native.load_library()
+        nl = row_off.shape[0] - 1
+        h = ctypes.c_void_p()
+        _native.check(lib.qadc_b200_index_create_device(
+            d, m, nl, _native.dptr(coarse), _native.dptr(codes), _native.dptr(row_off),
+            _native.dptr(ids), _native.dptr(codebooks), _native.dptr(rotation),
+            ctypes.byref(h)), "index_create_device")
+        return cls(h.value, d, m, 0 if coarse is None else nl, nl, int(codes.shape[0]))
+
+    # ------------------------------------------------------------ search
+    def search(self, queries, R: int, ma: int = 1, init: int = 1000, lut=None, cells=None,
+               stream=None) -> BatchResult:
+        """Batched Quick ADC search. `queries` is a (Q, d) float32 torch
+        tensor on the GPU (device I/O) or a numpy array (host I/O: the
+        host<->device copies happen inside the call). lut/cells inject the
+        float tables (Q, ma, m, 16) and probe order (Q, ma)."""
+        import torch
+
+        lib = _native.load_library()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        stats = np.zeros(8, dtype=np.int64)
+        flags = _native.LUT_IN if lut is not None else 0
+        if isinstance(queries, np.ndarray):
+            q = _np(queries, np.float32).reshape(-1, self.d)
+            nq = q.shape[0]
+            ids = np.empty((nq, R), np.int64)
+            dist = np.empty((nq, R), np.float32)
+            cnt = np.empty(nq, np.int32)
+            lut_h = None if lut is None else _np(lut, np.float32)
+            cells_h = None if cells is None else _np(cells, np.int64)
+            rc = lib.qadc_b200_search_batch(
+                self._h, q.ctypes.data, nq, R, ma, init, flags | _native.HOST_IO,
+                None if lut_h is None else lut_h.ctypes.data,
+                None if cells_h is None else cells_h.ctypes.data,
+                ids.ctypes.data, dist.ctypes.data, cnt.ctypes.data, st.cuda_stream,
+                stats.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+        else:
+            q = queries.to(dtype=torch.float32).contiguous()
+            nq = q.shape[0]
+            dev = q.device
+            ids = torch.empty((nq, R), dtype=torch.int64, device=dev)
+            dist = torch.empty((nq, R), dtype=torch.float32, device=dev)
+            cnt = torch.empty(nq, dtype=torch.int32, device=dev)
+            lut_d = None if lut is None else lut.to(dtype=torch.float32).contiguous()
+            cells_d = None if cells is None else cells.to(dtype=torch.int64).contiguous()
+            rc = lib.qadc_b200_search_batch(
+                self._h, _native.dptr(q), nq, R, ma, init, flags, _native.dptr(lut_d),
+                _native.dptr(cells_d), _native.dptr(ids), _native.dptr(dist), _native.dptr(cnt),
+                st.cuda_stream, stats.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+        _native.check(rc, "search_batch")
+        keys = ("codes", "candidates", "reruns", "scan_launches", "launches", "scan_us")
+        return BatchResult(ids, dist, cnt, {k: int(v) for k, v in zip(keys, stats)})
+
+    @property
+    def nbytes(self) -> int:
+        return int(_native.load_library().qadc_b200_index_bytes(self._h)) if self._h else 0
+
+    def close(self) -> None:
+        if self._h:
+            _native.load_library().qadc_b200_index_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
