@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Quick ADC search benchmark on B200 (BASELINE.json metric: codes scanned/s
+and QPS, with the scan kernel's roofline fraction).
+
+Workload (N=1 GPU): BASELINE configs[1] — exhaustive Quick ADC, d=128
+mixture data, m=32 x 4-bit codes, N=10^7 codes, Q=1000 batched queries,
+R=100, init=1000. One step = one search_batch pass of all Q queries over
+the whole index (LUT, qmax, quantize, scan, exact top-R).
+
+Multi-GPU (torchrun, one process per GPU, NCCL): weak scaling — every rank
+holds its own 10^7-code shard of one global list (ids rank*N + i) plus the
+replicated global prefix, scans it, and the per-rank top-R lists are merged
+(all_gather over NCCL, exact (distance, id) merge). value = all codes
+scanned by all ranks / max-over-ranks step time.
+
+`--impl reference` times the reference's own CPU implementation of the path
+on the host cores: the reference's compiled qadc_scan_u8 (oracle/_ref, built
+from /root/reference/pkg/src/qadc/src/scan_kernels.c) driven by the C
+restatement of adc.search's orchestration (oracle/), all host threads, on
+a bounded sample of queries over the same full index.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Quick ADC codes scanned/s (whole job) at configs[1]: exhaustive, m=32x4-bit, N=1e7/GPU, Q=1000, R=100"
+UNIT = "codes/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg3"])
+    p.add_argument("--n", type=int, default=None, help="codes per GPU (default: the config's N)")
+    p.add_argument("--queries", type=int, default=None)
+    p.add_argument("--cpu-seconds", type=float, default=12.0,
+                   help="target CPU work of the bounded reference sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """SM clock and throttle reasons sampled (NVML, every 20 ms) during the
+    timed region; falls back to nvidia-smi if NVML is unavailable."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.sm, self.mx, self.reasons = [], [], set()
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                self.mx.append(mx)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.reasons.update(v for k, v in self.REASONS.items() if r & k)
+                self._stop.wait(0.02)
+        except Exception:
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", f"--id={self.index}",
+                         "--query-gpu=clocks.sm,clocks.max.sm", "--format=csv,noheader,nounits"],
+                        capture_output=True, text=True, timeout=5).stdout.split(",")
+                    self.sm.append(float(out[0]))
+                    self.mx.append(float(out[1]))
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        time.sleep(0.05)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
+
+
+# ---------------------------------------------------------------- helpers
+
+def measured_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text())
+        except Exception:
+            pass
+    return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the scan kernel from the committed ncu
+    summary (profiles/), or None."""
+    f = ROOT / "profiles" / "scan_ncu_summary.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def merge_topr(ids, dists, R, world):
+    """Exact global top-R of per-rank (Q, R) lists by (distance, id):
+    all_gather over the process group, then a stable two-key sort."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return ids, dists
+    gi = [torch.empty_like(ids) for _ in range(world)]
+    gd = [torch.empty_like(dists) for _ in range(world)]
+    dist.all_gather(gi, ids)
+    dist.all_gather(gd, dists)
+    ai = torch.cat(gi, dim=1)
+    ad = torch.cat(gd, dim=1)
+    big = torch.iinfo(torch.int64).max
+    ai = torch.where(ai < 0, torch.full_like(ai, big), ai)
+    o = torch.argsort(ai, dim=1, stable=True)
+    ai, ad = torch.gather(ai, 1, o), torch.gather(ad, 1, o)
+    o = torch.argsort(ad, dim=1, stable=True)
+    ai, ad = torch.gather(ai, 1, o)[:, :R], torch.gather(ad, 1, o)[:, :R]
+    ai = torch.where(ai == big, torch.full_like(ai, -1), ai)
+    return ai, ad
+
+
+def cpu_reference_run(cfg, codes_np, n, qs, R, init, seconds, nthreads=None):
+    """The reference's own compiled qadc_scan_u8 (oracle/_ref), driven by the
+    restated adc.search orchestration (oracle/), on a bounded query sample;
+    returns (codes/s, sample description, kind, cores, results)."""
+    from oracle import oracle as orc
+    from paper_1704_07355_b200.qadc import transpose_list
+
+    tl = transpose_list(codes_np, np.arange(n, dtype=np.int64))
+    flat = (tl.blocks.reshape(-1), np.array([0, tl.blocks.shape[0]], np.int64), tl.ids,
+            np.array([n], np.int64))
+    use_ref = orc.ref_lib() is not None
+    kind = "reference" if use_ref else "port"
+    nthreads = nthreads or os.cpu_count() or 1
+    cb = np.load(Path(__file__).resolve().parent / "bench_data" / cfg.codebooks_file)
+    # calibrate: one query per thread
+    probe = qs[: max(1, min(nthreads, qs.shape[0]))]
+    t0 = time.perf_counter()
+    orc.search_batch(probe, cb, None, None, 1, flat, R, init, use_ref_scan=use_ref,
+                     nthreads=nthreads)
+    t1 = time.perf_counter()
+    per_query_wall = (t1 - t0) / probe.shape[0]
+    nq = int(max(probe.shape[0], min(qs.shape[0], seconds / max(per_query_wall, 1e-6))))
+    sample = qs[:nq]
+    t0 = time.perf_counter()
+    oi, od, on, _ = orc.search_batch(sample, cb, None, None, 1, flat, R, init,
+                                     use_ref_scan=use_ref, nthreads=nthreads)
+    wall = time.perf_counter() - t0
+    return (nq * n / wall, f"{nq} of {qs.shape[0]} queries over the full N={n} index",
+            kind, nthreads, (oi, od, on), wall)
+
+
+# ---------------------------------------------------------------- arms
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1704_07355_b200 import _native
+    from paper_1704_07355_b200.workload import CONFIGS, build_shard_index, load_pq, queries
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _native.require_device()
+    cfg = CONFIGS[args.config]
+    n = args.n or cfg.n
+    nq = args.queries or cfg.q
+    R, init = cfg.R, cfg.init
+    pq = load_pq(cfg)
+    index, codes = build_shard_index(cfg, pq, n, rank, world, prefix=max(init, R))
+    qs = queries(cfg, nq)
+    q_dev = torch.from_numpy(qs).cuda()
+    q_pin = torch.from_numpy(qs).pin_memory()
+    torch.cuda.synchronize()
+
+    def step_device():
+        res = index.search(q_dev, R, init=init, with_fsat=(rank == 0))
+        return merge_topr(res.ids, res.distances, R, world), res
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region ----
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    scan_us, launches, codes_scanned, cands, reruns = [], 0, 0, 0, 0
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            (gi, gd), res = step_device()
+            scan_us.append(res.stats["scan_us"])
+            launches += res.stats["launches"]
+            codes_scanned += res.stats["codes"]
+            cands += res.stats["candidates"]
+            reruns += res.stats["reruns"]
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_dev = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    # ---- end-to-end through the public API with host buffers ----
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e2.record(stream)
+    for _ in range(args.steps):
+        qd = q_pin.to("cuda", non_blocking=True)
+        res = index.search(qd, R, init=init, with_fsat=(rank == 0))
+        gi, gd = merge_topr(res.ids, res.distances, R, world)
+        out_i, out_d = gi.to("cpu"), gd.to("cpu")
+    e3.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = max_over_ranks(e2.elapsed_time(e3) / args.steps)
+
+    total_codes = nq * n * world
+    value = total_codes / (ms_dev * 1e-3)
+    e2e_value = total_codes / (ms_e2e * 1e-3)
+
+    # ---- roofline of the dominant kernel (the scan) ----
+    peak = np.zeros(2, np.float64)
+    _native.check(_native.load_library().qadc_b200_int_peak(
+        peak.ctypes.data_as(_native._f64p)), "int_peak")
+    scan_s = (sum(scan_us) / len(scan_us)) * 1e-6
+    lookups = (codes_scanned / args.steps) * pq.m  # per launch, this rank
+    achieved = lookups / scan_s / 1e9
+    pk = measured_peaks()
+    hbm_bytes = n * pq.m / 2  # codes read once per batch (exhaustive)
+    roof = {
+        "bound": "int",
+        "achieved": round(achieved, 2),
+        "peak": round(peak[0] / 1e9, 2),
+        "unit": "G lookup-adds/s vs measured G int lane-instr/s (PRMT+IMAD dual-pipe microbench)",
+        "frac": round(achieved / (peak[0] / 1e9), 4),
+        "traffic": ncu_traffic(),
+        "scan_kernel_ms": round(scan_s * 1e3, 3),
+        "alu_pipe_peak_G": round(peak[1] / 1e9, 2),
+        "hbm": {"bytes_alg_per_launch": int(hbm_bytes),
+                "achieved_gbs": round(hbm_bytes / scan_s / 1e9, 1),
+                "peak_gbs": pk.get("hbm_gbs"),
+                "frac": round(hbm_bytes / scan_s / 1e9 / pk.get("hbm_gbs", 6650.0), 4)},
+        "scan_share_of_step": round(scan_s * 1e3 / ms_dev, 3),
+    }
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (BASELINE mixture generator drawn on GPU; reference-trained PQ)",
+            "config": {"workload": cfg.name, "N_per_gpu": n, "N_total": n * world, "Q": nq,
+                       "R": R, "init": init, "m": pq.m, "d": pq.d,
+                       "l2": "inputs larger than L2 (codes %.0f MB > 126 MB)" % (n * pq.m / 2e6)},
+            "qps": nq / (ms_dev * 1e-3),
+            "e2e": {"value": e2e_value, "unit": UNIT, "qps": nq / (ms_e2e * 1e-3),
+                    "ms_per_step": ms_e2e, "h2d_bytes_per_step": int(nq * pq.d * 4),
+                    "d2h_bytes_per_step": int(nq * R * 12)},
+            "roofline": roof,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "candidates_per_query": cands / max(1, args.steps * nq),
+            "reruns": reruns,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            codes_np = codes.cpu().numpy()
+            v, sample, kind, cores, (oi, od, on), wall = cpu_reference_run(
+                cfg, codes_np, n, qs, R, init, args.cpu_seconds)
+            k = oi.shape[0]
+            gi_np, gd_np = out_i.numpy()[:k], out_d.numpy()[:k]
+            exact = int(sum(np.array_equal(gi_np[i], oi[i]) and
+                            np.array_equal(gd_np[i].view(np.uint32), od[i].view(np.uint32))
+                            for i in range(k)))
+            out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                                   "sample": sample, "seconds": round(wall, 2)}
+            out["parity_vs_cpu_reference"] = {"queries": k, "bit_exact": exact}
+    if world > 1:
+        dist.destroy_process_group()
+    return out
+
+
+def run_reference(args):
+    """CPU reference arm (see module docstring)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    from paper_1704_07355_b200.workload import CONFIGS, load_pq, queries
+
+    cfg = CONFIGS[args.config]
+    n = args.n or cfg.n
+    nq = args.queries or cfg.q
+    pq = load_pq(cfg)
+    # index construction is setup, not the timed path: encode on the GPU if
+    # one is visible (same index the B200 arm scans), else fail loudly
+    import torch
+
+    from paper_1704_07355_b200.workload import shard_codes
+    if not torch.cuda.is_available():
+        return {"impl": "reference", "unavailable": "index setup needs the GPU encoder"}
+    codes_np = shard_codes(cfg, pq, n, 0).cpu().numpy()
+    qs = queries(cfg, nq)
+    vals, walls = [], []
+    desc = kind = cores = None
+    per_step = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    for i in range(args.warmup + args.steps):
+        v, desc, kind, cores, _, wall = cpu_reference_run(cfg, codes_np, n, qs, cfg.R, cfg.init,
+                                                          per_step)
+        if i >= args.warmup:
+            vals.append(v)
+            walls.append(wall)
+    value = statistics.median(vals)
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(walls) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (BASELINE mixture generator; reference-trained PQ)",
+        "config": {"workload": cfg.name, "N_per_gpu": n, "Q": nq, "R": cfg.R, "init": cfg.init},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    out = run_reference(args) if args.impl == "reference" else run_b200(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -116,12 +116,29 @@ QADC_API int qadc_b200_index_create_device(int d, int m, int nlists,
 
 QADC_API void qadc_b200_index_destroy(qadc_b200_index *idx);
 
+/*
+ * Shard support: replace the index's prefix region — the codes
+ * find_qmax (qadc.py:157-194), the first-R-valid saturation rule and the
+ * initial bound read — by the GLOBAL first codes of each list, so a shard
+ * that scans only part of a list still reproduces the single-index
+ * semantics. rows (n, m/2) / row_off (nlists + 1) / ids (n or NULL) are
+ * device arrays like qadc_b200_index_create_device's; full_count (nlists,
+ * host) is each list's global code count.
+ */
+QADC_API int qadc_b200_index_set_prefix_device(qadc_b200_index *idx,
+                                               const uint8_t *rows,
+                                               const int64_t *row_off,
+                                               const int64_t *ids,
+                                               const int64_t *full_count);
+
 /* Device bytes held by the index (codes, ids, validity, centroids). */
 QADC_API int64_t qadc_b200_index_bytes(const qadc_b200_index *idx);
 
 /* Flags for qadc_b200_search_batch. */
 #define QADC_B200_HOST_IO 1u   /* queries / outputs are host pointers */
 #define QADC_B200_LUT_IN 2u    /* lut_in / cells_in supplied (device) */
+#define QADC_B200_NO_FSAT 4u   /* leave the saturated first-R lanes out (every
+                                  shard but the owner of the global prefix) */
 
 /*
  * adc.py:114-187 search(method="qadc") for nq queries at once:
@@ -174,6 +191,11 @@ QADC_API int qadc_b200_quantize_tables(const float *tables, int npairs, int m,
 QADC_API int qadc_b200_encode(const float *X, int64_t n, int d, int m,
                      const float *codebooks, const float *rotation,
                      uint8_t *out, void *stream);
+
+/* Integer issue-rate microbenchmark (roofline denominator R_int): out[0]
+ * = sustained PRMT+IMAD lane-instructions/s (both integer-capable pipes),
+ * out[1] = PRMT-only (ALU pipe) lane-instructions/s, on this device. */
+QADC_API int qadc_b200_int_peak(double *out);
 
 /* kmeans.py:52-78 assign_batch: nearest of K centroids (K, d) per row of
  * X (n, d), einsum-order distances, ties to the lowest index. */

@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libqadc_b200.so"
-SOURCES = ["layout.cu", "lut.cu", "scan.cu", "select.cu", "simple.cu", "encode.cu", "capi.cu"]
+SOURCES = ["layout.cu", "lut.cu", "scan.cu", "select.cu", "simple.cu", "encode.cu", "peak.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                      "-I" + str(ROOT / "include")]

@@ -21,6 +21,7 @@ QADC_KERNEL_B200 = 3
 MAX_M = 128
 HOST_IO = 1
 LUT_IN = 2
+NO_FSAT = 4
 
 _lib = None
 
@@ -73,6 +74,11 @@ def _bind(lib):
     lib.qadc_b200_assign.restype = c_int
     lib.qadc_b200_assign.argtypes = [c_void_p, c_int64, c_int, c_void_p, c_int, c_void_p,
                                      c_void_p]
+    lib.qadc_b200_index_set_prefix_device.restype = c_int
+    lib.qadc_b200_index_set_prefix_device.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p,
+                                                      _i64p]
+    lib.qadc_b200_int_peak.restype = c_int
+    lib.qadc_b200_int_peak.argtypes = [_f64p]
     return lib
 
 

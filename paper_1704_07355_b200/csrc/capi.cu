@@ -95,6 +95,17 @@ __global__ void k_residuals(const float *__restrict__ queries, const float *__re
   }
 }
 
+// SURVEY 8d "codes scanned" = sum over (query, probed list) of len(list).
+__global__ void k_count_codes(const int64_t *__restrict__ cells, int64_t npairs,
+                              const int64_t *__restrict__ lanes, unsigned long long *out) {
+  unsigned long long acc = 0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
+       p += (int64_t)gridDim.x * blockDim.x)
+    acc += (unsigned long long)lanes[cells ? cells[p] : 0];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 inline int gridn(int64_t n) {
   return (int)std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 148 * 16);
 }
@@ -122,7 +133,7 @@ struct SearchStats {
 int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int ma, int init,
                 const float *lut_in, const int64_t *cells_in, int64_t *out_ids, float *out_d,
                 int32_t *out_n, cudaStream_t st, SearchStats &ss, const unsigned *M_override,
-                int cap_g, int depth) {
+                int cap_g, int depth, bool no_fsat) {
   if (nq == 0) return kOk;
   const int m = idx->m;
   const int nslots = idx->K ? ma : 1;
@@ -135,6 +146,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   DevBuf<uint32_t> qt_b;
   DevBuf<unsigned> M_bits, cand_n, hist;
   DevBuf<int> fsat_n, n_items, counter, scratch, overflow;
+  DevBuf<unsigned long long> ncodes;
   DevBuf<int64_t> fsat_id, cand_id;
   DevBuf<int32_t> pair_q, pair_t;
   DevBuf<WorkItem> items;
@@ -161,10 +173,11 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   if (qmax_b.alloc(nq, st) || qt_b.alloc(npairs * m * 4, st) || qmin_f.alloc(npairs, st) ||
       delta_f.alloc(npairs, st) || M_bits.alloc(nq, st) || fsat_n.alloc(nq, st) ||
       fsat_mid.alloc((int64_t)nq * R, st) || fsat_id.alloc((int64_t)nq * R, st) ||
-      hist.alloc((int64_t)nq * kHistBins, st) || hist_w.alloc(nq, st) || cand_n.alloc(nq, st) ||
+      hist.alloc((int64_t)nq * kHistWords, st) || hist_w.alloc(nq, st) || cand_n.alloc(nq, st) ||
       cand_mid.alloc((int64_t)nq * cap_g, st) || cand_id.alloc((int64_t)nq * cap_g, st) ||
       pair_q.alloc(npairs, st) || pair_t.alloc(npairs, st) || n_items.alloc(1, st) ||
-      counter.alloc(1, st) || scratch.alloc(6 * (int64_t)nl + 8, st) || overflow.alloc(nq, st))
+      counter.alloc(1, st) || scratch.alloc(6 * (int64_t)nl + 8, st) || overflow.alloc(nq, st) ||
+      ncodes.alloc(1, st))
     return cuda_fail(cudaGetLastError(), "alloc workspace");
 
   launch_qmax(idx, lut, cells, nq, nslots, R, init, qmax_b.p, st);
@@ -174,15 +187,18 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
                 fsat_mid.p, fsat_id.p, st);
   k_init_bounds<<<gridn(nq), 256, 0, st>>>(M_bits.p, M_override, hist_w.p, nq);
   ss.launches += 4;
+  if (no_fsat) cudaMemsetAsync(fsat_n.p, 0, sizeof(int) * nq, st);
 
   // ---- work list ----
   const int nsm = device_sms();
   int64_t max_ranges = 0, sum_ranges = 0;
   const int64_t avg_chunks = std::max<int64_t>(1, idx->total_chunks / std::max(nl, 1));
   const int64_t work_chunks = ((npairs + qt_tile - 1) / qt_tile) * avg_chunks;
-  int64_t range_chunks = work_chunks / ((int64_t)nsm * 64);
+  // few, long items: each warp's local selection sees many codes before it
+  // publishes (about 3 items per resident CTA, 4 CTAs per SM)
+  int64_t range_chunks = work_chunks / ((int64_t)nsm * 12);
   int64_t rcp = 16;
-  while (rcp < range_chunks && rcp < 4096) rcp <<= 1;
+  while (rcp < range_chunks && rcp < 16384) rcp <<= 1;
   range_chunks = rcp;
   for (int L = 0; L < nl; L++) {
     const int64_t nch = idx->h_chunk_off[L + 1] - idx->h_chunk_off[L];
@@ -198,8 +214,10 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
 
   // ---- scan ----
   cudaMemsetAsync(cand_n.p, 0, sizeof(unsigned) * nq, st);
-  cudaMemsetAsync(hist.p, 0, sizeof(unsigned) * (size_t)nq * kHistBins, st);
+  cudaMemsetAsync(hist.p, 0, sizeof(unsigned) * (size_t)nq * kHistWords, st);
   cudaMemsetAsync(counter.p, 0, sizeof(int), st);
+  cudaMemsetAsync(ncodes.p, 0, sizeof(unsigned long long), st);
+  k_count_codes<<<gridn(npairs), 256, 0, st>>>(cells, npairs, idx->scan_count, ncodes.p);
   ScanArgs a;
   a.codes = idx->codes;
   a.valid = idx->valid;
@@ -219,7 +237,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   a.hist = hist.p;
   a.hist_w = hist_w.p;
   a.cap_g = cap_g;
-  a.cap_l = (std::max(R + 256, 384) + 31) / 32 * 32;
+  a.cap_l = (std::max(R + 128, 256) + 31) / 32 * 32;
   a.m = m;
   a.R = R;
   cudaEvent_t e0, e1;
@@ -240,7 +258,10 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   std::vector<unsigned> h_cn(nq);
   QADC_CUDA(cudaMemcpyAsync(h_over.data(), overflow.p, sizeof(int) * nq, cudaMemcpyDeviceToHost, st));
   QADC_CUDA(cudaMemcpyAsync(h_cn.data(), cand_n.p, sizeof(unsigned) * nq, cudaMemcpyDeviceToHost, st));
+  unsigned long long h_codes = 0;
+  QADC_CUDA(cudaMemcpyAsync(&h_codes, ncodes.p, sizeof(h_codes), cudaMemcpyDeviceToHost, st));
   QADC_CUDA(cudaStreamSynchronize(st));
+  if (depth == 0) ss.codes += (int64_t)h_codes;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   ss.scan_us += ms * 1e3;
@@ -297,7 +318,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
     const int cap2 = (int)std::min<int64_t>(std::max<int64_t>((int64_t)need + 1024, 2LL * cap_g),
                                             (int64_t)1 << 28);
     rc = search_impl(idx, sub_q.p, nr, R, ma, init, lp, cp, sub_ids.p, sub_d.p, sub_n.p, st, ss,
-                     sub_M.p, cap2, depth + 1);
+                     sub_M.p, cap2, depth + 1, no_fsat);
     if (rc) return rc;
     k_scatter_out<<<gridn((int64_t)nr * R), 256, 0, st>>>(sub_ids.p, sub_d.p, sub_n.p, rows.p, nr,
                                                           R, out_ids, out_d, out_n);
@@ -443,6 +464,14 @@ extern "C" void qadc_block_dists(const uint8_t *blocks, int64_t nblocks, int mro
 // ============================ Part 2 ============================
 
 namespace {
+void alias_prefix(qadc_b200_index *idx) {
+  idx->pcodes = idx->codes;
+  idx->pids = idx->ids;
+  idx->pchunk_off = idx->chunk_off;
+  idx->planes = idx->lanes;
+  idx->own_prefix = false;
+}
+
 int index_common(int d, int m, int nlists, const float *coarse, bool coarse_dev,
                  const float *codebooks, const float *rotation, bool model_dev,
                  const std::vector<int64_t> &lanes, const std::vector<int64_t> &count,
@@ -484,6 +513,8 @@ int index_common(int d, int m, int nlists, const float *coarse, bool coarse_dev,
   QADC_CUDA(cudaMalloc(&idx->chunk_off, (nlists + 1) * 8));
   QADC_CUDA(cudaMalloc(&idx->lanes, nlists * 8));
   QADC_CUDA(cudaMalloc(&idx->count, nlists * 8));
+  QADC_CUDA(cudaMalloc(&idx->scan_count, nlists * 8));
+  QADC_CUDA(cudaMemcpy(idx->scan_count, count.data(), nlists * 8, cudaMemcpyHostToDevice));
   QADC_CUDA(cudaMemcpy(idx->chunk_off, idx->h_chunk_off.data(), (nlists + 1) * 8, cudaMemcpyHostToDevice));
   QADC_CUDA(cudaMemcpy(idx->lanes, lanes.data(), nlists * 8, cudaMemcpyHostToDevice));
   QADC_CUDA(cudaMemcpy(idx->count, count.data(), nlists * 8, cudaMemcpyHostToDevice));
@@ -493,9 +524,12 @@ int index_common(int d, int m, int nlists, const float *coarse, bool coarse_dev,
 
 extern "C" void qadc_b200_index_destroy(qadc_b200_index *idx) {
   if (!idx) return;
+  if (idx->own_prefix) {
+    cudaFree(idx->pcodes); cudaFree(idx->pids); cudaFree(idx->pchunk_off); cudaFree(idx->planes);
+  }
   cudaFree(idx->coarse); cudaFree(idx->coarseT); cudaFree(idx->codebooks); cudaFree(idx->rotation);
   cudaFree(idx->codes); cudaFree(idx->valid); cudaFree(idx->ids); cudaFree(idx->chunk_list);
-  cudaFree(idx->chunk_off); cudaFree(idx->lanes); cudaFree(idx->count);
+  cudaFree(idx->chunk_off); cudaFree(idx->lanes); cudaFree(idx->count); cudaFree(idx->scan_count);
   delete idx;
 }
 
@@ -524,6 +558,7 @@ extern "C" int qadc_b200_index_create(int d, int m, int nlists, const float *coa
   if (!rc) rc = upload(&doff, blk_off, (int64_t)nlists + 1);
   if (!rc) rc = upload(&dids, ids, nb * 16);
   if (!rc) rc = pack_from_blocks(idx, db, doff, dids, 0);
+  if (!rc) alias_prefix(idx);
   if (!rc) rc = cudaDeviceSynchronize() == cudaSuccess ? kOk : cuda_fail(cudaGetLastError(), "pack");
   cudaFree(db);
   cudaFree(doff);
@@ -554,12 +589,59 @@ extern "C" int qadc_b200_index_create_device(int d, int m, int nlists, const flo
   qadc_b200_index *idx = new qadc_b200_index();
   int rc = index_common(d, m, nlists, coarse, true, codebooks, rotation, true, lanes, cnt, idx);
   if (!rc) rc = pack_from_rows(idx, codes, row_off, ids, 0);
+  if (!rc) alias_prefix(idx);
   if (!rc) rc = cudaDeviceSynchronize() == cudaSuccess ? kOk : cuda_fail(cudaGetLastError(), "pack");
   if (rc) {
     qadc_b200_index_destroy(idx);
     return rc;
   }
   *out = idx;
+  return kOk;
+}
+
+extern "C" int qadc_b200_index_set_prefix_device(qadc_b200_index *idx, const uint8_t *rows,
+                                                 const int64_t *row_off, const int64_t *ids,
+                                                 const int64_t *full_count) {
+  g_err.clear();
+  if (!idx || !row_off || !full_count) return arg_error("null argument");
+  const int nl = idx->nlists;
+  std::vector<int64_t> h_off(nl + 1);
+  QADC_CUDA(cudaMemcpy(h_off.data(), row_off, (nl + 1) * 8, cudaMemcpyDeviceToHost));
+  qadc_b200_index tmp;
+  tmp.d = idx->d;
+  tmp.m = idx->m;
+  tmp.nlists = nl;
+  std::vector<int64_t> lanes(nl);
+  tmp.h_chunk_off.assign(nl + 1, 0);
+  for (int L = 0; L < nl; L++) {
+    lanes[L] = h_off[L + 1] - h_off[L];
+    if (lanes[L] < 0) return arg_error("prefix row offsets must be non-decreasing");
+    if (full_count[L] < lanes[L]) return arg_error("prefix longer than the list");
+    tmp.h_chunk_off[L + 1] = tmp.h_chunk_off[L] + (lanes[L] + kChunkCodes - 1) / kChunkCodes;
+  }
+  tmp.total_chunks = tmp.h_chunk_off[nl];
+  QADC_CUDA(cudaMalloc(&tmp.chunk_off, (nl + 1) * 8));
+  QADC_CUDA(cudaMalloc(&tmp.lanes, nl * 8));
+  QADC_CUDA(cudaMemcpy(tmp.chunk_off, tmp.h_chunk_off.data(), (nl + 1) * 8, cudaMemcpyHostToDevice));
+  QADC_CUDA(cudaMemcpy(tmp.lanes, lanes.data(), nl * 8, cudaMemcpyHostToDevice));
+  int rc = pack_from_rows(&tmp, rows, row_off, ids, 0);
+  if (!rc) rc = cudaDeviceSynchronize() == cudaSuccess ? kOk : cuda_fail(cudaGetLastError(), "pack prefix");
+  cudaFree(tmp.valid);
+  cudaFree(tmp.chunk_list);
+  if (rc) {
+    cudaFree(tmp.codes); cudaFree(tmp.ids); cudaFree(tmp.chunk_off); cudaFree(tmp.lanes);
+    return rc;
+  }
+  if (idx->own_prefix) {
+    cudaFree(idx->pcodes); cudaFree(idx->pids); cudaFree(idx->pchunk_off); cudaFree(idx->planes);
+  }
+  idx->pcodes = tmp.codes;
+  idx->pids = tmp.ids;
+  idx->pchunk_off = tmp.chunk_off;
+  idx->planes = tmp.lanes;
+  idx->own_prefix = true;
+  idx->h_count.assign(full_count, full_count + nl);
+  QADC_CUDA(cudaMemcpy(idx->count, full_count, nl * 8, cudaMemcpyHostToDevice));
   return kOk;
 }
 
@@ -612,7 +694,8 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
   }
   SearchStats ss;
   const int cap_g = (int)std::min<int64_t>(std::max<int64_t>(8192, 8LL * R), 1 << 20);
-  int rc = search_impl(idx, q, nq, R, ma, init, lin, cin, oi, od, on, st, ss, nullptr, cap_g, 0);
+  int rc = search_impl(idx, q, nq, R, ma, init, lin, cin, oi, od, on, st, ss, nullptr, cap_g, 0,
+                       (flags & QADC_B200_NO_FSAT) != 0);
   if (rc) return rc;
   if (host) {
     QADC_CUDA(cudaMemcpyAsync(out_ids, oi, (size_t)nq * R * 8, cudaMemcpyDeviceToHost, st));
@@ -621,7 +704,7 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
     QADC_CUDA(cudaStreamSynchronize(st));
   }
   if (stats) {
-    stats[0] = 0;
+    stats[0] = ss.codes;
     stats[1] = ss.cands;
     stats[2] = ss.reruns;
     stats[3] = ss.scan_launches;

@@ -31,7 +31,16 @@ struct qadc_b200_index {
   int32_t *chunk_list = nullptr;  // [total_chunks] owning list
   int64_t *chunk_off = nullptr;   // [nlists + 1]
   int64_t *lanes = nullptr;       // [nlists] lanes in layout (16 * nblocks)
-  int64_t *count = nullptr;       // [nlists] valid-code count (find_qmax prefix)
+  int64_t *count = nullptr;       // [nlists] GLOBAL code count (find_qmax prefix)
+  int64_t *scan_count = nullptr;  // [nlists] codes in this index's scan region
+  // Prefix region read by find_qmax / F_sat / the initial bound. By default
+  // it aliases the scan region; a shard of a distributed index stores the
+  // global list prefixes here (qadc_b200_index_set_prefix_device).
+  uint32_t *pcodes = nullptr;
+  int64_t *pids = nullptr;
+  int64_t *pchunk_off = nullptr;
+  int64_t *planes = nullptr;
+  bool own_prefix = false;
   std::vector<int64_t> h_chunk_off, h_lanes, h_count;
   int64_t bytes = 0;
 };
@@ -101,7 +110,7 @@ struct ScanArgs {
   unsigned *cand_n;        // [nq]
   float *cand_mid;         // [nq][cap_g]
   int64_t *cand_id;        // [nq][cap_g]
-  unsigned *hist;          // [nq][kHistBins] midpoint histogram of published candidates
+  unsigned *hist;          // [nq][kHistWords] midpoint histogram of appended candidates
   const float *hist_w;     // [nq] bucket width (0 disables)
   int cap_g;
   int cap_l;               // per-warp per-query buffer capacity
@@ -109,7 +118,8 @@ struct ScanArgs {
   int R;
 };
 
-constexpr int kHistBins = 1024;
+constexpr int kHistBins = 1024;                 // 32 coarse x 32 fine
+constexpr int kHistWords = kHistBins + 32;      // fine bins, then coarse sums
 int scan_qt_per_cta(int m);
 void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st);
 // Work-list construction (device side): returns item upper bound.

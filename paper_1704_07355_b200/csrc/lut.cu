@@ -93,6 +93,7 @@ __global__ void k_tables(const float *__restrict__ codebooks, int m, int dsub,
 // memory, candidates of all tiles are merged by a final select, and the
 // winners are sorted.
 constexpr int kProbeTile = 4096;
+constexpr int kBoundPrefix = 16384;
 
 __device__ uint64_t block_kth_u64(const uint64_t *keys, int n, int k, unsigned *hist,
                                   uint64_t *s_prefix, int *s_k) {
@@ -370,7 +371,7 @@ __global__ void k_quantize(const float *__restrict__ lut, int m,
 //     exactly these (_pykernels.py:80-83).
 // (2) Initial distance bound M: max midpoint of those first R valid lanes,
 //     tightened by the R-th smallest non-saturated midpoint among the
-//     first `init` codes of the first cell. Both are midpoints of members
+//     first max(init, kBoundPrefix) codes of the first cell. Both are midpoints of members
 //     of the candidate set, so at least R candidates lie at or below M.
 __global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ codes,
                                                 const int64_t *__restrict__ chunk_off,
@@ -399,7 +400,10 @@ __global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ cod
     const int64_t L = cells ? cells[pair] : 0;
     const int64_t c0 = chunk_off[L], n = lanes[L];
     const float qmin = qmin_f[pair], delta = delta_f[pair];
-    const int64_t pref = (s == 0) ? ((int64_t)init < n ? (int64_t)init : n) : 0;  // init prefix (cell 0)
+    // bound prefix of cell 0: at least init codes, and up to kBoundPrefix
+    // so the initial bound starts near the R/kBoundPrefix quantile
+    const int64_t want = (int64_t)(init > kBoundPrefix ? init : kBoundPrefix);
+    const int64_t pref = (s == 0) ? (want < n ? want : n) : 0;
     for (int e = threadIdx.x; e < m * 4; e += blockDim.x)
       ((uint32_t *)sqt)[e] = qt[(size_t)pair * m * 4 + e];
     __syncthreads();
@@ -491,7 +495,7 @@ void launch_qmax(const qadc_b200_index *idx, const float *lut, const int64_t *ce
   if (nq <= 0) return;
   unsigned *scratch = nullptr;
   cudaMallocAsync(&scratch, (size_t)nq * std::max(init, 1) * 4, st);
-  k_qmax<<<nq, 256, (size_t)idx->m * 64, st>>>(idx->codes, idx->chunk_off, idx->count, lut,
+  k_qmax<<<nq, 256, (size_t)idx->m * 64, st>>>(idx->pcodes, idx->pchunk_off, idx->count, lut,
                                                idx->K ? cells : nullptr, idx->m, nslots, R, init,
                                                scratch, qmax);
   cudaFreeAsync(scratch, st);
@@ -510,7 +514,7 @@ void launch_prefix(const qadc_b200_index *idx, const uint32_t *qt, const float *
                    unsigned *M_bits, int *fsat_n, float *fsat_mid, int64_t *fsat_id,
                    cudaStream_t st) {
   if (nq <= 0) return;
-  k_prefix<<<nq, 256, 0, st>>>(idx->codes, idx->chunk_off, idx->lanes, idx->ids, qt, qmin_f,
+  k_prefix<<<nq, 256, 0, st>>>(idx->pcodes, idx->pchunk_off, idx->planes, idx->pids, qt, qmin_f,
                                delta_f, idx->K ? cells : nullptr, idx->m, nslots, R, init, M_bits,
                                fsat_n, fsat_mid, fsat_id);
 }

@@ -43,27 +43,34 @@ struct Smem {
   unsigned kbias[kWarps][16];
   unsigned mc[kWarps][16];
   int bn[kWarps][16];
+  unsigned hist[256];
 };
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
 
 __device__ __forceinline__ unsigned kbias_of(int thr) {
   return (0x8000u - (unsigned)(thr + 1)) * 0x10001u;
 }
 
-// Every published candidate is counted in a per-query histogram of
-// midpoints (bucket b = floor(mid / w)). The R-th smallest bucket bounds
-// the R-th best candidate published so far: M = (b + 2) * w (one bucket
-// of slack absorbs fp32 rounding of the bucket index). This lets the
-// global bound converge to the true R-th best of everything scanned, not
-// just to the best per-warp local bound.
-__device__ __noinline__ void publish_bound(const ScanArgs &a, int query) {
+// Every candidate a warp appends to its buffer is counted once in a
+// per-query two-level histogram of midpoints (bucket b = floor(mid / w),
+// 32 coarse x 32 fine bins). Lanes are tested exactly once, so the counts
+// are of distinct members of the candidate set, and the R-th smallest
+// bucket bounds the R-th best candidate seen by ANY warp so far:
+// M = (b + 2) * w (one bucket of slack absorbs fp32 rounding of b). The
+// global bound therefore tracks the union of all warps' scans, not only
+// the best single warp.
+__device__ __forceinline__ unsigned hist_bound(const ScanArgs &a, int query) {
   const int lane = threadIdx.x & 31;
   const float hw = a.hist_w[query];
-  if (!(hw > 0.f)) return;
-  const unsigned *h = a.hist + (size_t)query * kHistBins;
-  constexpr int per = kHistBins / 32;
-  unsigned c = 0;
-#pragma unroll 8
-  for (int i = 0; i < per; i++) c += *(volatile const unsigned *)&h[lane * per + i];
+  if (!(hw > 0.f)) return 0x7f800000u;
+  const unsigned *h = a.hist + (size_t)query * kHistWords;
+  const unsigned c = *(volatile const unsigned *)&h[kHistBins + lane];
   unsigned incl = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -72,19 +79,26 @@ __device__ __noinline__ void publish_bound(const ScanArgs &a, int query) {
   }
   const unsigned R = (unsigned)a.R;
   const unsigned hit = __ballot_sync(kFull, incl >= R);
-  if (!hit) return;
-  const int src = __ffs(hit) - 1;
-  if (lane == src) {
-    unsigned cum = incl - c;
-    int b = lane * per;
-    for (int i = 0; i < per; i++, b++) {
-      cum += *(volatile const unsigned *)&h[b];
-      if (cum >= R) break;
-    }
-    const float M = __fmul_rn((float)(b + 2), hw);
-    atomicMin(&a.M_bits[query], fbits(M));
+  if (!hit) return 0x7f800000u;
+  const int k = __ffs(hit) - 1;
+  const unsigned base = __shfl_sync(kFull, incl - c, k);
+  const unsigned f = *(volatile const unsigned *)&h[k * 32 + lane];
+  unsigned fi = f;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, fi, o);
+    if (lane >= o) fi += y;
   }
-  __syncwarp();
+  const unsigned hit2 = __ballot_sync(kFull, base + fi >= R);
+  const int b = k * 32 + (hit2 ? __ffs(hit2) - 1 : 31);
+  return fbits(__fmul_rn((float)(b + 2), hw));
+}
+
+__device__ __forceinline__ void hist_add(const ScanArgs &a, int query, float hw, float mid) {
+  const int b = min((int)(mid / hw), kHistBins - 1);
+  unsigned *h = a.hist + (size_t)query * kHistWords;
+  atomicAdd(&h[b], 1u);
+  atomicAdd(&h[kHistBins + (b >> 5)], 1u);
 }
 
 // Global append of every buffered entry of (warp, q) whose midpoint is <=
@@ -95,7 +109,6 @@ __device__ __noinline__ void flush_buffer(const ScanArgs &a, Smem &s, uint32_t *
   const int query = s.query[q];
   const float qmin = s.qmin[q], delta = s.delta[q];
   const float Mg = __uint_as_float(*(volatile unsigned *)&a.M_bits[query]);
-  const float hw = a.hist_w[query];
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
     bool keep = false;
@@ -112,7 +125,6 @@ __device__ __noinline__ void flush_buffer(const ScanArgs &a, Smem &s, uint32_t *
     if (lane == 0) pos = atomicAdd(&a.cand_n[query], (unsigned)__popc(bal));
     pos = __shfl_sync(kFull, pos, 0);
     if (keep) {
-      if (hw > 0.f) atomicAdd(&a.hist[(size_t)query * kHistBins + min((int)(mid / hw), kHistBins - 1)], 1u);
       const unsigned slot = pos + __popc(bal & ((1u << lane) - 1));
       if (slot < (unsigned)a.cap_g) {
         const size_t o = (size_t)query * a.cap_g + slot;
@@ -124,7 +136,6 @@ __device__ __noinline__ void flush_buffer(const ScanArgs &a, Smem &s, uint32_t *
   __syncwarp();
   if (lane == 0) s.bn[w][q] = 0;
   __syncwarp();
-  if (n > 0) publish_bound(a, query);
 }
 
 // Tighten (warp, q)'s threshold to the R-th smallest buffered value and
@@ -183,7 +194,7 @@ __device__ __noinline__ void append(const ScanArgs &a, Smem &s, uint32_t *buf, i
   }
   int total = __shfl_sync(kFull, incl, 31);
   int n = s.bn[w][q];
-  if (n + total > a.cap_l) {
+  if (n + total > a.cap_l) {  // n > cap_l - 128 >= R
     if (n >= a.R) compact_buffer(a, s, buf, w, q);
     // re-filter with the (possibly) tightened threshold
     const int thr = s.thr[w][q];
@@ -208,16 +219,50 @@ __device__ __noinline__ void append(const ScanArgs &a, Smem &s, uint32_t *buf, i
   }
   int off = n + incl - cnt;
   const uint32_t base_idx = (uint32_t)chunk_local * kChunkCodes + 8u * lane;
+  const int query = s.query[q];
+  const float hw = a.hist_w[query], qmin = s.qmin[q], delta = s.delta[q];
 #pragma unroll
   for (int k = 0; k < 8; k++) {
     if (mask8 & (1u << k)) {
       const uint32_t v = ((k < 4 ? v0 : v1) >> (8 * (k & 3))) & 255u;
       buf[off++] = (v << 24) | (base_idx + k);
+      if (hw > 0.f) hist_add(a, query, hw, midpoint(qmin, delta, (int)v));
     }
   }
   __syncwarp();
   if (lane == 0) s.bn[w][q] = n + total;
+  // the union of all warps' candidates may now bound the query tighter
+  const unsigned mb = hist_bound(a, query);
+  if (lane == 0 && mb < s.mc[w][q]) {
+    atomicMin(&a.M_bits[query], mb);
+    s.mc[w][q] = mb;
+    const int t = q_threshold(__uint_as_float(mb), qmin, delta);
+    if (t < s.thr[w][q]) {
+      s.thr[w][q] = t;
+      s.kbias[w][q] = kbias_of(t);
+    }
+  }
   __syncwarp();
+}
+
+// Rare path of the per-chunk test: some lane of (warp, q) may qualify.
+__device__ __noinline__ void candidates(const ScanArgs &a, Smem &s, uint32_t *buf, int w, int q,
+                                        uint32_t E0, uint32_t O0, uint32_t E1, uint32_t O1,
+                                        uint32_t valid8, int chunk_local) {
+  const unsigned kb = s.kbias[w][q];
+  const uint32_t pe0 = ~(E0 + kb) & 0x80008000u, po0 = ~(O0 + kb) & 0x80008000u;
+  const uint32_t pe1 = ~(E1 + kb) & 0x80008000u, po1 = ~(O1 + kb) & 0x80008000u;
+  uint32_t mask8 = ((pe0 >> 15) & 1u) | ((po0 >> 14) & 2u) | ((pe0 >> 29) & 4u) |
+                   ((po0 >> 28) & 8u);
+  mask8 |= (((pe1 >> 15) & 1u) | ((po1 >> 14) & 2u) | ((pe1 >> 29) & 4u) | ((po1 >> 28) & 8u))
+           << 4;
+  mask8 &= valid8;
+  const uint32_t v0 = prmt(E0, O0, 0x6240), v1 = prmt(E1, O1, 0x6240);  // low bytes
+  // at most 4 codes per lane per append: the buffer needs R + 128 slots
+  if (__any_sync(kFull, (mask8 & 0x0fu) != 0))
+    append(a, s, buf, w, q, mask8 & 0x0fu, v0, v1, chunk_local);
+  if (__any_sync(kFull, (mask8 & 0xf0u) != 0))
+    append(a, s, buf, w, q, mask8 & 0xf0u, v0, v1, chunk_local);
 }
 
 // Refresh each query's threshold from the global bound (lanes in parallel).
@@ -238,7 +283,7 @@ __device__ __forceinline__ void refresh(const ScanArgs &a, Smem &s, int w, int n
 }
 
 template <int MC, int QT>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_scan(ScanArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 5) k_scan(ScanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Smem s;
   const int m = MC ? MC : a.m;
@@ -246,6 +291,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_scan(ScanArgs a) {
   uint32_t *s_buf = (uint32_t *)(dsm + (size_t)QT * m * 16);        // [W][QT][cap_l]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t *wbuf = s_buf + (size_t)w * QT * a.cap_l;
+  const uint32_t tab_sa = (uint32_t)__cvta_generic_to_shared(s_tab);
   const uint32_t one = (uint32_t)(a.R > 0);  // runtime 1 (keeps IMAD on the FMA pipe)
   const int n_items = *a.n_items;
   for (;;) {
@@ -303,14 +349,23 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_scan(ScanArgs a) {
       uint32_t acc_a[QT][2], acc_o[QT][2];
 #pragma unroll
       for (int q = 0; q < QT; q++) acc_a[q][0] = acc_a[q][1] = acc_o[q][0] = acc_o[q][1] = 0;
-#pragma unroll(MC ? MC / 2 : 2)
+      // two sub-quantizer pairs per iteration keep the loop body inside the
+      // instruction cache (a fully unrolled body stalls on no_inst); the
+      // next pair's code words are prefetched one iteration ahead
+      uint32_t nw0 = __ldg(cw), nw1 = __ldg(cw + 32);
+#pragma unroll 2
       for (int j = 0; j < m; j += 2) {
-        const uint32_t w0 = __ldg(cw + j * 32), w1 = __ldg(cw + (j + 1) * 32);
+        const uint32_t w0 = nw0, w1 = nw1;
+        if (j + 2 < m) {
+          nw0 = __ldg(cw + (j + 2) * 32);
+          nw1 = __ldg(cw + (j + 3) * 32);
+        }
         const uint32_t a0 = w0, a1 = w0 >> 16, a0x = w0 ^ 0x88888888u, a1x = a0x >> 16;
         const uint32_t b0 = w1, b1 = w1 >> 16, b0x = w1 ^ 0x88888888u, b1x = b0x >> 16;
 #pragma unroll
         for (int q = 0; q < QT; q++) {
-          const uint4 t = s_tab[q * m + j], u = s_tab[q * m + j + 1];
+          const uint4 t = lds128(tab_sa + (uint32_t)((q * m + j) * 16));
+          const uint4 u = lds128(tab_sa + (uint32_t)((q * m + j + 1) * 16));
           // codes 0-3 of the octet: sub-quantizers j and j+1, both halves
           const uint32_t s0 = imad(prmt(t.x, t.y, a0), one,
                               imad(prmt(t.z, t.w, a0x), one,
@@ -325,27 +380,57 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_scan(ScanArgs a) {
           acc_o[q][1] = imad(prmt(s1, 0, 0x4341), one, acc_o[q][1]);
         }
       }
-      // ---- threshold test: 16-bit lanes, bit 15 clear <=> lane <= thr ----
+      // ---- threshold test: 16-bit lanes, bit 15 clear <=> lane <= thr.
+      // One combined test and one vote per query; the per-lane mask is
+      // built only on the rare path. ----
       const int chunk_local = (int)(g - it.chunk_begin);
 #pragma unroll
       for (int q = 0; q < QT; q++) {
         const unsigned kb = s.kbias[w][q];
-        uint32_t mask8 = 0, v[2];
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const uint32_t O = acc_o[q][h];
-          const uint32_t E = acc_a[q][h] - (O << 8);
-          const uint32_t pe = ~(E + kb) & 0x80008000u;
-          const uint32_t po = ~(O + kb) & 0x80008000u;
-          mask8 |= (((pe >> 15) & 1u) | ((po >> 14) & 2u) | ((pe >> 29) & 4u) |
-                    ((po >> 28) & 8u)) << (4 * h);
-          v[h] = prmt(E, O, 0x6240);  // low bytes of lanes 0..3
-        }
-        mask8 &= valid8;
-        if (__any_sync(kFull, mask8 != 0)) append(a, s, wbuf + q * a.cap_l, w, q, mask8, v[0], v[1], chunk_local);
+        const uint32_t O0 = acc_o[q][0], E0 = acc_a[q][0] - (O0 << 8);
+        const uint32_t O1 = acc_o[q][1], E1 = acc_a[q][1] - (O1 << 8);
+        const uint32_t all = (E0 + kb) & (O0 + kb) & (E1 + kb) & (O1 + kb);
+        if (__any_sync(kFull, (all & 0x80008000u) != 0x80008000u))
+          candidates(a, s, wbuf + q * a.cap_l, w, q, E0, O0, E1, O1, valid8, chunk_local);
       }
     }
-    // ---- end of item: publish survivors ----
+    // ---- end of item: CTA-level bound per query (the R-th smallest value
+    // over all four warps' buffers lowers the global M), then publish ----
+    __syncthreads();
+    for (int q = 0; q < nq_tile; q++) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) s.hist[i] = 0;
+      __syncthreads();
+      int tot = 0;
+      for (int ww = 0; ww < kWarps; ww++) {
+        const int n = s.bn[ww][q];
+        tot += n;
+        const uint32_t *b = s_buf + ((size_t)ww * QT + q) * a.cap_l;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&s.hist[b[i] >> 24], 1u);
+      }
+      __syncthreads();
+      if (w == 0 && tot >= a.R) {
+        unsigned c = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) c += s.hist[lane * 8 + i];
+        unsigned incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const unsigned hit = __ballot_sync(kFull, incl >= (unsigned)a.R);
+        if (lane == __ffs(hit) - 1) {
+          unsigned cum = incl - c;
+          int t = lane * 8;
+          for (int i = 0; i < 8; i++, t++) {
+            cum += s.hist[t];
+            if (cum >= (unsigned)a.R) break;
+          }
+          atomicMin(&a.M_bits[s.query[q]], fbits(midpoint(s.qmin[q], s.delta[q], t)));
+        }
+      }
+      __syncthreads();
+    }
     for (int q = 0; q < nq_tile; q++) flush_buffer(a, s, wbuf + q * a.cap_l, w, q);
     __syncthreads();
   }

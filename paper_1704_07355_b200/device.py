@@ -85,9 +85,19 @@ class DeviceIndex:
             ctypes.byref(h)), "index_create_device")
         return cls(h.value, d, m, 0 if coarse is None else nl, nl, int(codes.shape[0]))
 
+    def set_prefix(self, rows, row_off, full_count, ids=None) -> None:
+        """Install the GLOBAL first codes of every list (device rows in list
+        order, row_off (nlists + 1) device int64, full_count host ints) as
+        the prefix find_qmax / the saturation rule read: a shard holding
+        part of a list then reproduces the unsharded search."""
+        fc = _np(full_count, np.int64)
+        _native.check(_native.load_library().qadc_b200_index_set_prefix_device(
+            self._h, _native.dptr(rows), _native.dptr(row_off), _native.dptr(ids),
+            _native.ptr(fc, ctypes.c_int64)), "index_set_prefix_device")
+
     # ------------------------------------------------------------ search
     def search(self, queries, R: int, ma: int = 1, init: int = 1000, lut=None, cells=None,
-               stream=None) -> BatchResult:
+               stream=None, with_fsat: bool = True) -> BatchResult:
         """Batched Quick ADC search. `queries` is a (Q, d) float32 torch
         tensor on the GPU (device I/O) or a numpy array (host I/O: the
         host<->device copies happen inside the call). lut/cells inject the
@@ -98,6 +108,8 @@ class DeviceIndex:
         st = stream if stream is not None else torch.cuda.current_stream()
         stats = np.zeros(8, dtype=np.int64)
         flags = _native.LUT_IN if lut is not None else 0
+        if not with_fsat:
+            flags |= _native.NO_FSAT
         if isinstance(queries, np.ndarray):
             q = _np(queries, np.float32).reshape(-1, self.d)
             nq = q.shape[0]

@@ -1,0 +1,104 @@
+"""BASELINE.json workloads built on the GPU (index-build side, not the
+search hot path): synthetic mixture base vectors drawn on the device,
+encoded by the GPU encoder with reference-trained codebooks
+(bench_data/*_codebooks.npy), and repacked into a DeviceIndex without a
+host round trip.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import datagen
+from .device import DeviceIndex
+
+BENCH_DATA = Path(__file__).resolve().parent.parent / "bench_data"
+
+
+@dataclass(frozen=True)
+class FlatConfig:
+    name: str
+    mix: datagen.Mixture
+    m: int
+    n: int
+    q: int
+    R: int
+    init: int
+    codebooks_file: str
+
+
+CONFIGS = {
+    "cfg0": FlatConfig("cfg0_exhaustive_m16_N1e6_Q100", datagen.SIFT_LIKE, 16, 1_000_000, 100,
+                       100, 1000, "cfg0_m16_codebooks.npy"),
+    "cfg1": FlatConfig("cfg1_exhaustive_m32_N1e7_Q1000", datagen.SIFT_LIKE, 32, 10_000_000,
+                       1000, 100, 1000, "cfg1_m32_codebooks.npy"),
+    "cfg3": FlatConfig("cfg3_exhaustive_d960_m32_N1e6_Q1000", datagen.GIST_LIKE, 32, 1_000_000,
+                       1000, 100, 1000, "cfg3_m32_d960_codebooks.npy"),
+}
+
+SEED = 1
+
+
+class _PQ:
+    """Minimal ProductQuantizer-shaped holder (codebooks trained by the
+    reference, loaded from bench_data)."""
+
+    def __init__(self, codebooks: np.ndarray, rotation=None):
+        self.codebooks = np.ascontiguousarray(codebooks, dtype=np.float32)
+        self.m = self.codebooks.shape[0]
+        self.b = 4
+        self.rotation = rotation
+
+    @property
+    def d(self) -> int:
+        return self.m * self.codebooks.shape[2]
+
+
+def load_pq(cfg: FlatConfig) -> _PQ:
+    return _PQ(np.load(BENCH_DATA / cfg.codebooks_file))
+
+
+def shard_codes(cfg: FlatConfig, pq: _PQ, n: int, shard: int, device="cuda"):
+    """Packed codes (n, m/2) of base shard `shard` (drawn + encoded on GPU)."""
+    import torch
+
+    from .ivf import encode_device
+
+    out = torch.empty((n, pq.m // 2), dtype=torch.uint8, device=device)
+    step = datagen.CHUNK
+    for c0 in range(0, n, 4 * step):
+        k = min(4 * step, n - c0)
+        X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + shard,
+                                  stream=datagen.STREAM_BASE * 100 + c0 // (4 * step),
+                                  device=device)
+        out[c0:c0 + k] = encode_device(pq, X)
+        del X
+    return out
+
+
+def queries(cfg: FlatConfig, q: int | None = None) -> np.ndarray:
+    return datagen.mixture_numpy(cfg.mix, q or cfg.q, seed=SEED, stream=datagen.STREAM_QUERY)
+
+
+def build_shard_index(cfg: FlatConfig, pq: _PQ, n: int, rank: int, world: int, prefix: int):
+    """DeviceIndex over shard `rank` of a flat list of world * n codes
+    (global ids rank * n + i). For world > 1 every shard also installs the
+    GLOBAL prefix (the first `prefix` codes = the start of shard 0) so
+    qmax and the saturation rule match the unsharded search."""
+    import torch
+
+    codes = shard_codes(cfg, pq, n, rank)
+    dev = torch.device("cuda")
+    row_off = torch.tensor([0, n], dtype=torch.int64, device=dev)
+    ids = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int64, device=dev)
+    cb = torch.from_numpy(pq.codebooks).to(dev)
+    index = DeviceIndex.from_device_rows(pq.d, pq.m, codes, row_off, cb, ids=ids)
+    if world > 1:
+        p = min(prefix, n)
+        head = codes[:p] if rank == 0 else shard_codes(cfg, pq, min(n, datagen.CHUNK), 0)[:p]
+        index.set_prefix(head.contiguous(), torch.tensor([0, p], dtype=torch.int64, device=dev),
+                         [world * n], ids=torch.arange(p, dtype=torch.int64, device=dev))
+    return index, codes

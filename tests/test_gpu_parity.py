@@ -1,0 +1,325 @@
+"""GPU parity: the sm_100a path (through the C ABI of libqadc_b200.so)
+against the reference's golden outputs and the CPU oracle on the same
+seeded inputs. Integer / byte / id results must be bit-exact; reported
+distances are compared by fp32 bit pattern."""
+
+import numpy as np
+import pytest
+from conftest import cases, golden
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+# ------------------------------------------------------------ kernels
+
+def test_block_distances_match_golden(gpu):
+    from paper_1704_07355_b200 import kernels
+    for c in cases(golden("block_dists.npz")):
+        assert np.array_equal(kernels.block_distances(c["blocks"], c["shared"]), c["out_shared"])
+        assert np.array_equal(kernels.block_distances(c["blocks"], c["per"]), c["out_per"])
+
+
+def test_acceptance_criterion_1_fuzz(gpu):
+    """tests/test_acceptance.py:118-142: >=10^5 block/table pairs, m in
+    (8, 16, 32), half with full-range table bytes, byte-exact."""
+    from paper_1704_07355_b200 import kernels
+    rng = np.random.default_rng(7)
+    pairs = 0
+    for m in (8, 16, 32):
+        nb = 34000
+        blocks = rng.integers(0, 256, (nb, m // 2, 16), dtype=np.uint8)
+        tables = rng.integers(0, 128, (nb, m, 16), dtype=np.uint8)
+        tables[nb // 2:] = rng.integers(0, 256, (nb - nb // 2, m, 16), dtype=np.uint8)
+        assert np.array_equal(kernels.block_distances(blocks, tables),
+                              orc.block_dists(blocks, tables))
+        pairs += nb
+    assert pairs >= 100_000
+
+
+def test_saturation_kat(gpu):
+    from paper_1704_07355_b200.qadc import scan_block_scalar
+    qt = np.zeros((2, 16), np.uint8)
+    qt[0, 2], qt[1, 3] = 200, 100
+    block = np.full((1, 16), 0x32, np.uint8)
+    assert (scan_block_scalar(block, qt) == 255).all()
+    qt[1, 3] = 50
+    assert (scan_block_scalar(block, qt) == 250).all()
+
+
+def test_quantize_tables_match_golden(gpu):
+    from paper_1704_07355_b200.qadc import quantize_tables
+    for c in cases(golden("quantize.npz")):
+        qt = quantize_tables(c["tables"], float(c["qmin"]), float(c["qmax"]))
+        assert np.array_equal(qt.tables, c["q"])
+        assert qt.delta == float(c["delta"])
+
+
+def test_scan_blocks_match_golden(gpu):
+    """Padding lanes, pre-filled heaps, saturation rule (test_kernels.py:145-168)."""
+    from paper_1704_07355_b200 import kernels
+    from paper_1704_07355_b200.heap import NeighborHeap
+    for c in cases(golden("scan_blocks.npz")):
+        h = NeighborHeap(int(c["cap"]))
+        if c["pre_i"].shape[0]:
+            h.push_batch(c["pre_i"], c["pre_d"])
+        kernels.scan_blocks(c["blocks"], c["ids"], c["qt"], float(c["qmin"]), float(c["delta"]), h)
+        gi, gd = h.extract()
+        assert np.array_equal(gi, c["out_i"])
+        assert np.array_equal(_bits(gd), _bits(c["out_d"]))
+
+
+def test_scan_blocks_saturated_only_below_capacity(gpu):
+    """test_qadc.py:255-274: every lane saturates -> first `capacity` ids;
+    a full heap never admits a saturated lane."""
+    from paper_1704_07355_b200 import qadc as Q
+    from paper_1704_07355_b200.heap import NeighborHeap
+    from paper_1704_07355_b200.pq_util import pack_codes
+    codes = np.full((64, 4), 3, np.uint8)
+    tl = Q.transpose_list(pack_codes(codes), np.arange(64, dtype=np.int64))
+    qt = np.full((4, 16), 127, np.uint8)
+    h = NeighborHeap(10)
+    Q.qadc_scan(tl, qt, h, qmin=0.0, delta=0.1)
+    assert np.array_equal(h.extract()[0], np.arange(10))
+    h2 = NeighborHeap(10)
+    h2.push_batch(np.arange(100, 110, dtype=np.int64), np.full(10, 500.0, np.float32))
+    Q.qadc_scan(tl, qt, h2, qmin=0.0, delta=0.1)
+    assert np.array_equal(h2.extract()[0], np.arange(100, 110))
+
+
+def test_scan_codes_float_matches_oracle(gpu, rng):
+    from paper_1704_07355_b200 import kernels
+    from paper_1704_07355_b200.heap import NeighborHeap
+    lib = orc.lib()
+    import ctypes
+    for trial in range(30):
+        b = int(rng.choice([4, 8, 16]))
+        m = int(rng.integers(1, 7)) * (2 if b == 4 else 1)
+        n = int(rng.integers(0, 300))
+        cap = int(rng.integers(1, 30))
+        tables = (rng.random((m, 1 << b), dtype=np.float32) * 10).astype(np.float32)
+        width = {4: m // 2, 8: m, 16: 2 * m}[b]
+        codes = rng.integers(0, 256, (n, width), dtype=np.uint8)
+        ids = rng.permutation(n).astype(np.int64) * 3
+        h = NeighborHeap(cap)
+        kernels.scan_codes(codes, ids, tables, b, h)
+        hd, hi = np.zeros(cap, np.float32), np.zeros(cap, np.int64)
+        p = lambda a, t: a.ctypes.data_as(ctypes.POINTER(t))  # noqa: E731
+        k = lib.orc_adc_scan_f32(p(codes, ctypes.c_uint8), n, p(ids, ctypes.c_int64), m, b,
+                                 p(tables, ctypes.c_float), p(hd, ctypes.c_float),
+                                 p(hi, ctypes.c_int64), 0, cap)
+        lib.orc_heap_extract(p(hd, ctypes.c_float), p(hi, ctypes.c_int64), k)
+        gi, gd = h.extract()
+        assert np.array_equal(gi, hi[:k]) and np.array_equal(_bits(gd), _bits(hd[:k]))
+
+
+def test_find_qmax_matches_golden(gpu):
+    from paper_1704_07355_b200.qadc import find_qmax, transpose_list
+    for c in cases(golden("find_qmax.npz")):
+        tl = transpose_list(c["codes"], np.arange(c["codes"].shape[0], dtype=np.int64))
+        got = find_qmax([(c["tables"], tl)], R=int(c["R"]), init=int(c["init"]))
+        assert np.float32(got) == np.float32(c["qmax"])
+
+
+def test_compute_tables_bit_exact(gpu):
+    """einsum-order LUT (adc.py:61-75) is bit-exact, not just within 1e-5."""
+    from paper_1704_07355_b200.adc import compute_tables
+    from paper_1704_07355_b200.workload import _PQ
+    for c in cases(golden("tables.npz")):
+        pq = _PQ(c["codebooks"])
+        for y, want in zip(c["y"], c["tables"]):
+            assert np.array_equal(_bits(compute_tables(pq, y).tables), _bits(want))
+
+
+def test_probe_matches_golden(gpu):
+    from paper_1704_07355_b200 import ivf
+    g = golden("probe.npz")
+    index = ivf.IvfIndex(d=128, m=16, b=4, coarse=ivf.Codebook(g["centroids"]),
+                         lists=[None] * g["centroids"].shape[0], layout=ivf.LAYOUT_STANDARD)
+    for q, cells, res in zip(g["queries"], g["cells"], g["residuals"]):
+        ps = ivf.probe(index, q, int(g["ma"]))
+        assert np.array_equal(ps.cells, cells)
+        assert np.array_equal(_bits(ps.residual_queries), _bits(res))
+
+
+# ------------------------------------------------------------ batched search
+
+def _index_from_golden(g):
+    from paper_1704_07355_b200 import ivf
+    from paper_1704_07355_b200.qadc import transpose_list
+    sizes = g["list_sizes"]
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    lists = [transpose_list(g["codes"][off[L]:off[L + 1]], g["ids"][off[L]:off[L + 1]])
+             for L in range(sizes.shape[0])]
+    coarse = ivf.Codebook(g["coarse"]) if "coarse" in g.files else None
+    return ivf.IvfIndex(d=g["queries"].shape[1], m=g["codebooks"].shape[0], b=4, coarse=coarse,
+                        lists=lists, layout=ivf.LAYOUT_TRANSPOSED)
+
+
+def _pq_from_golden(g):
+    from paper_1704_07355_b200.workload import _PQ
+    return _PQ(g["codebooks"], g["rotation"] if "rotation" in g.files else None)
+
+
+@pytest.mark.parametrize("name", ["search_flat16.npz", "search_flat_hd.npz"])
+def test_flat_search_batch_matches_reference(gpu, name):
+    from paper_1704_07355_b200.adc import search_batch
+    g = golden(name)
+    index, pq = _index_from_golden(g), _pq_from_golden(g)
+    for key in [k for k in g.files if k.endswith("_ids")]:
+        R = int(key.split("_R")[1].split("_")[0])
+        res = search_batch(index, pq, g["queries"], R, init=int(g["init"]))
+        assert np.array_equal(res.ids, g[key]), key
+        assert np.array_equal(_bits(res.distances), _bits(g[key.replace("_ids", "_d")])), key
+        assert np.array_equal(res.counts, g[key.replace("_ids", "_n")]), key
+
+
+def test_single_query_search_matches_reference(gpu):
+    from paper_1704_07355_b200.adc import search
+    g = golden("search_flat16.npz")
+    index, pq = _index_from_golden(g), _pq_from_golden(g)
+    for qi in range(5):
+        r = search(index, pq, g["queries"][qi], R=10, method="qadc")
+        n = int(g["ma1_R10_n"][qi])
+        assert np.array_equal(r.ids, g["ma1_R10_ids"][qi, :n])
+        assert np.array_equal(_bits(r.distances), _bits(g["ma1_R10_d"][qi, :n]))
+        t = r.timings
+        assert t.total_ms == pytest.approx(t.index_ms + t.tables_ms + t.scan_ms, abs=1e-9)
+
+
+@pytest.mark.parametrize("ma", [4, 16])
+def test_ivf_opq_injected_lut_bit_exact(gpu, ma):
+    """Reference-LUT-injected mode: with the reference's fp32
+    tables and probe order, ids and distances are bit-exact."""
+    from paper_1704_07355_b200.adc import search_batch
+    g = golden("search_ivf_opq.npz")
+    index, pq = _index_from_golden(g), _pq_from_golden(g)
+    res = search_batch(index, pq, g["queries"], 100, ma=ma, init=int(g["init"]),
+                       lut=g[f"ma{ma}_luts"], cells=g[f"ma{ma}_cells"])
+    assert np.array_equal(res.ids, g[f"ma{ma}_R100_ids"])
+    assert np.array_equal(_bits(res.distances), _bits(g[f"ma{ma}_R100_d"]))
+
+
+@pytest.mark.parametrize("ma", [4, 16])
+def test_ivf_opq_native_counts_flips(gpu, ma):
+    """Native OPQ mode: the GPU rotates in float64 where the reference
+    uses OpenBLAS sgemv (order unpinned); LUT rel err <= 1e-5,
+    probe order exact, and top-R ids exact on every query whose uint8
+    tables did not flip."""
+    from paper_1704_07355_b200.adc import search_batch
+    g = golden("search_ivf_opq.npz")
+    index, pq = _index_from_golden(g), _pq_from_golden(g)
+    res = search_batch(index, pq, g["queries"], 100, ma=ma, init=int(g["init"]))
+    want = g[f"ma{ma}_R100_ids"]
+    same = sum(np.array_equal(res.ids[i], want[i]) for i in range(want.shape[0]))
+    overlap = np.mean([len(set(res.ids[i]) & set(want[i])) / 100 for i in range(want.shape[0])])
+    assert overlap >= 0.97
+    assert same >= want.shape[0] * 0.6, f"{same}/{want.shape[0]} queries id-exact"
+
+
+# ------------------------------------------------------------ oracle, larger sizes
+
+def _random_flat(rng, n, m, d, nq, cb_scale=50.0):
+    import torch
+
+    from paper_1704_07355_b200.device import DeviceIndex
+    from paper_1704_07355_b200.ivf import encode_device
+    from paper_1704_07355_b200.qadc import transpose_list
+    from paper_1704_07355_b200.workload import _PQ
+    cb = (rng.random((m, 16, d // m)) * cb_scale).astype(np.float32)
+    pq = _PQ(cb)
+    X = torch.from_numpy((rng.random((n, d)) * cb_scale).astype(np.float32)).cuda()
+    codes = encode_device(pq, X)
+    idx = DeviceIndex.from_device_rows(d, m, codes, torch.tensor([0, n], device="cuda"),
+                                       torch.from_numpy(cb).cuda())
+    tl = transpose_list(codes.cpu().numpy(), np.arange(n, dtype=np.int64))
+    flat = (tl.blocks.reshape(-1), np.array([0, tl.blocks.shape[0]], np.int64), tl.ids,
+            np.array([n], np.int64))
+    qs = (rng.random((nq, d)) * cb_scale).astype(np.float32)
+    return idx, flat, qs, cb
+
+
+@pytest.mark.parametrize("m,R,init", [(16, 1, 1000), (16, 100, 1000), (32, 100, 1000),
+                                      (32, 1000, 1000), (8, 37, 50), (64, 100, 1000),
+                                      (32, 100, 20)])
+def test_search_batch_vs_oracle(gpu, m, R, init):
+    rng = np.random.default_rng(m * 1000 + R)
+    idx, flat, qs, cb = _random_flat(rng, 150_000, m, 128, 48)
+    res = idx.search(qs, R, init=init)
+    oi, od, on, _ = orc.search_batch(qs, cb, None, None, 1, flat, R, init)
+    assert np.array_equal(res.ids, oi)
+    assert np.array_equal(_bits(res.distances), _bits(od))
+    assert np.array_equal(res.counts, on)
+
+
+def test_edge_cases_vs_oracle(gpu):
+    rng = np.random.default_rng(3)
+    # tiny lists (R > N), odd sizes, exactly one chunk, chunk + 1
+    for n in (1, 7, 16, 255, 256, 257, 1000):
+        idx, flat, qs, cb = _random_flat(rng, n, 16, 64, 8)
+        for R in (1, 5, 300):
+            res = idx.search(qs, R, init=1000)
+            oi, od, on, _ = orc.search_batch(qs, cb, None, None, 1, flat, R, 1000)
+            assert np.array_equal(res.ids, oi), (n, R)
+            assert np.array_equal(_bits(res.distances), _bits(od)), (n, R)
+            assert np.array_equal(res.counts, on), (n, R)
+
+
+def test_massive_ties_vs_oracle(gpu):
+    """Identical codes everywhere: every lane ties; the exact (distance, id)
+    order must still pick the lowest ids (overflow / large-select paths)."""
+    import torch
+
+    from paper_1704_07355_b200.device import DeviceIndex
+    from paper_1704_07355_b200.qadc import transpose_list
+    n, m, d = 60_000, 16, 64
+    rng = np.random.default_rng(5)
+    cb = (rng.random((m, 16, d // m)) * 10).astype(np.float32)
+    codes = np.full((n, m // 2), 0x21, np.uint8)
+    codes[::7] = 0x43
+    idx = DeviceIndex.from_device_rows(d, m, torch.from_numpy(codes).cuda(),
+                                       torch.tensor([0, n], device="cuda"),
+                                       torch.from_numpy(cb).cuda())
+    tl = transpose_list(codes, np.arange(n, dtype=np.int64))
+    flat = (tl.blocks.reshape(-1), np.array([0, tl.blocks.shape[0]], np.int64), tl.ids,
+            np.array([n], np.int64))
+    qs = (rng.random((4, d)) * 10).astype(np.float32)
+    for R in (10, 100):
+        res = idx.search(qs, R, init=1000)
+        oi, od, on, _ = orc.search_batch(qs, cb, None, None, 1, flat, R, 1000)
+        assert np.array_equal(res.ids, oi)
+        assert np.array_equal(_bits(res.distances), _bits(od))
+
+
+def test_property_large_index_sorted_and_self_consistent(gpu):
+    """At 4*10^6 codes (oracle too slow for every query): results are sorted
+    by (distance, id), distances are bin midpoints, and a sampled query
+    matches the oracle bit-exactly."""
+    rng = np.random.default_rng(11)
+    idx, flat, qs, cb = _random_flat(rng, 4_000_000, 32, 128, 64)
+    res = idx.search(qs, 100, init=1000)
+    ids, d = res.ids, res.distances
+    for i in range(ids.shape[0]):
+        o = np.lexsort((ids[i], d[i]))
+        assert np.array_equal(o, np.arange(100))
+        assert len(set(ids[i].tolist())) == 100
+    oi, od, on, _ = orc.search_batch(qs[:3], cb, None, None, 1, flat, 100, 1000)
+    assert np.array_equal(ids[:3], oi) and np.array_equal(_bits(d[:3]), _bits(od))
+
+
+def test_encoder_matches_reference_assignment(gpu):
+    """GPU encoder == reference pq.encode_batch codes (golden corpus)."""
+    import torch
+
+    from paper_1704_07355_b200 import datagen
+    from paper_1704_07355_b200.ivf import encode_device
+    g = golden("search_flat16.npz")
+    pq = _pq_from_golden(g)
+    base = datagen.mixture_numpy(datagen.SIFT_LIKE, 20000, seed=1, stream=datagen.STREAM_BASE)
+    codes = encode_device(pq, torch.from_numpy(base).cuda()).cpu().numpy()
+    assert np.array_equal(codes, g["codes"][np.argsort(g["ids"])])
