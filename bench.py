@@ -136,30 +136,6 @@ def ncu_traffic():
     return None
 
 
-def merge_topr(ids, dists, R, world):
-    """Exact global top-R of per-rank (Q, R) lists by (distance, id):
-    all_gather over the process group, then a stable two-key sort."""
-    import torch
-    import torch.distributed as dist
-
-    if world == 1:
-        return ids, dists
-    gi = [torch.empty_like(ids) for _ in range(world)]
-    gd = [torch.empty_like(dists) for _ in range(world)]
-    dist.all_gather(gi, ids)
-    dist.all_gather(gd, dists)
-    ai = torch.cat(gi, dim=1)
-    ad = torch.cat(gd, dim=1)
-    big = torch.iinfo(torch.int64).max
-    ai = torch.where(ai < 0, torch.full_like(ai, big), ai)
-    o = torch.argsort(ai, dim=1, stable=True)
-    ai, ad = torch.gather(ai, 1, o), torch.gather(ad, 1, o)
-    o = torch.argsort(ad, dim=1, stable=True)
-    ai, ad = torch.gather(ai, 1, o)[:, :R], torch.gather(ad, 1, o)[:, :R]
-    ai = torch.where(ai == big, torch.full_like(ai, -1), ai)
-    return ai, ad
-
-
 def cpu_reference_run(cfg, codes_np, n, qs, R, init, seconds, nthreads=None):
     """The reference's own compiled qadc_scan_u8 (oracle/_ref), driven by the
     restated adc.search orchestration (oracle/), on a bounded query sample;
@@ -198,6 +174,7 @@ def run_b200(args):
     import torch.distributed as dist
 
     from paper_1704_07355_b200 import _native
+    from paper_1704_07355_b200.dist import merge_topr
     from paper_1704_07355_b200.workload import CONFIGS, build_shard_index, load_pq, queries
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -220,7 +197,8 @@ def run_b200(args):
 
     def step_device():
         res = index.search(q_dev, R, init=init, with_fsat=(rank == 0))
-        return merge_topr(res.ids, res.distances, R, world), res
+        gi, gd, _ = merge_topr(res.ids, res.distances, R)
+        return (gi, gd), res
 
     def barrier():
         if world > 1:
@@ -258,15 +236,20 @@ def run_b200(args):
     ms_dev = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
     # ---- end-to-end through the public API with host buffers ----
+    def step_e2e():
+        qd = q_pin.to("cuda", non_blocking=True)
+        res = index.search(qd, R, init=init, with_fsat=(rank == 0))
+        gi, gd, _ = merge_topr(res.ids, res.distances, R)
+        return gi.to("cpu"), gd.to("cpu")
+
+    for _ in range(args.warmup):
+        step_e2e()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
     e2.record(stream)
     for _ in range(args.steps):
-        qd = q_pin.to("cuda", non_blocking=True)
-        res = index.search(qd, R, init=init, with_fsat=(rank == 0))
-        gi, gd = merge_topr(res.ids, res.distances, R, world)
-        out_i, out_d = gi.to("cpu"), gd.to("cpu")
+        out_i, out_d = step_e2e()
     e3.record(stream)
     torch.cuda.synchronize()
     barrier()

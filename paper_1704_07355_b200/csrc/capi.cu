@@ -130,6 +130,21 @@ struct SearchStats {
   double scan_us = 0.0;
 };
 
+// Keep stream-ordered workspace in the device pool between calls (the
+// default release threshold of 0 returns it to the OS at every sync, which
+// turns each search's workspace allocation into page mapping work).
+void retain_pool_memory() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int ma, int init,
                 const float *lut_in, const int64_t *cells_in, int64_t *out_ids, float *out_d,
                 int32_t *out_n, cudaStream_t st, SearchStats &ss, const unsigned *M_override,
@@ -662,6 +677,7 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
     return arg_error("LUT injection needs lut_in (and cells_in for an IVF index)");
   if (R > 1 << 20) return arg_error("R too large");
   cudaStream_t st = (cudaStream_t)stream;
+  retain_pool_memory();
   const int nslots = idx->K ? ma : 1;
   const bool host = flags & QADC_B200_HOST_IO;
   DevBuf<float> dq, dd, dl;

@@ -44,6 +44,8 @@ struct Smem {
   unsigned mc[kWarps][16];
   int bn[kWarps][16];
   unsigned hist[256];
+  int depth;
+  uint8_t rmax[16 * kMaxM];
 };
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -282,8 +284,149 @@ __device__ __forceinline__ void refresh(const ScanArgs &a, Smem &s, int w, int n
   __syncwarp();
 }
 
+// Exact lane sums of one chunk for QT queries: lane `lane` owns the octet
+// of codes 8*lane .. 8*lane+7. Per sub-quantizer pair the two code words
+// become PRMT selectors (low / high 16 bits; XOR 0x8888 flips bit 3 so the
+// 8-15 half of the table answers), reused for every query. Lookups of D
+// consecutive sub-quantizers are summed in bytes (sacc; carry-free because
+// the tile's tables satisfy sum of D row maxima <= 255), then widened into
+// 16-bit lanes: acc_a += sacc, acc_o += odd bytes of sacc; the even lanes
+// are acc_a - (acc_o << 8). Adds run on the FMA pipe (IMAD), lookups on the
+// ALU pipe (PRMT). Two pairs per iteration keep the body inside the
+// instruction cache; code words are prefetched one pair ahead.
+// One sub-quantizer pair (j, j+1) of the octet for every query of the tile.
+template <int QT>
+__device__ __forceinline__ void pair_lookups(uint32_t w0, uint32_t w1, int j, int m,
+                                             uint32_t tab_sa, uint32_t one,
+                                             uint32_t (&sacc)[QT][2]) {
+  const uint32_t a0 = w0, a1 = w0 >> 16, a0x = w0 ^ 0x88888888u, a1x = a0x >> 16;
+  const uint32_t b0 = w1, b1 = w1 >> 16, b0x = w1 ^ 0x88888888u, b1x = b0x >> 16;
+#pragma unroll
+  for (int q = 0; q < QT; q++) {
+    const uint4 t = lds128(tab_sa + (uint32_t)((q * m + j) * 16));
+    const uint4 u = lds128(tab_sa + (uint32_t)((q * m + j + 1) * 16));
+    // codes 0-3 of the octet: sub-quantizers j and j+1, both table halves
+    sacc[q][0] = imad(prmt(t.x, t.y, a0), one,
+                 imad(prmt(t.z, t.w, a0x), one,
+                 imad(prmt(u.x, u.y, b0), one,
+                 imad(prmt(u.z, u.w, b0x), one, sacc[q][0]))));
+    // codes 4-7
+    sacc[q][1] = imad(prmt(t.x, t.y, a1), one,
+                 imad(prmt(t.z, t.w, a1x), one,
+                 imad(prmt(u.x, u.y, b1), one,
+                 imad(prmt(u.z, u.w, b1x), one, sacc[q][1]))));
+  }
+}
+
+template <int QT>
+__device__ __forceinline__ void widen(uint32_t one, uint32_t (&sacc)[QT][2],
+                                      uint32_t (&acc_a)[QT][2], uint32_t (&acc_o)[QT][2]) {
+#pragma unroll
+  for (int q = 0; q < QT; q++) {
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      acc_a[q][h] = imad(sacc[q][h], one, acc_a[q][h]);
+      acc_o[q][h] = imad(prmt(sacc[q][h], 0, 0x4341), one, acc_o[q][h]);
+      sacc[q][h] = 0;
+    }
+  }
+}
+
+// Lane sums of one chunk, two sub-quantizer pairs per iteration. The code
+// words of the NEXT iteration's two pairs (possibly the first pairs of the
+// warp's next chunk, cw_next) are loaded at the top of the iteration and
+// moved into place at its end, ~170 instructions later, so no L2 latency
+// is exposed and no register move waits on an in-flight load. Groups of D
+// sub-quantizers are summed in bytes (sacc), then widened.
+template <int D, int MC, int QT>
+__device__ __forceinline__ void lane_sums(const uint32_t *__restrict__ cw,
+                                          const uint32_t *__restrict__ cw_next, int m,
+                                          uint32_t tab_sa, uint32_t one, uint32_t (&c)[4],
+                                          uint32_t (&acc_a)[QT][2], uint32_t (&acc_o)[QT][2]) {
+  uint32_t sacc[QT][2];
+#pragma unroll
+  for (int q = 0; q < QT; q++)
+    acc_a[q][0] = acc_a[q][1] = acc_o[q][0] = acc_o[q][1] = sacc[q][0] = sacc[q][1] = 0;
+  if (!MC && m < 4) {  // a single pair per chunk
+    pair_lookups<QT>(__ldg(cw), __ldg(cw + 32), 0, m, tab_sa, one, sacc);
+    widen<QT>(one, sacc, acc_a, acc_o);
+    return;
+  }
+#pragma unroll 1
+  for (int j = 0; j < m; j += 4) {
+    // next iteration: pairs (jn, jn + 2) of this chunk, or of the next one
+    const bool same = j + 4 < m;
+    const uint32_t *base = same ? cw : cw_next;
+    const int jn = same ? j + 4 : 0;
+    const int jn2 = jn + 2 < m ? jn + 2 : jn;  // absent second pair: any valid row
+    const uint32_t n0 = __ldg(base + jn * 32), n1 = __ldg(base + (jn + 1) * 32);
+    const uint32_t n2 = __ldg(base + jn2 * 32), n3 = __ldg(base + (jn2 + 1) * 32);
+    pair_lookups<QT>(c[0], c[1], j, m, tab_sa, one, sacc);
+    if (D == 2) widen<QT>(one, sacc, acc_a, acc_o);
+    const bool second = (MC && MC % 4 == 0) || j + 2 < m;
+    if (second) pair_lookups<QT>(c[2], c[3], j + 2, m, tab_sa, one, sacc);
+    if ((D == 2 && second) || (D != 2 && (((j + 4) % D) == 0 || j + 4 >= m)))
+      widen<QT>(one, sacc, acc_a, acc_o);
+    c[0] = n0;
+    c[1] = n1;
+    c[2] = n2;
+    c[3] = n3;
+  }
+}
+
+// The chunk loop of one work item for a fixed byte-sum depth D: lane sums,
+// then one combined threshold test per query and ONE warp reduction for
+// the whole tile; the per-lane candidate masks are built only for the
+// queries that have a qualifying lane (rare once the bound has converged).
+template <int D, int MC, int QT>
+__device__ __forceinline__ void chunk_loop(const ScanArgs &a, Smem &s, const WorkItem &it,
+                                           uint32_t *wbuf, int m, uint32_t tab_sa,
+                                           uint32_t one, int nq_tile) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int iter = 0;
+  uint32_t ring[4] = {0, 0, 0, 0};  // words of pairs 0 and 1 of the next chunk
+  if (m >= 4 && it.chunk_begin + w < it.chunk_end) {
+    const uint32_t *c0 = a.codes + (size_t)(it.chunk_begin + w) * m * 32 + lane;
+    ring[0] = __ldg(c0);
+    ring[1] = __ldg(c0 + 32);
+    ring[2] = __ldg(c0 + 64);
+    ring[3] = __ldg(c0 + 96);
+  }
+  for (int64_t g = it.chunk_begin + w; g < it.chunk_end; g += kWarps, iter++) {
+    if ((iter & 3) == 3) refresh(a, s, w, nq_tile);
+    const uint32_t valid8 = a.valid[g * 32 + lane];
+    const uint32_t *cw = a.codes + (size_t)g * m * 32 + lane;
+    // no next chunk: prefetch reads this chunk again (valid memory, unused)
+    const uint32_t *cw_next = g + kWarps < it.chunk_end ? cw + (size_t)kWarps * m * 32 : cw;
+    uint32_t acc_a[QT][2], acc_o[QT][2];
+    lane_sums<D, MC, QT>(cw, cw_next, m, tab_sa, one, ring, acc_a, acc_o);
+    // ---- threshold test: 16-bit lanes, bit 15 clear <=> lane <= thr ----
+    uint32_t hitq = 0;
+#pragma unroll
+    for (int q = 0; q < QT; q++) {
+      const unsigned kb = s.kbias[w][q];
+      const uint32_t O0 = acc_o[q][0], E0 = acc_a[q][0] - (O0 << 8);
+      const uint32_t O1 = acc_o[q][1], E1 = acc_a[q][1] - (O1 << 8);
+      const uint32_t all = (E0 + kb) & (O0 + kb) & (E1 + kb) & (O1 + kb);
+      hitq |= ((all & 0x80008000u) != 0x80008000u) ? (1u << q) : 0u;
+    }
+    hitq = __reduce_or_sync(kFull, hitq);
+    if (hitq) {
+      const int chunk_local = (int)(g - it.chunk_begin);
+#pragma unroll
+      for (int q = 0; q < QT; q++) {
+        if (hitq & (1u << q)) {
+          const uint32_t O0 = acc_o[q][0], E0 = acc_a[q][0] - (O0 << 8);
+          const uint32_t O1 = acc_o[q][1], E1 = acc_a[q][1] - (O1 << 8);
+          candidates(a, s, wbuf + q * a.cap_l, w, q, E0, O0, E1, O1, valid8, chunk_local);
+        }
+      }
+    }
+  }
+}
+
 template <int MC, int QT>
-__global__ void __launch_bounds__(kWarps * 32, 5) k_scan(ScanArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 5) k_scan(const __grid_constant__ ScanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Smem s;
   const int m = MC ? MC : a.m;
@@ -337,62 +480,42 @@ __global__ void __launch_bounds__(kWarps * 32, 5) k_scan(ScanArgs a) {
     if (threadIdx.x == 0) {
       s.pair_count = it.pair_count;
       s.chunk_begin = it.chunk_begin;
+      s.depth = 16;
+    }
+    __syncthreads();
+    // byte-sum depth of this tile: the largest D in {16, 8, 4, 2} such that
+    // every aligned group of D sub-quantizers has sum of row maxima <= 255
+    // for every query (D = 2 always holds: entries are <= 127)
+    for (int e = threadIdx.x; e < QT * m; e += blockDim.x) {
+      const uint4 v = s_tab[e];
+      uint32_t mx = __vmaxu4(__vmaxu4(v.x, v.y), __vmaxu4(v.z, v.w));
+      mx = max(max(mx & 255u, (mx >> 8) & 255u), max((mx >> 16) & 255u, mx >> 24));
+      s.rmax[e] = (uint8_t)mx;
+    }
+    __syncthreads();
+    if (threadIdx.x < QT) {
+      const int q = threadIdx.x;
+      int dd = 16;
+      for (; dd > 2; dd >>= 1) {
+        bool ok = true;
+        for (int j0 = 0; j0 < m && ok; j0 += dd) {
+          int sum = 0;
+          for (int j = j0; j < min(j0 + dd, m); j++) sum += s.rmax[q * m + j];
+          ok = sum <= 255;
+        }
+        if (ok) break;
+      }
+      atomicMin(&s.depth, dd);
     }
     __syncthreads();
     const int nq_tile = s.pair_count;
-    // ---- warp loop over chunks ----
-    int iter = 0;
-    for (int64_t g = it.chunk_begin + w; g < it.chunk_end; g += kWarps, iter++) {
-      if ((iter & 3) == 3) refresh(a, s, w, nq_tile);
-      const uint32_t valid8 = a.valid[g * 32 + lane];
-      const uint32_t *cw = a.codes + (size_t)g * m * 32 + lane;
-      uint32_t acc_a[QT][2], acc_o[QT][2];
-#pragma unroll
-      for (int q = 0; q < QT; q++) acc_a[q][0] = acc_a[q][1] = acc_o[q][0] = acc_o[q][1] = 0;
-      // two sub-quantizer pairs per iteration keep the loop body inside the
-      // instruction cache (a fully unrolled body stalls on no_inst); the
-      // next pair's code words are prefetched one iteration ahead
-      uint32_t nw0 = __ldg(cw), nw1 = __ldg(cw + 32);
-#pragma unroll 2
-      for (int j = 0; j < m; j += 2) {
-        const uint32_t w0 = nw0, w1 = nw1;
-        if (j + 2 < m) {
-          nw0 = __ldg(cw + (j + 2) * 32);
-          nw1 = __ldg(cw + (j + 3) * 32);
-        }
-        const uint32_t a0 = w0, a1 = w0 >> 16, a0x = w0 ^ 0x88888888u, a1x = a0x >> 16;
-        const uint32_t b0 = w1, b1 = w1 >> 16, b0x = w1 ^ 0x88888888u, b1x = b0x >> 16;
-#pragma unroll
-        for (int q = 0; q < QT; q++) {
-          const uint4 t = lds128(tab_sa + (uint32_t)((q * m + j) * 16));
-          const uint4 u = lds128(tab_sa + (uint32_t)((q * m + j + 1) * 16));
-          // codes 0-3 of the octet: sub-quantizers j and j+1, both halves
-          const uint32_t s0 = imad(prmt(t.x, t.y, a0), one,
-                              imad(prmt(t.z, t.w, a0x), one,
-                              imad(prmt(u.x, u.y, b0), one, prmt(u.z, u.w, b0x))));
-          // codes 4-7
-          const uint32_t s1 = imad(prmt(t.x, t.y, a1), one,
-                              imad(prmt(t.z, t.w, a1x), one,
-                              imad(prmt(u.x, u.y, b1), one, prmt(u.z, u.w, b1x))));
-          acc_a[q][0] = imad(s0, one, acc_a[q][0]);
-          acc_a[q][1] = imad(s1, one, acc_a[q][1]);
-          acc_o[q][0] = imad(prmt(s0, 0, 0x4341), one, acc_o[q][0]);
-          acc_o[q][1] = imad(prmt(s1, 0, 0x4341), one, acc_o[q][1]);
-        }
-      }
-      // ---- threshold test: 16-bit lanes, bit 15 clear <=> lane <= thr.
-      // One combined test and one vote per query; the per-lane mask is
-      // built only on the rare path. ----
-      const int chunk_local = (int)(g - it.chunk_begin);
-#pragma unroll
-      for (int q = 0; q < QT; q++) {
-        const unsigned kb = s.kbias[w][q];
-        const uint32_t O0 = acc_o[q][0], E0 = acc_a[q][0] - (O0 << 8);
-        const uint32_t O1 = acc_o[q][1], E1 = acc_a[q][1] - (O1 << 8);
-        const uint32_t all = (E0 + kb) & (O0 + kb) & (E1 + kb) & (O1 + kb);
-        if (__any_sync(kFull, (all & 0x80008000u) != 0x80008000u))
-          candidates(a, s, wbuf + q * a.cap_l, w, q, E0, O0, E1, O1, valid8, chunk_local);
-      }
+    const int depth = s.depth;
+    // ---- warp loop over chunks (one specialization per byte-sum depth) ----
+    switch (depth) {
+      case 16: chunk_loop<16, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+      case 8: chunk_loop<8, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+      case 4: chunk_loop<4, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+      default: chunk_loop<2, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
     }
     // ---- end of item: CTA-level bound per query (the R-th smallest value
     // over all four warps' buffers lowers the global M), then publish ----

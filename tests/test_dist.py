@@ -1,0 +1,116 @@
+"""Multi-process merge of per-shard top-R lists (world_size 2, gloo, CPU)
+and the sharded-search semantics on one GPU (two shards of one list)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1704_07355_b200.dist import merge_sorted_lists, merge_topr
+
+
+def _oracle_topr(ids, d, R):
+    out_i = np.full((ids.shape[0], R), -1, np.int64)
+    out_d = np.full((ids.shape[0], R), np.inf, np.float32)
+    for q in range(ids.shape[0]):
+        ok = ids[q] >= 0
+        o = np.lexsort((ids[q][ok], d[q][ok]))[:R]
+        out_i[q, :len(o)] = ids[q][ok][o]
+        out_d[q, :len(o)] = d[q][ok][o]
+    return out_i, out_d
+
+
+def _shard_lists(seed, Q, R, world):
+    """Per-rank (Q, R) ascending lists with heavy distance ties and padding."""
+    rng = np.random.default_rng(seed)
+    ids, ds = [], []
+    for r in range(world):
+        d = np.sort(rng.integers(0, 30, (Q, R)).astype(np.float32), axis=1)
+        i = rng.integers(0, 10**6, (Q, R)).astype(np.int64) * world + r  # disjoint per rank
+        pad = rng.random((Q, R)) < 0.1
+        d = np.where(pad, np.inf, d).astype(np.float32)
+        i = np.where(pad, -1, i)
+        o = np.argsort(d, axis=1, kind="stable")
+        ids.append(np.take_along_axis(i, o, 1))
+        ds.append(np.take_along_axis(d, o, 1))
+    return ids, ds
+
+
+def _worker(rank, world, port, seed, Q, R, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ids, ds = _shard_lists(seed, Q, R, world)
+    gi, gd, gc = merge_topr(torch.from_numpy(ids[rank]), torch.from_numpy(ds[rank]), R)
+    q.put((rank, gi.numpy(), gd.numpy(), gc.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_merge_sorted_lists_matches_lexsort():
+    ids, ds = _shard_lists(3, 16, 50, 3)
+    ai, ad = np.concatenate(ids, 1), np.concatenate(ds, 1)
+    gi, gd, gc = merge_sorted_lists(torch.from_numpy(ai), torch.from_numpy(ad), 50)
+    wi, wd = _oracle_topr(ai, ad, 50)
+    assert np.array_equal(gi.numpy(), wi)
+    assert np.array_equal(gd.numpy(), wd)
+    assert np.array_equal(gc.numpy(), (wi >= 0).sum(1))
+
+
+def test_gloo_world2_merge_equals_global_topr():
+    world, Q, R, seed = 2, 8, 40, 11
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 2000
+    procs = [ctx.Process(target=_worker, args=(r, world, port, seed, Q, R, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ids, ds = _shard_lists(seed, Q, R, world)
+    wi, wd = _oracle_topr(np.concatenate(ids, 1), np.concatenate(ds, 1), R)
+    for _, gi, gd, gc in got:  # every rank holds the same global result
+        assert np.array_equal(gi, wi)
+        assert np.array_equal(gd, wd)
+
+
+@pytest.mark.gpu
+def test_two_shards_with_global_prefix_equal_unsharded(gpu):
+    """Shard a flat list in two ranges on one GPU (sequentially, no waits
+    between ranks): each shard installs the global prefix, only shard 0
+    keeps F_sat; the merged result equals the unsharded search bit for bit,
+    including saturated first-R lanes and qmax from the global prefix."""
+    from paper_1704_07355_b200.device import DeviceIndex
+    from paper_1704_07355_b200.ivf import encode_device
+    from paper_1704_07355_b200.workload import _PQ
+    rng = np.random.default_rng(21)
+    n, m, d, R, init = 120_000, 16, 64, 100, 1000
+    cb = (rng.random((m, 16, d // m)) * 40).astype(np.float32)
+    pq = _PQ(cb)
+    X = torch.from_numpy((rng.random((n, d)) * 40).astype(np.float32)).cuda()
+    codes = encode_device(pq, X)
+    cbt = torch.from_numpy(cb).cuda()
+    full = DeviceIndex.from_device_rows(d, m, codes, torch.tensor([0, n], device="cuda"), cbt)
+    qs = (rng.random((32, d)) * 40).astype(np.float32)
+    want = full.search(qs, R, init=init)
+    cut = 70_001
+    parts = []
+    for k, (lo, hi) in enumerate([(0, cut), (cut, n)]):
+        sh = DeviceIndex.from_device_rows(
+            d, m, codes[lo:hi].contiguous(), torch.tensor([0, hi - lo], device="cuda"), cbt,
+            ids=torch.arange(lo, hi, dtype=torch.int64, device="cuda"))
+        p = max(init, R)
+        sh.set_prefix(codes[:p].contiguous(), torch.tensor([0, p], device="cuda"), [n],
+                      ids=torch.arange(p, dtype=torch.int64, device="cuda"))
+        parts.append(sh.search(qs, R, init=init, with_fsat=(k == 0)))
+    gi, gd, gc = merge_sorted_lists(torch.from_numpy(np.concatenate([p.ids for p in parts], 1)),
+                                    torch.from_numpy(np.concatenate([p.distances for p in parts],
+                                                                    1)), R)
+    assert np.array_equal(gi.numpy(), want.ids)
+    assert np.array_equal(gd.numpy().view(np.uint32), want.distances.view(np.uint32))
+    assert np.array_equal(gc.numpy(), want.counts)
