@@ -37,7 +37,13 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "Quick ADC codes scanned/s (whole job) at configs[1]: exhaustive, m=32x4-bit, N=1e7/GPU, Q=1000, R=100"
+METRICS = {
+    "cfg0": "Quick ADC codes scanned/s (whole job) at configs[0]: exhaustive, m=16x4-bit, N=1e6, Q=100, R=100",
+    "cfg1": "Quick ADC codes scanned/s (whole job) at configs[1]: exhaustive, m=32x4-bit, N=1e7/GPU, Q=1000, R=100",
+    "cfg2": "Quick ADC codes scanned/s (whole job) at configs[2]: IVF K=4096 + OPQ, m=32x4-bit, Q=1e4, R=100",
+    "cfg3": "Quick ADC codes scanned/s (whole job) at configs[3]: exhaustive, d=960, m=32x4-bit, N=1e6, Q=1000, R=100",
+}
+METRIC = METRICS["cfg1"]
 UNIT = "codes/s"
 
 
@@ -47,7 +53,8 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg3"])
+    p.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3"])
+    p.add_argument("--nprobe", type=int, default=None, help="IVF configs: probed cells (ma)")
     p.add_argument("--n", type=int, default=None, help="codes per GPU (default: the config's N)")
     p.add_argument("--queries", type=int, default=None)
     p.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -59,7 +66,7 @@ def parse():
 # ---------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """SM clock and throttle reasons sampled (NVML, every 20 ms) during the
+    """SM clock and throttle reasons sampled (NVML, every 100 ms) during the
     timed region; falls back to nvidia-smi if NVML is unavailable."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
@@ -82,7 +89,7 @@ class ClockSampler:
                 self.mx.append(mx)
                 r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.reasons.update(v for k, v in self.REASONS.items() if r & k)
-                self._stop.wait(0.02)
+                self._stop.wait(0.1)
         except Exception:
             while not self._stop.is_set():
                 try:
@@ -167,6 +174,50 @@ def cpu_reference_run(cfg, codes_np, n, qs, R, init, seconds, nthreads=None):
             kind, nthreads, (oi, od, on), wall)
 
 
+def flat_lists(codes_np, ids_np, row_off):
+    """Reference-layout (blocks, blk_off, ids, count) of row-ordered lists."""
+    from paper_1704_07355_b200.qadc import transpose_list
+
+    blocks, ids, boff, count = [], [], [0], []
+    for L in range(row_off.shape[0] - 1):
+        a, b = int(row_off[L]), int(row_off[L + 1])
+        tl = transpose_list(codes_np[a:b], ids_np[a:b])
+        blocks.append(tl.blocks.reshape(-1))
+        ids.append(tl.ids)
+        boff.append(boff[-1] + tl.blocks.shape[0])
+        count.append(tl.count)
+    return (np.concatenate(blocks), np.asarray(boff, np.int64), np.concatenate(ids),
+            np.asarray(count, np.int64))
+
+
+def cpu_reference_run_ivf(cfg, pq, coarse, codes_np, ids_np, row_off, qs, R, init, ma, seconds,
+                          nthreads=None):
+    """IVF variant of cpu_reference_run: probe, OPQ rotation, tables, qmax
+    and quantization restated (oracle/), block scan = the reference's own
+    compiled qadc_scan_u8 (oracle/_ref)."""
+    from oracle import oracle as orc
+
+    flat = flat_lists(codes_np, ids_np, row_off)
+    use_ref = orc.ref_lib() is not None
+    nthreads = nthreads or os.cpu_count() or 1
+    probe = qs[: max(1, min(nthreads, qs.shape[0]))]
+    t0 = time.perf_counter()
+    orc.search_batch(probe, pq.codebooks, pq.rotation, coarse, ma, flat, R, init,
+                     use_ref_scan=use_ref, nthreads=nthreads)
+    per_q = (time.perf_counter() - t0) / probe.shape[0]
+    nq = int(max(probe.shape[0], min(qs.shape[0], seconds / max(per_q, 1e-6))))
+    sample = qs[:nq]
+    t0 = time.perf_counter()
+    oi, od, on, _ = orc.search_batch(sample, pq.codebooks, pq.rotation, coarse, ma, flat, R, init,
+                                     use_ref_scan=use_ref, nthreads=nthreads)
+    wall = time.perf_counter() - t0
+    sizes = np.diff(flat[1]) * 16
+    cells = np.array([orc.probe(coarse, q, ma)[0] for q in sample])
+    codes_scanned = int(np.asarray(flat[3])[cells].sum())
+    return (codes_scanned / wall, f"{nq} of {qs.shape[0]} queries, nprobe={ma}",
+            "reference" if use_ref else "port", nthreads, (oi, od, on), wall)
+
+
 # ---------------------------------------------------------------- arms
 
 def run_b200(args):
@@ -184,19 +235,29 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     _native.require_device()
-    cfg = CONFIGS[args.config]
+    from paper_1704_07355_b200.workload import IVF_CONFIGS, build_ivf_index, load_ivf_model
+    ivf_cfg = IVF_CONFIGS.get(args.config)
+    cfg = ivf_cfg or CONFIGS[args.config]
     n = args.n or cfg.n
     nq = args.queries or cfg.q
     R, init = cfg.R, cfg.init
-    pq = load_pq(cfg)
-    index, codes = build_shard_index(cfg, pq, n, rank, world, prefix=max(init, R))
+    ma = 1
+    if ivf_cfg is not None:
+        if world > 1:
+            raise SystemExit("IVF list sharding across ranks is not wired into bench.py yet")
+        ma = args.nprobe or ivf_cfg.nprobe
+        pq, coarse = load_ivf_model(ivf_cfg)
+        index, sizes, codes, order, row_off = build_ivf_index(ivf_cfg, pq, coarse, n)
+    else:
+        pq = load_pq(cfg)
+        index, codes = build_shard_index(cfg, pq, n, rank, world, prefix=max(init, R))
     qs = queries(cfg, nq)
     q_dev = torch.from_numpy(qs).cuda()
     q_pin = torch.from_numpy(qs).pin_memory()
     torch.cuda.synchronize()
 
     def step_device():
-        res = index.search(q_dev, R, init=init, with_fsat=(rank == 0))
+        res = index.search(q_dev, R, ma=ma, init=init, with_fsat=(rank == 0))
         gi, gd, _ = merge_topr(res.ids, res.distances, R)
         return (gi, gd), res
 
@@ -238,7 +299,7 @@ def run_b200(args):
     # ---- end-to-end through the public API with host buffers ----
     def step_e2e():
         qd = q_pin.to("cuda", non_blocking=True)
-        res = index.search(qd, R, init=init, with_fsat=(rank == 0))
+        res = index.search(qd, R, ma=ma, init=init, with_fsat=(rank == 0))
         gi, gd, _ = merge_topr(res.ids, res.distances, R)
         return gi.to("cpu"), gd.to("cpu")
 
@@ -255,7 +316,10 @@ def run_b200(args):
     barrier()
     ms_e2e = max_over_ranks(e2.elapsed_time(e3) / args.steps)
 
-    total_codes = nq * n * world
+    # codes scanned per step = sum over (query, probed list) of len(list),
+    # counted by the library (stats["codes"]); all ranks together
+    per_rank_codes = codes_scanned / args.steps
+    total_codes = per_rank_codes * world if ivf_cfg is None else per_rank_codes
     value = total_codes / (ms_dev * 1e-3)
     e2e_value = total_codes / (ms_e2e * 1e-3)
 
@@ -267,7 +331,8 @@ def run_b200(args):
     lookups = (codes_scanned / args.steps) * pq.m  # per launch, this rank
     achieved = lookups / scan_s / 1e9
     pk = measured_peaks()
-    hbm_bytes = n * pq.m / 2  # codes read once per batch (exhaustive)
+    # codes of every DISTINCT list touched once per batch
+    hbm_bytes = n * pq.m / 2
     roof = {
         "bound": "int",
         "achieved": round(achieved, 2),
@@ -287,13 +352,16 @@ def run_b200(args):
     out = None
     if rank == 0:
         out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (BASELINE mixture generator drawn on GPU; reference-trained PQ)",
             "config": {"workload": cfg.name, "N_per_gpu": n, "N_total": n * world, "Q": nq,
-                       "R": R, "init": init, "m": pq.m, "d": pq.d,
-                       "l2": "inputs larger than L2 (codes %.0f MB > 126 MB)" % (n * pq.m / 2e6)},
+                       "R": R, "init": init, "m": pq.m, "d": pq.d, "nprobe": ma,
+                       "codes_scanned_per_step": int(total_codes),
+                       "l2": "inputs larger than L2 (codes %.0f MB > 126 MB)" % (n * pq.m / 2e6)
+                       if n * pq.m / 2 > 126e6 else
+                       "index %.0f MB fits L2: steady-state (L2-warm) throughput" % (n * pq.m / 2e6)},
             "qps": nq / (ms_dev * 1e-3),
             "e2e": {"value": e2e_value, "unit": UNIT, "qps": nq / (ms_e2e * 1e-3),
                     "ms_per_step": ms_e2e, "h2d_bytes_per_step": int(nq * pq.d * 4),
@@ -306,8 +374,13 @@ def run_b200(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             codes_np = codes.cpu().numpy()
-            v, sample, kind, cores, (oi, od, on), wall = cpu_reference_run(
-                cfg, codes_np, n, qs, R, init, args.cpu_seconds)
+            if ivf_cfg is not None:
+                v, sample, kind, cores, (oi, od, on), wall = cpu_reference_run_ivf(
+                    ivf_cfg, pq, coarse, codes_np, order.cpu().numpy(), row_off.cpu().numpy(),
+                    qs, R, init, ma, args.cpu_seconds)
+            else:
+                v, sample, kind, cores, (oi, od, on), wall = cpu_reference_run(
+                    cfg, codes_np, n, qs, R, init, args.cpu_seconds)
             k = oi.shape[0]
             gi_np, gd_np = out_i.numpy()[:k], out_d.numpy()[:k]
             exact = int(sum(np.array_equal(gi_np[i], oi[i]) and
@@ -353,7 +426,7 @@ def run_reference(args):
             walls.append(wall)
     value = statistics.median(vals)
     return {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(walls) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8",

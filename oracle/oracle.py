@@ -51,6 +51,7 @@ def lib():
         L.orc_sum_f32.argtypes = [_f32p, c_int]
         L.orc_compute_tables.argtypes = [_f32p, c_int, c_int, _f32p, _f32p]
         L.orc_probe.argtypes = [_f32p, c_int, c_int, _f32p, c_int, _i64p, _f32p]
+        L.orc_rotate.argtypes = [_f32p, c_int, _f32p, _f32p]
         L.orc_find_qmax.restype = c_float
         L.orc_find_qmax.argtypes = [_f32p, c_int, _u8p, c_int64, c_int, c_int]
         L.orc_quantize_tables.restype = c_double
@@ -118,6 +119,14 @@ def probe(cent, q, ma):
     lib().orc_probe(_p(cent, c_float), K, d, _p(q, c_float), ma, _p(cells, c_int64),
                     _p(res, c_float))
     return cells, res
+
+
+def rotate(R, v):
+    R = np.ascontiguousarray(R, np.float32)
+    v = np.ascontiguousarray(v, np.float32).ravel()
+    out = np.empty_like(v)
+    lib().orc_rotate(_p(R, c_float), v.shape[0], _p(v, c_float), _p(out, c_float))
+    return out
 
 
 def find_qmax(tables, blocks, count, R, init) -> float:

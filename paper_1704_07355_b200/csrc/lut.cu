@@ -401,8 +401,10 @@ __global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ cod
     const int64_t c0 = chunk_off[L], n = lanes[L];
     const float qmin = qmin_f[pair], delta = delta_f[pair];
     // bound prefix of cell 0: at least init codes, and up to kBoundPrefix
-    // so the initial bound starts near the R/kBoundPrefix quantile
-    const int64_t want = (int64_t)(init > kBoundPrefix ? init : kBoundPrefix);
+    // (at most 1/64 of the list) so the initial bound starts near the
+    // R/prefix quantile without costing more than ~2% of the scan
+    int64_t want = n / 64 < kBoundPrefix ? n / 64 : kBoundPrefix;
+    if (want < init) want = init;
     const int64_t pref = (s == 0) ? (want < n ? want : n) : 0;
     for (int e = threadIdx.x; e < m * 4; e += blockDim.x)
       ((uint32_t *)sqt)[e] = qt[(size_t)pair * m * 4 + e];

@@ -23,6 +23,7 @@
 //    are appended to a per-query global candidate list; select.cu picks
 //    the exact top-R by (midpoint, id).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -426,7 +427,8 @@ __device__ __forceinline__ void chunk_loop(const ScanArgs &a, Smem &s, const Wor
 }
 
 template <int MC, int QT>
-__global__ void __launch_bounds__(kWarps * 32, 5) k_scan(const __grid_constant__ ScanArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, QT >= 16 ? 3 : (QT >= 8 ? 5 : 6))
+k_scan(const __grid_constant__ ScanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Smem s;
   const int m = MC ? MC : a.m;
@@ -663,16 +665,31 @@ __global__ void k_emit_items(const int *__restrict__ list_pairs, const int *__re
 
 }  // namespace
 
-int scan_qt_per_cta(int m) { return m <= 64 ? 8 : 4; }
+// Queries per tile: 8 by default (selector construction amortized over 8
+// queries at 96 registers, 5 CTAs/SM); QADC_B200_QT=4|16 overrides (tuning).
+int scan_qt_per_cta(int m) {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("QADC_B200_QT");
+    env = e ? atoi(e) : 0;
+  }
+  if (env == 4 || env == 8 || env == 16) return (m > 64 && env > 4) ? 4 : env;
+  return m <= 64 ? 8 : 4;
+}
 
 void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st) {
   const int qt = scan_qt_per_cta(a.m);
-  if (qt == 8) {
+  if (qt == 16) {
+    if (a.m == 32) launch_t<32, 16>(a, nsm, st);
+    else launch_t<0, 16>(a, nsm, st);
+  } else if (qt == 8) {
     if (a.m == 16) launch_t<16, 8>(a, nsm, st);
     else if (a.m == 32) launch_t<32, 8>(a, nsm, st);
     else launch_t<0, 8>(a, nsm, st);
   } else {
-    launch_t<0, 4>(a, nsm, st);
+    if (a.m == 16) launch_t<16, 4>(a, nsm, st);
+    else if (a.m == 32) launch_t<32, 4>(a, nsm, st);
+    else launch_t<0, 4>(a, nsm, st);
   }
 }
 

@@ -35,8 +35,8 @@ def merge_topr(ids: torch.Tensor, dists: torch.Tensor, R: int, group=None):
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    if world == 1:
-        return merge_sorted_lists(ids, dists, R)
+    if world == 1:  # a single shard's list is already the exact top-R
+        return ids, dists, (ids >= 0).sum(dim=1).to(torch.int32)
     gi = [torch.empty_like(ids) for _ in range(world)]
     gd = [torch.empty_like(dists) for _ in range(world)]
     dist.all_gather(gi, ids.contiguous(), group=group)

@@ -102,3 +102,67 @@ def build_shard_index(cfg: FlatConfig, pq: _PQ, n: int, rank: int, world: int, p
         index.set_prefix(head.contiguous(), torch.tensor([0, p], dtype=torch.int64, device=dev),
                          [world * n], ids=torch.arange(p, dtype=torch.int64, device=dev))
     return index, codes
+
+
+# ------------------------------------------------------------------ IVF
+
+
+@dataclass(frozen=True)
+class IvfConfig:
+    name: str
+    mix: datagen.Mixture
+    m: int
+    n: int
+    q: int
+    R: int
+    init: int
+    K: int
+    nprobe: int
+    coarse_file: str
+    codebooks_file: str
+    rotation_file: str
+
+
+IVF_CONFIGS = {
+    "cfg2": IvfConfig("cfg2_ivf_opq_K4096_m32_N1e8_Q1e4", datagen.SIFT_LIKE, 32, 100_000_000,
+                      10_000, 100, 1000, 4096, 16, "cfg2_coarse_K4096.npy",
+                      "cfg2_m32_codebooks.npy", "cfg2_rotation.npy"),
+}
+
+
+def load_ivf_model(cfg: IvfConfig):
+    pq = _PQ(np.load(BENCH_DATA / cfg.codebooks_file), np.load(BENCH_DATA / cfg.rotation_file))
+    return pq, np.load(BENCH_DATA / cfg.coarse_file)
+
+
+def build_ivf_index(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, shard: int = 0,
+                    device="cuda", chunk: int = 1 << 22):
+    """IVF index of n base vectors drawn on the GPU: coarse assignment,
+    residual, OPQ rotation + PQ encoding (GPU encoder), lists with ids
+    ascending (ivf.py:109-151). Returns the DeviceIndex and the list sizes."""
+    import torch
+
+    from .ivf import assign_device, encode_device
+
+    C = torch.from_numpy(np.ascontiguousarray(coarse, dtype=np.float32)).to(device)
+    codes = torch.empty((n, pq.m // 2), dtype=torch.uint8, device=device)
+    labels = torch.empty(n, dtype=torch.int64, device=device)
+    for c0 in range(0, n, chunk):
+        k = min(chunk, n - c0)
+        X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + shard,
+                                  stream=datagen.STREAM_BASE * 100 + c0 // chunk, device=device)
+        lab = assign_device(coarse, X)
+        labels[c0:c0 + k] = lab
+        codes[c0:c0 + k] = encode_device(pq, X - C[lab])
+        del X
+    order = torch.argsort(labels, stable=True)
+    sizes = torch.bincount(labels, minlength=C.shape[0])
+    row_off = torch.zeros(C.shape[0] + 1, dtype=torch.int64, device=device)
+    row_off[1:] = torch.cumsum(sizes, 0)
+    sorted_codes = codes[order].contiguous()
+    del codes, labels
+    index = DeviceIndex.from_device_rows(
+        pq.d, pq.m, sorted_codes, row_off, torch.from_numpy(pq.codebooks).to(device),
+        rotation=torch.from_numpy(np.ascontiguousarray(pq.rotation, np.float32)).to(device),
+        coarse=C, ids=order + shard * n)
+    return index, sizes.cpu().numpy(), sorted_codes, order, row_off
