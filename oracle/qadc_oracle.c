@@ -120,15 +120,19 @@ void orc_probe(const float *cent, int K, int d, const float *q, int ma,
     free(bd);
 }
 
-/* adc.py:108-111, sequential order (see header: not OpenBLAS-exact). */
+/* adc.py:108-111 (v @ R^T). OpenBLAS sgemv's summation order is not
+ * reproducible, so the restatement accumulates in float64 and
+ * rounds once — the same arithmetic as the GPU kernel (k_residual_lut), so
+ * native-OPQ GPU results can be checked bit-exactly against this port while
+ * both differ from OpenBLAS by rare low-bit flips. */
 void orc_rotate(const float *R, int d, const float *v, float *out)
 {
     int i, k;
     for (i = 0; i < d; i++) {
-        float acc = 0.0f;
+        double acc = 0.0;
         for (k = 0; k < d; k++)
-            acc = acc + R[(size_t)i * d + k] * v[k];
-        out[i] = acc;
+            acc += (double)R[(size_t)i * d + k] * (double)v[k];
+        out[i] = (float)acc;
     }
 }
 

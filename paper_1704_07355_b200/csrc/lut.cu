@@ -86,18 +86,22 @@ __global__ void k_tables(const float *__restrict__ codebooks, int m, int dsub,
 }
 
 // ---------------- probe (ivf.py:166-182) ----------------
-// One CTA per query. Coarse distances in einsum order from the transposed
-// centroid array (coalesced), keys (d2 bits << 32 | cell) so lexsort's
-// (d2, cell) order is plain u64 order (d2 >= 0). The ma smallest keys are
-// found per tile of up to 4096 cells by an MSB radix select in shared
-// memory, candidates of all tiles are merged by a final select, and the
-// winners are sorted.
-constexpr int kProbeTile = 4096;
+// kProbeQ queries per CTA share every centroid load (coalesced reads of the
+// transposed centroid array, reused from registers for all queries of the
+// CTA). Coarse distances follow NumPy's einsum order exactly; keys are
+// (d2 bits << 32 | cell), so lexsort((cell, d2)) order is plain u64 order
+// (d2 >= 0). Per tile of kProbeTile cells each query's ma smallest keys are
+// found by an MSB radix select in shared memory and merged into a running
+// best-ma set; the winners are sorted at the end.
+constexpr int kProbeQ = 8;
+constexpr int kProbeTile = 2048;
 constexpr int kBoundPrefix = 16384;
 
+// k-th smallest (1-based) of n keys; the 256-bin digit search runs on warp 0
+// with shuffles instead of a serial scan.
 __device__ uint64_t block_kth_u64(const uint64_t *keys, int n, int k, unsigned *hist,
                                   uint64_t *s_prefix, int *s_k) {
-  // returns the k-th smallest (1-based) key among keys[0..n)
+  const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) { *s_prefix = 0; *s_k = k; }
   __syncthreads();
   for (int shift = 56; shift >= 0; shift -= 8) {
@@ -110,14 +114,29 @@ __device__ uint64_t block_kth_u64(const uint64_t *keys, int n, int k, unsigned *
       if ((key & hmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int kk = *s_k, dgt = 0;
-      for (; dgt < 256; dgt++) {
-        if ((int)hist[dgt] >= kk) break;
-        kk -= hist[dgt];
+    if (threadIdx.x < 32) {
+      unsigned c = 0;
+#pragma unroll
+      for (int i = 0; i < 8; i++) c += hist[lane * 8 + i];
+      unsigned incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
-      *s_k = kk;
-      *s_prefix = prefix | ((uint64_t)dgt << shift);
+      const unsigned kk = (unsigned)*s_k;
+      const unsigned hit = __ballot_sync(0xffffffffu, incl >= kk);
+      const int src = __ffs(hit) - 1;
+      if (lane == src) {
+        unsigned cum = incl - c;
+        int dgt = lane * 8;
+        for (int i = 0; i < 8; i++, dgt++) {
+          if (cum + hist[dgt] >= kk) break;
+          cum += hist[dgt];
+        }
+        *s_k = (int)(kk - cum);
+        *s_prefix = prefix | ((uint64_t)dgt << shift);
+      }
     }
     __syncthreads();
   }
@@ -141,54 +160,104 @@ __device__ void block_sort_u64(uint64_t *keys, int n_pow2) {
 }
 
 __global__ void __launch_bounds__(512) k_probe(const float *__restrict__ coarseT, int K, int d,
-                                               const float *__restrict__ queries, int ma,
+                                               const float *__restrict__ queries, int nq, int ma,
                                                int64_t *__restrict__ cells) {
-  extern __shared__ unsigned char smem[];
-  float *sq = (float *)smem;                                   // d
-  uint64_t *keys = (uint64_t *)(smem + ((d * 4 + 15) & ~15));  // kProbeTile
-  uint64_t *cand = keys + kProbeTile;                          // ntiles * ma (<= 16 * 64)
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t *keys = (uint64_t *)smem;                         // [kProbeQ][kProbeTile]
+  uint64_t *best = keys + (size_t)kProbeQ * kProbeTile;      // [kProbeQ][2 * ma]
+  float *sq = (float *)(best + (size_t)kProbeQ * 2 * ma);    // [kProbeQ][d]
   __shared__ unsigned hist[256];
   __shared__ uint64_t s_prefix;
-  __shared__ int s_k, s_nc;
-  const int q = blockIdx.x;
-  for (int t = threadIdx.x; t < d; t += blockDim.x) sq[t] = queries[(size_t)q * d + t];
-  if (threadIdx.x == 0) s_nc = 0;
+  __shared__ int s_k, s_nb[kProbeQ];
+  const int q0 = blockIdx.x * kProbeQ;
+  const int nqb = min(kProbeQ, nq - q0);
+  for (int e = threadIdx.x; e < kProbeQ * d; e += blockDim.x) {
+    const int q = e / d;
+    sq[e] = q < nqb ? queries[(size_t)(q0 + q) * d + (e - q * d)] : 0.f;
+  }
+  if (threadIdx.x < kProbeQ) s_nb[threadIdx.x] = 0;
   __syncthreads();
   for (int base = 0; base < K; base += kProbeTile) {
     const int n = min(kProbeTile, K - base);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int k = base + i;
-      const float d2 = einsum_sq([&](int t) { return coarseT[(size_t)t * K + k]; }, sq, d);
-      keys[i] = ((uint64_t)__float_as_uint(d2) << 32) | (uint32_t)k;
+      float acc[kProbeQ][4];
+#pragma unroll
+      for (int q = 0; q < kProbeQ; q++) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+      // einsum order (see einsum_sq): blocks of 16 as v3..v0, tail in 4s
+      int t0 = 0;
+      for (; d - t0 >= 16; t0 += 16) {
+#pragma unroll
+        for (int v = 3; v >= 0; v--) {
+#pragma unroll
+          for (int l = 0; l < 4; l++) {
+            const int t = t0 + 4 * v + l;
+            const float c = coarseT[(size_t)t * K + k];
+#pragma unroll
+            for (int q = 0; q < kProbeQ; q++) {
+              const float df = __fsub_rn(c, sq[q * d + t]);
+              acc[q][l] = __fadd_rn(acc[q][l], __fmul_rn(df, df));
+            }
+          }
+        }
+      }
+      for (; t0 < d; t0 += 4) {
+#pragma unroll
+        for (int l = 0; l < 4; l++) {
+          const int t = t0 + l;
+          const float c = t < d ? coarseT[(size_t)t * K + k] : 0.f;
+#pragma unroll
+          for (int q = 0; q < kProbeQ; q++) {
+            float pr = 0.f;
+            if (t < d) {
+              const float df = __fsub_rn(c, sq[q * d + t]);
+              pr = __fmul_rn(df, df);
+            }
+            acc[q][l] = __fadd_rn(acc[q][l], pr);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kProbeQ; q++) {
+        const float d2 = __fadd_rn(__fadd_rn(acc[q][0], acc[q][1]), __fadd_rn(acc[q][2], acc[q][3]));
+        keys[(size_t)q * kProbeTile + i] = ((uint64_t)__float_as_uint(d2) << 32) | (uint32_t)k;
+      }
     }
     __syncthreads();
-    const int take = min(ma, n);
-    const uint64_t kth = block_kth_u64(keys, n, take, hist, &s_prefix, &s_k);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      if (keys[i] <= kth) {
-        const int p = atomicAdd(&s_nc, 1);
-        cand[p] = keys[i];
+    for (int q = 0; q < nqb; q++) {
+      uint64_t *kq = keys + (size_t)q * kProbeTile;
+      uint64_t *bq = best + (size_t)q * 2 * ma;
+      const int take = min(ma, n);
+      const uint64_t kth = block_kth_u64(kq, n, take, hist, &s_prefix, &s_k);
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (kq[i] <= kth) bq[atomicAdd(&s_nb[q], 1)] = kq[i];
+      __syncthreads();
+      const int nb = s_nb[q];
+      if (nb > ma) {  // keep the ma smallest of the running set (keys unique)
+        const uint64_t k2 = block_kth_u64(bq, nb, ma, hist, &s_prefix, &s_k);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          int w = 0;
+          for (int i = 0; i < nb; i++)
+            if (bq[i] <= k2) bq[w++] = bq[i];
+          s_nb[q] = w;
+        }
+        __syncthreads();
       }
     }
     __syncthreads();
   }
-  // final: ma smallest among candidates (keys are unique)
-  const int nc = s_nc;
-  const uint64_t kth = block_kth_u64(cand, nc, ma, hist, &s_prefix, &s_k);
-  __syncthreads();
-  // gather winners into keys[0..ma), pad, sort
-  if (threadIdx.x == 0) s_nc = 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < nc; i += blockDim.x)
-    if (cand[i] <= kth) keys[atomicAdd(&s_nc, 1)] = cand[i];
-  __syncthreads();
   int p2 = 1;
   while (p2 < ma) p2 <<= 1;
-  for (int i = ma + threadIdx.x; i < p2; i += blockDim.x) keys[i] = ~0ull;
-  __syncthreads();
-  block_sort_u64(keys, p2);
-  for (int i = threadIdx.x; i < ma; i += blockDim.x)
-    cells[(size_t)q * ma + i] = (int64_t)(keys[i] & 0xffffffffu);
+  for (int q = 0; q < nqb; q++) {
+    uint64_t *bq = best + (size_t)q * 2 * ma;
+    for (int i = ma + threadIdx.x; i < p2; i += blockDim.x) bq[i] = ~0ull;
+    __syncthreads();
+    block_sort_u64(bq, p2);
+    for (int i = threadIdx.x; i < ma; i += blockDim.x)
+      cells[(size_t)(q0 + q) * ma + i] = (int64_t)(bq[i] & 0xffffffffu);
+    __syncthreads();
+  }
 }
 
 // ---------------- residual + rotation + LUT (adc.py:108-111, 141-148,
@@ -197,39 +266,57 @@ __global__ void __launch_bounds__(512) k_probe(const float *__restrict__ coarseT
 // rotation y = R r accumulated in float64 and rounded once (the reference
 // uses OpenBLAS sgemv whose order is unpinned: rotated
 // configs are "native OPQ" parity with counted bucket flips).
-__global__ void k_residual_lut(const float *__restrict__ queries, const float *__restrict__ coarse,
-                               const float *__restrict__ rotation,
-                               const float *__restrict__ codebooks, const int64_t *__restrict__ cells,
-                               int d, int m, int nslots, float *__restrict__ lut) {
+constexpr int kLutPairs = 16;  // (query, slot) pairs per CTA
+
+// kLutPairs (query, slot) pairs per CTA so the rotation matrix is staged
+// in shared memory once (transposed: conflict-free column reads) and
+// reused by every pair of the CTA.
+__global__ void __launch_bounds__(256) k_residual_lut(
+    const float *__restrict__ queries, const float *__restrict__ coarse,
+    const float *__restrict__ rotation, const float *__restrict__ codebooks,
+    const int64_t *__restrict__ cells, int d, int m, int nslots, int npairs, int rot_in_smem,
+    float *__restrict__ lut) {
   extern __shared__ float sm[];
-  float *sr = sm, *sy = sm + d;
-  const int pair = blockIdx.x;
-  const int q = pair / nslots;
-  const float *qp = queries + (size_t)q * d;
-  if (coarse) {
-    const int64_t c = cells[pair];
-    for (int t = threadIdx.x; t < d; t += blockDim.x)
-      sr[t] = __fsub_rn(qp[t], coarse[(size_t)c * d + t]);
-  } else {
-    for (int t = threadIdx.x; t < d; t += blockDim.x) sr[t] = qp[t];
+  float *sr = sm;                            // [kLutPairs][d] residuals
+  float *sy = sm + kLutPairs * d;            // [kLutPairs][d] rotated
+  float *rt = sm + 2 * kLutPairs * d;        // [d][d] R^T (if staged)
+  const int p0 = blockIdx.x * kLutPairs;
+  const int np = min(kLutPairs, npairs - p0);
+  for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
+    const int p = e / d, t = e - p * d;
+    const int pair = p0 + p;
+    const float qv = queries[(size_t)(pair / nslots) * d + t];
+    sr[e] = coarse ? __fsub_rn(qv, coarse[(size_t)cells[pair] * d + t]) : qv;
   }
+  if (rotation && rot_in_smem)
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+      const int i = e / d, k = e - i * d;
+      rt[k * d + i] = rotation[e];
+    }
   __syncthreads();
   const float *y = sr;
   if (rotation) {
-    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
+      const int p = e / d, i = e - p * d;
+      const float *r = sr + p * d;
       double acc = 0.0;
-      for (int k = 0; k < d; k++) acc += (double)rotation[(size_t)i * d + k] * (double)sr[k];
-      sy[i] = (float)acc;
+      if (rot_in_smem) {
+        for (int k = 0; k < d; k++) acc += (double)rt[k * d + i] * (double)r[k];
+      } else {
+        for (int k = 0; k < d; k++) acc += (double)rotation[(size_t)i * d + k] * (double)r[k];
+      }
+      sy[e] = (float)acc;
     }
     __syncthreads();
     y = sy;
   }
   const int dsub = d / m;
-  for (int e = threadIdx.x; e < m * 16; e += blockDim.x) {
-    const int j = e >> 4;
-    const float *cb = codebooks + (size_t)e * dsub;
-    lut[(size_t)pair * m * 16 + e] =
-        einsum_sq([&](int t) { return cb[t]; }, y + (size_t)j * dsub, dsub);
+  for (int e = threadIdx.x; e < np * m * 16; e += blockDim.x) {
+    const int p = e / (m * 16), ent = e - p * m * 16;
+    const int j = ent >> 4;
+    const float *cb = codebooks + (size_t)ent * dsub;
+    lut[(size_t)(p0 + p) * m * 16 + ent] =
+        einsum_sq([&](int t) { return cb[t]; }, y + (size_t)p * d + (size_t)j * dsub, dsub);
   }
 }
 
@@ -477,19 +564,24 @@ void launch_compute_tables(const float *codebooks, int m, int dsub, const float 
 void launch_probe(const float *coarseT, int K, int d, const float *queries, int nq, int ma,
                   int64_t *cells, cudaStream_t st) {
   if (nq <= 0) return;
-  const int ntiles = (K + kProbeTile - 1) / kProbeTile;
-  size_t smem = ((size_t)d * 4 + 15) / 16 * 16 + (size_t)kProbeTile * 8 + (size_t)ntiles * ma * 8;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_probe<<<nq, 512, smem, st>>>(coarseT, K, d, queries, ma, cells);
+  int p2 = 1;
+  while (p2 < ma) p2 <<= 1;
+  const size_t smem = (size_t)kProbeQ * kProbeTile * 8 + (size_t)kProbeQ * 2 * std::max(ma, p2) * 8 +
+                      (size_t)kProbeQ * d * 4;
+  cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_probe<<<(nq + kProbeQ - 1) / kProbeQ, 512, smem, st>>>(coarseT, K, d, queries, nq, ma, cells);
 }
 
 void launch_residual_lut(const qadc_b200_index *idx, const float *queries, const int64_t *cells,
                          int nq, int nslots, float *lut, cudaStream_t st) {
   if (nq <= 0) return;
-  k_residual_lut<<<nq * nslots, 256, (size_t)idx->d * 8, st>>>(
-      queries, idx->K ? idx->coarse : nullptr, idx->rotation, idx->codebooks, cells, idx->d,
-      idx->m, nslots, lut);
+  const int npairs = nq * nslots, d = idx->d;
+  const int rot_smem = idx->rotation && (size_t)d * d * 4 <= 64 * 1024;
+  const size_t smem = (size_t)2 * kLutPairs * d * 4 + (rot_smem ? (size_t)d * d * 4 : 0);
+  cudaFuncSetAttribute(k_residual_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_residual_lut<<<(npairs + kLutPairs - 1) / kLutPairs, 256, smem, st>>>(
+      queries, idx->K ? idx->coarse : nullptr, idx->rotation, idx->codebooks, cells, d, idx->m,
+      nslots, npairs, rot_smem, lut);
 }
 
 void launch_qmax(const qadc_b200_index *idx, const float *lut, const int64_t *cells, int nq,

@@ -381,7 +381,10 @@ def test_ivf_search_vs_oracle_at_scale(gpu, ma):
     assert np.array_equal(got.ids, oi)
     assert np.array_equal(_bits(got.distances), _bits(od))
     assert np.array_equal(got.counts, on)
-    # native: GPU probe equals the oracle probe; results mostly id-exact
+    # native: the GPU rotates, probes and builds the tables itself; the
+    # oracle port uses the same float64 rotation arithmetic, so the whole
+    # native path is bit-exact against it too
     nat = idx.search(qs, R, ma=ma, init=1000)
-    exact = sum(np.array_equal(nat.ids[i], oi[i]) for i in range(qs.shape[0]))
-    assert exact >= qs.shape[0] // 2
+    ni, nd, nn, _ = orc.search_batch(qs, cb, Rm, coarse, ma, flat, R, 1000)
+    assert np.array_equal(nat.ids, ni)
+    assert np.array_equal(_bits(nat.distances), _bits(nd))
