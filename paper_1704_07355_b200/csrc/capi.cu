@@ -174,6 +174,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
     } else {
       if ((rc = cells_b.alloc(npairs, st))) return cuda_fail(cudaGetLastError(), "alloc cells");
       launch_probe(idx->coarseT, idx->K, idx->d, queries, nq, ma, cells_b.p, st);
+      QADC_CUDA(cudaGetLastError());
       ss.launches++;
       cells = cells_b.p;
     }
@@ -182,6 +183,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   if (!lut) {
     if (lut_b.alloc(npairs * m * 16, st)) return cuda_fail(cudaGetLastError(), "alloc lut");
     launch_residual_lut(idx, queries, cells, nq, nslots, lut_b.p, st);
+    QADC_CUDA(cudaGetLastError());
     ss.launches++;
     lut = lut_b.p;
   }
@@ -201,6 +203,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   launch_prefix(idx, qt_b.p, qmin_f.p, delta_f.p, cells, nq, nslots, R, init, M_bits.p, fsat_n.p,
                 fsat_mid.p, fsat_id.p, st);
   k_init_bounds<<<gridn(nq), 256, 0, st>>>(M_bits.p, M_override, hist_w.p, nq);
+  QADC_CUDA(cudaGetLastError());
   ss.launches += 4;
   if (no_fsat) cudaMemsetAsync(fsat_n.p, 0, sizeof(int) * nq, st);
 
@@ -260,6 +263,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   cudaEventCreate(&e1);
   cudaEventRecord(e0, st);
   launch_scan(a, nsm, st);
+  QADC_CUDA(cudaGetLastError());
   cudaEventRecord(e1, st);
   ss.scan_launches++;
   ss.launches++;

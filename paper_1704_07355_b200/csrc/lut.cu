@@ -268,44 +268,68 @@ __global__ void __launch_bounds__(512) k_probe(const float *__restrict__ coarseT
 // configs are "native OPQ" parity with counted bucket flips).
 constexpr int kLutPairs = 16;  // (query, slot) pairs per CTA
 
-// kLutPairs (query, slot) pairs per CTA so the rotation matrix is staged
-// in shared memory once (transposed: conflict-free column reads) and
-// reused by every pair of the CTA.
+// kLutPairs (query, slot) pairs per CTA. The rotation is staged in shared
+// memory once per CTA as float64 R^T (products of two floats are exact in
+// float64, so y = R r accumulated in float64 and rounded once does not depend
+// on FMA contraction), and each thread produces 4 consecutive outputs of one
+// pair so one broadcast r[k] feeds 4 DFMAs.
 __global__ void __launch_bounds__(256) k_residual_lut(
     const float *__restrict__ queries, const float *__restrict__ coarse,
     const float *__restrict__ rotation, const float *__restrict__ codebooks,
     const int64_t *__restrict__ cells, int d, int m, int nslots, int npairs, int rot_in_smem,
     float *__restrict__ lut) {
-  extern __shared__ float sm[];
-  float *sr = sm;                            // [kLutPairs][d] residuals
-  float *sy = sm + kLutPairs * d;            // [kLutPairs][d] rotated
-  float *rt = sm + 2 * kLutPairs * d;        // [d][d] R^T (if staged)
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double *rtd = (double *)smraw;                                      // [d][d] R^T (if staged)
+  double *srd = rtd + (rot_in_smem ? (size_t)d * d : 0);              // [kLutPairs][d] if rotating
+  float *sr = (float *)(srd + (rotation ? (size_t)kLutPairs * d : 0));  // [kLutPairs][d]
+  float *sy = sr + (size_t)kLutPairs * d;                             // [kLutPairs][d]
   const int p0 = blockIdx.x * kLutPairs;
   const int np = min(kLutPairs, npairs - p0);
   for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
     const int p = e / d, t = e - p * d;
     const int pair = p0 + p;
     const float qv = queries[(size_t)(pair / nslots) * d + t];
-    sr[e] = coarse ? __fsub_rn(qv, coarse[(size_t)cells[pair] * d + t]) : qv;
+    const float r = coarse ? __fsub_rn(qv, coarse[(size_t)cells[pair] * d + t]) : qv;
+    sr[e] = r;
+    if (rotation) srd[e] = (double)r;
   }
   if (rotation && rot_in_smem)
     for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
       const int i = e / d, k = e - i * d;
-      rt[k * d + i] = rotation[e];
+      rtd[(size_t)k * d + i] = (double)rotation[e];
     }
   __syncthreads();
   const float *y = sr;
   if (rotation) {
-    for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
-      const int p = e / d, i = e - p * d;
-      const float *r = sr + p * d;
-      double acc = 0.0;
-      if (rot_in_smem) {
-        for (int k = 0; k < d; k++) acc += (double)rt[k * d + i] * (double)r[k];
-      } else {
-        for (int k = 0; k < d; k++) acc += (double)rotation[(size_t)i * d + k] * (double)r[k];
+    if (rot_in_smem && (d & 3) == 0) {
+      const int quads = d >> 2;
+      for (int task = threadIdx.x; task < np * quads; task += blockDim.x) {
+        const int p = task / quads, i0 = (task - p * quads) * 4;
+        const double *r = srd + (size_t)p * d;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (int k = 0; k < d; k++) {
+          const double rv = r[k];
+          const double2 c01 = *(const double2 *)(rtd + (size_t)k * d + i0);
+          const double2 c23 = *(const double2 *)(rtd + (size_t)k * d + i0 + 2);
+          a0 += c01.x * rv;
+          a1 += c01.y * rv;
+          a2 += c23.x * rv;
+          a3 += c23.y * rv;
+        }
+        float *o = sy + (size_t)p * d + i0;
+        o[0] = (float)a0;
+        o[1] = (float)a1;
+        o[2] = (float)a2;
+        o[3] = (float)a3;
       }
-      sy[e] = (float)acc;
+    } else {
+      for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
+        const int p = e / d, i = e - p * d;
+        const double *r = srd + (size_t)p * d;
+        double acc = 0.0;
+        for (int k = 0; k < d; k++) acc += (double)rotation[(size_t)i * d + k] * r[k];
+        sy[e] = (float)acc;
+      }
     }
     __syncthreads();
     y = sy;
@@ -576,8 +600,12 @@ void launch_residual_lut(const qadc_b200_index *idx, const float *queries, const
                          int nq, int nslots, float *lut, cudaStream_t st) {
   if (nq <= 0) return;
   const int npairs = nq * nslots, d = idx->d;
-  const int rot_smem = idx->rotation && (size_t)d * d * 4 <= 64 * 1024;
-  const size_t smem = (size_t)2 * kLutPairs * d * 4 + (rot_smem ? (size_t)d * d * 4 : 0);
+  const bool rot = idx->rotation != nullptr;
+  const int rot_smem = rot && (size_t)d * d * 8 <= 128 * 1024;
+  // per pair: float residual, and with a rotation a float64 copy + output
+  const size_t per_pair = (size_t)d * (rot ? 8 + 4 + 4 : 4 + 4);
+  const size_t fixed = rot_smem ? (size_t)d * d * 8 : 0;
+  const size_t smem = fixed + kLutPairs * per_pair;
   cudaFuncSetAttribute(k_residual_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_residual_lut<<<(npairs + kLutPairs - 1) / kLutPairs, 256, smem, st>>>(
       queries, idx->K ? idx->coarse : nullptr, idx->rotation, idx->codebooks, cells, d, idx->m,

@@ -513,27 +513,40 @@ k_scan(const __grid_constant__ ScanArgs a) {
     const int nq_tile = s.pair_count;
     const int depth = s.depth;
     // ---- warp loop over chunks (one specialization per byte-sum depth) ----
-    switch (depth) {
-      case 16: chunk_loop<16, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
-      case 8: chunk_loop<8, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
-      case 4: chunk_loop<4, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
-      default: chunk_loop<2, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+    // tiles with at most half the query slots in use (the last tile of an
+    // inverted list) run the QT/2 loop instead of computing empty slots
+    constexpr int QH = QT / 2 > 0 ? QT / 2 : 1;
+    if (QH < QT && nq_tile <= QH) {
+      switch (depth) {
+        case 16: chunk_loop<16, MC, QH>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        case 8: chunk_loop<8, MC, QH>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        case 4: chunk_loop<4, MC, QH>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        default: chunk_loop<2, MC, QH>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+      }
+    } else {
+      switch (depth) {
+        case 16: chunk_loop<16, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        case 8: chunk_loop<8, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        case 4: chunk_loop<4, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        default: chunk_loop<2, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+      }
     }
     // ---- end of item: CTA-level bound per query (the R-th smallest value
     // over all four warps' buffers lowers the global M), then publish ----
     __syncthreads();
     for (int q = 0; q < nq_tile; q++) {
+      int tot = 0;
+      for (int ww = 0; ww < kWarps; ww++) tot += s.bn[ww][q];
+      if (tot < a.R) continue;  // uniform: s.bn is stable after the barrier
       for (int i = threadIdx.x; i < 256; i += blockDim.x) s.hist[i] = 0;
       __syncthreads();
-      int tot = 0;
       for (int ww = 0; ww < kWarps; ww++) {
         const int n = s.bn[ww][q];
-        tot += n;
         const uint32_t *b = s_buf + ((size_t)ww * QT + q) * a.cap_l;
         for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&s.hist[b[i] >> 24], 1u);
       }
       __syncthreads();
-      if (w == 0 && tot >= a.R) {
+      if (w == 0) {
         unsigned c = 0;
 #pragma unroll
         for (int i = 0; i < 8; i++) c += s.hist[lane * 8 + i];

@@ -114,3 +114,69 @@ def test_two_shards_with_global_prefix_equal_unsharded(gpu):
     assert np.array_equal(gi.numpy(), want.ids)
     assert np.array_equal(gd.numpy().view(np.uint32), want.distances.view(np.uint32))
     assert np.array_equal(gc.numpy(), want.counts)
+
+
+@pytest.mark.gpu
+def test_ivf_list_shards_with_global_prefix_equal_unsharded(gpu):
+    """IVF list sharding (BASELINE config 2 "lists sharded across GPUs"),
+    emulated on one GPU: shard k keeps the lists L with L % 2 == k, installs
+    the global prefix of EVERY list (qmax and the saturation rule read the
+    first probed cell's global prefix, whichever shard owns it), only shard
+    0 keeps F_sat; the merged shard results equal the unsharded search."""
+    from paper_1704_07355_b200 import datagen
+    from paper_1704_07355_b200.device import DeviceIndex
+    from paper_1704_07355_b200.ivf import assign_device, encode_device
+    from paper_1704_07355_b200.workload import _PQ
+    rng = np.random.default_rng(8)
+    K, n, m, d, R, ma, init = 64, 60_000, 16, 64, 50, 6, 300
+    mix = datagen.Mixture(d=d, components=40, centre_high=100.0, sigma=10.0)
+    X = datagen.mixture_numpy(mix, n, seed=2, stream=2)
+    coarse = X[rng.choice(n, K, replace=False)].copy()
+    Rm = np.linalg.qr(rng.standard_normal((d, d)))[0].astype(np.float32)
+    cb = (rng.standard_normal((m, 16, d // m)) * 6).astype(np.float32)
+    pq = _PQ(cb, Rm)
+    Xd, C = torch.from_numpy(X).cuda(), torch.from_numpy(coarse).cuda()
+    lab = assign_device(coarse, Xd)
+    codes = encode_device(pq, Xd - C[lab])
+    order = torch.argsort(lab, stable=True)
+    sizes = torch.bincount(lab, minlength=K)
+    off = torch.zeros(K + 1, dtype=torch.int64, device="cuda")
+    off[1:] = torch.cumsum(sizes, 0)
+    sc = codes[order].contiguous()
+    cbt, Rt = torch.from_numpy(cb).cuda(), torch.from_numpy(Rm).cuda()
+    full = DeviceIndex.from_device_rows(d, m, sc, off, cbt, rotation=Rt, coarse=C, ids=order)
+    qs = datagen.mixture_numpy(mix, 32, seed=2, stream=3)
+    want = full.search(qs, R, ma=ma, init=init)
+    # global prefixes of every list
+    p = max(init, R)
+    offn, szn = off.cpu().numpy(), sizes.cpu().numpy()
+    pre_rows, pre_ids, pre_off = [], [], [0]
+    for L in range(K):
+        k = min(p, int(szn[L]))
+        pre_rows.append(sc[offn[L]:offn[L] + k])
+        pre_ids.append(order[offn[L]:offn[L] + k])
+        pre_off.append(pre_off[-1] + k)
+    pre_rows = torch.cat(pre_rows).contiguous()
+    pre_ids = torch.cat(pre_ids).contiguous()
+    pre_off = torch.tensor(pre_off, dtype=torch.int64, device="cuda")
+    parts = []
+    for shard in range(2):
+        rows, ids, soff = [], [], [0]
+        for L in range(K):
+            a, b = int(offn[L]), int(offn[L + 1])
+            if L % 2 != shard:
+                b = a  # list owned by the other shard: empty here
+            rows.append(sc[a:b])
+            ids.append(order[a:b])
+            soff.append(soff[-1] + (b - a))
+        sh = DeviceIndex.from_device_rows(
+            d, m, torch.cat(rows).contiguous(), torch.tensor(soff, device="cuda"), cbt,
+            rotation=Rt, coarse=C, ids=torch.cat(ids).contiguous())
+        sh.set_prefix(pre_rows, pre_off, szn, ids=pre_ids)
+        parts.append(sh.search(qs, R, ma=ma, init=init, with_fsat=(shard == 0)))
+    gi, gd, gc = merge_sorted_lists(torch.from_numpy(np.concatenate([x.ids for x in parts], 1)),
+                                    torch.from_numpy(np.concatenate([x.distances for x in parts],
+                                                                    1)), R)
+    assert np.array_equal(gi.numpy(), want.ids)
+    assert np.array_equal(gd.numpy().view(np.uint32), want.distances.view(np.uint32))
+    assert np.array_equal(gc.numpy(), want.counts)
