@@ -121,18 +121,18 @@ void orc_probe(const float *cent, int K, int d, const float *q, int ma,
 }
 
 /* adc.py:108-111 (v @ R^T). OpenBLAS sgemv's summation order is not
- * reproducible, so the restatement accumulates in float64 and
- * rounds once — the same arithmetic as the GPU kernel (k_residual_lut), so
- * native-OPQ GPU results can be checked bit-exactly against this port while
- * both differ from OpenBLAS by rare low-bit flips. */
+ * reproducible, so the restatement fixes one: a sequential
+ * fp32 fused-multiply-add chain over k — the GPU kernel's arithmetic
+ * (k_residual_lut), so native-OPQ GPU results are bit-exact against this
+ * port while both differ from OpenBLAS by rare low-bit flips. */
 void orc_rotate(const float *R, int d, const float *v, float *out)
 {
     int i, k;
     for (i = 0; i < d; i++) {
-        double acc = 0.0;
+        float acc = 0.0f;
         for (k = 0; k < d; k++)
-            acc += (double)R[(size_t)i * d + k] * (double)v[k];
-        out[i] = (float)acc;
+            acc = fmaf(R[(size_t)i * d + k], v[k], acc);
+        out[i] = acc;
     }
 }
 

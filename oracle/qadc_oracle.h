@@ -34,9 +34,9 @@ void orc_compute_tables(const float *codebooks, int m, int dsub,
 void orc_probe(const float *cent, int K, int d, const float *q, int ma,
                int64_t *cells, float *residuals);
 
-/* adc.py:108-111 _rotate with float64 accumulation and one rounding (the
- * GPU's arithmetic). NOT bit-exact vs OpenBLAS sgemv; tests
- * that compare against the reference state "native OPQ" tolerance. */
+/* adc.py:108-111 _rotate as a sequential fp32 FMA chain (the GPU's
+ * arithmetic). NOT bit-exact vs OpenBLAS sgemv; tests that
+ * compare against the reference state "native OPQ" tolerance. */
 void orc_rotate(const float *R, int d, const float *v, float *out);
 
 /* qadc.py:157-194 find_qmax over ONE cell (the search path only ever

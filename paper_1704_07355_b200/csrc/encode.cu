@@ -7,7 +7,7 @@
 //   * pq.encode_batch (pq.py:210-217): optional rotation x @ R^T, then the
 //     per-subspace argmin, packed two sub-codes per byte, low nibble =
 //     even sub-code (pq.py:90-105).
-// The rotation is accumulated in float64 (OpenBLAS's order is unpinned,
+// The rotation is a sequential fp32 FMA chain (OpenBLAS's order is unpinned,
 // SURVEY A.7), and k*d > 2^20 coarse assignment uses the same einsum form
 // instead of the reference's clamped GEMM expansion.
 #include "qadc_b200.h"
@@ -44,7 +44,8 @@ __device__ __forceinline__ float sqdist_einsum(const float *__restrict__ a, cons
   return __fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3]));
 }
 
-// y = R x (float64 accumulation, one rounding), one CTA per 8 vectors.
+// y = R x (sequential fp32 FMA chain, the search path's arithmetic), one CTA
+// per 8 vectors.
 __global__ void k_rotate(const float *__restrict__ X, int64_t n, int d, const float *__restrict__ R,
                          float *__restrict__ Y) {
   extern __shared__ float sx[];  // 8 * d
@@ -54,9 +55,9 @@ __global__ void k_rotate(const float *__restrict__ X, int64_t n, int d, const fl
   __syncthreads();
   for (int t = threadIdx.x; t < nv * d; t += blockDim.x) {
     const int v = t / d, i = t % d;
-    double acc = 0.0;
-    for (int k = 0; k < d; k++) acc += (double)R[(size_t)i * d + k] * (double)sx[v * d + k];
-    Y[(v0 + v) * d + i] = (float)acc;
+    float acc = 0.f;
+    for (int k = 0; k < d; k++) acc = __fmaf_rn(R[(size_t)i * d + k], sx[v * d + k], acc);
+    Y[(v0 + v) * d + i] = acc;
   }
 }
 

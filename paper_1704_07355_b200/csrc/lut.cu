@@ -90,95 +90,72 @@ __global__ void k_tables(const float *__restrict__ codebooks, int m, int dsub,
 // transposed centroid array, reused from registers for all queries of the
 // CTA). Coarse distances follow NumPy's einsum order exactly; keys are
 // (d2 bits << 32 | cell), so lexsort((cell, d2)) order is plain u64 order
-// (d2 >= 0). Per tile of kProbeTile cells each query's ma smallest keys are
-// found by an MSB radix select in shared memory and merged into a running
-// best-ma set; the winners are sorted at the end.
+// (d2 >= 0). Per tile of cells, one warp per query keeps the ma smallest
+// keys: keys below the running ma-th best are buffered and merged by a warp
+// bitonic sort (exact; the running threshold only discards keys that
+// already have ma smaller ones).
 constexpr int kProbeQ = 8;
 constexpr int kProbeTile = 2048;
 constexpr int kBoundPrefix = 16384;
 
-// k-th smallest (1-based) of n keys; the 256-bin digit search runs on warp 0
-// with shuffles instead of a serial scan.
-__device__ uint64_t block_kth_u64(const uint64_t *keys, int n, int k, unsigned *hist,
-                                  uint64_t *s_prefix, int *s_k) {
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) { *s_prefix = 0; *s_k = k; }
-  __syncthreads();
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    const uint64_t prefix = *s_prefix;
-    const uint64_t hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint64_t key = keys[i];
-      if ((key & hmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      unsigned c = 0;
-#pragma unroll
-      for (int i = 0; i < 8; i++) c += hist[lane * 8 + i];
-      unsigned incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const unsigned kk = (unsigned)*s_k;
-      const unsigned hit = __ballot_sync(0xffffffffu, incl >= kk);
-      const int src = __ffs(hit) - 1;
-      if (lane == src) {
-        unsigned cum = incl - c;
-        int dgt = lane * 8;
-        for (int i = 0; i < 8; i++, dgt++) {
-          if (cum + hist[dgt] >= kk) break;
-          cum += hist[dgt];
-        }
-        *s_k = (int)(kk - cum);
-        *s_prefix = prefix | ((uint64_t)dgt << shift);
-      }
-    }
-    __syncthreads();
-  }
-  return *s_prefix;
-}
+// Warp-level exact selection of the ma smallest unique u64 keys: a running
+// set `best` (sorted, nb <= ma) plus a candidate buffer; keys below the
+// current ma-th best are appended; a full buffer is merged by a warp
+// bitonic sort of (best U buffer) in shared memory.
+constexpr int kSelBuf = 192;  // candidate slots per query (ma <= 64)
 
-__device__ void block_sort_u64(uint64_t *keys, int n_pow2) {
+__device__ __forceinline__ void warp_sort_u64(uint64_t *v, int n_pow2) {
+  const int lane = threadIdx.x & 31;
   for (int k = 2; k <= n_pow2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+      for (int i = lane; i < n_pow2; i += 32) {
         const int ixj = i ^ j;
         if (ixj > i) {
-          const uint64_t a = keys[i], b = keys[ixj];
+          const uint64_t a = v[i], b = v[ixj];
           const bool up = (i & k) == 0;
-          if ((a > b) == up) { keys[i] = b; keys[ixj] = a; }
+          if ((a > b) == up) { v[i] = b; v[ixj] = a; }
         }
       }
-      __syncthreads();
+      __syncwarp();
     }
   }
 }
 
-__global__ void __launch_bounds__(512) k_probe(const float *__restrict__ coarseT, int K, int d,
+// Merge buffer entries into best (kept in v[0 .. nb)); v has room for
+// ma + kSelBuf entries rounded up to a power of two.
+__device__ __forceinline__ void warp_merge(uint64_t *v, int &nb, int &bn, int ma, uint64_t &T) {
+  const int lane = threadIdx.x & 31;
+  const int n = nb + bn;
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  for (int i = n + lane; i < p2; i += 32) v[i] = ~0ull;
+  __syncwarp();
+  warp_sort_u64(v, p2);
+  nb = n < ma ? n : ma;
+  bn = 0;
+  T = nb == ma ? v[ma - 1] : ~0ull;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_probe(const float *__restrict__ coarseT, int K, int d,
                                                const float *__restrict__ queries, int nq, int ma,
-                                               int64_t *__restrict__ cells) {
+                                               int tile, int vcap, int64_t *__restrict__ cells) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t *keys = (uint64_t *)smem;                         // [kProbeQ][kProbeTile]
-  uint64_t *best = keys + (size_t)kProbeQ * kProbeTile;      // [kProbeQ][2 * ma]
-  float *sq = (float *)(best + (size_t)kProbeQ * 2 * ma);    // [kProbeQ][d]
-  __shared__ unsigned hist[256];
-  __shared__ uint64_t s_prefix;
-  __shared__ int s_k, s_nb[kProbeQ];
+  uint64_t *keys = (uint64_t *)smem;                        // [kProbeQ][tile]
+  uint64_t *sel = keys + (size_t)kProbeQ * tile;            // [kProbeQ][vcap]: best | buffer
+  float *sq = (float *)(sel + (size_t)kProbeQ * vcap);      // [kProbeQ][d]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int q0 = blockIdx.x * kProbeQ;
   const int nqb = min(kProbeQ, nq - q0);
   for (int e = threadIdx.x; e < kProbeQ * d; e += blockDim.x) {
     const int q = e / d;
     sq[e] = q < nqb ? queries[(size_t)(q0 + q) * d + (e - q * d)] : 0.f;
   }
-  if (threadIdx.x < kProbeQ) s_nb[threadIdx.x] = 0;
+  int nb = 0, bn = 0;  // warp w's selection state (query w)
+  uint64_t T = ~0ull;
   __syncthreads();
-  for (int base = 0; base < K; base += kProbeTile) {
-    const int n = min(kProbeTile, K - base);
+  for (int base = 0; base < K; base += tile) {
+    const int n = min(tile, K - base);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int k = base + i;
       float acc[kProbeQ][4];
@@ -220,43 +197,34 @@ __global__ void __launch_bounds__(512) k_probe(const float *__restrict__ coarseT
 #pragma unroll
       for (int q = 0; q < kProbeQ; q++) {
         const float d2 = __fadd_rn(__fadd_rn(acc[q][0], acc[q][1]), __fadd_rn(acc[q][2], acc[q][3]));
-        keys[(size_t)q * kProbeTile + i] = ((uint64_t)__float_as_uint(d2) << 32) | (uint32_t)k;
+        keys[(size_t)q * tile + i] = ((uint64_t)__float_as_uint(d2) << 32) | (uint32_t)k;
       }
     }
     __syncthreads();
-    for (int q = 0; q < nqb; q++) {
-      uint64_t *kq = keys + (size_t)q * kProbeTile;
-      uint64_t *bq = best + (size_t)q * 2 * ma;
-      const int take = min(ma, n);
-      const uint64_t kth = block_kth_u64(kq, n, take, hist, &s_prefix, &s_k);
-      for (int i = threadIdx.x; i < n; i += blockDim.x)
-        if (kq[i] <= kth) bq[atomicAdd(&s_nb[q], 1)] = kq[i];
-      __syncthreads();
-      const int nb = s_nb[q];
-      if (nb > ma) {  // keep the ma smallest of the running set (keys unique)
-        const uint64_t k2 = block_kth_u64(bq, nb, ma, hist, &s_prefix, &s_k);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          int w = 0;
-          for (int i = 0; i < nb; i++)
-            if (bq[i] <= k2) bq[w++] = bq[i];
-          s_nb[q] = w;
+    if (w < nqb) {  // warp w selects for query w
+      const uint64_t *kq = keys + (size_t)w * tile;
+      uint64_t *v = sel + (size_t)w * vcap;
+      for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        const uint64_t key = i < n ? kq[i] : ~0ull;
+        const bool take = key < T;
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        if (bal) {
+          if (bn + __popc(bal) > kSelBuf) warp_merge(v, nb, bn, ma, T);
+          const bool take2 = key < T;
+          const unsigned bal2 = __ballot_sync(0xffffffffu, take2);
+          if (take2) v[nb + bn + __popc(bal2 & ((1u << lane) - 1))] = key;
+          bn += __popc(bal2);
+          __syncwarp();
         }
-        __syncthreads();
       }
     }
     __syncthreads();
   }
-  int p2 = 1;
-  while (p2 < ma) p2 <<= 1;
-  for (int q = 0; q < nqb; q++) {
-    uint64_t *bq = best + (size_t)q * 2 * ma;
-    for (int i = ma + threadIdx.x; i < p2; i += blockDim.x) bq[i] = ~0ull;
-    __syncthreads();
-    block_sort_u64(bq, p2);
-    for (int i = threadIdx.x; i < ma; i += blockDim.x)
-      cells[(size_t)(q0 + q) * ma + i] = (int64_t)(bq[i] & 0xffffffffu);
-    __syncthreads();
+  if (w < nqb) {
+    uint64_t *v = sel + (size_t)w * vcap;
+    warp_merge(v, nb, bn, ma, T);
+    for (int i = lane; i < ma; i += 32) cells[(size_t)(q0 + w) * ma + i] = (int64_t)(v[i] & 0xffffffffu);
   }
 }
 
@@ -268,35 +236,33 @@ __global__ void __launch_bounds__(512) k_probe(const float *__restrict__ coarseT
 // configs are "native OPQ" parity with counted bucket flips).
 constexpr int kLutPairs = 16;  // (query, slot) pairs per CTA
 
-// kLutPairs (query, slot) pairs per CTA. The rotation is staged in shared
-// memory once per CTA as float64 R^T (products of two floats are exact in
-// float64, so y = R r accumulated in float64 and rounded once does not depend
-// on FMA contraction), and each thread produces 4 consecutive outputs of one
-// pair so one broadcast r[k] feeds 4 DFMAs.
+// kLutPairs (query, slot) pairs per CTA. OPQ rotation y = R r: the
+// reference calls OpenBLAS sgemv, whose summation order is not reproducible
+// (SURVEY A.7); here y_i = fma-chain over k = 0..d-1 in fp32 (the oracle
+// port restates exactly this order), R staged once per CTA in shared memory
+// as R^T (conflict-free), each thread producing 4 consecutive outputs of
+// one pair from one broadcast r[k].
 __global__ void __launch_bounds__(256) k_residual_lut(
     const float *__restrict__ queries, const float *__restrict__ coarse,
     const float *__restrict__ rotation, const float *__restrict__ codebooks,
     const int64_t *__restrict__ cells, int d, int m, int nslots, int npairs, int rot_in_smem,
     float *__restrict__ lut) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  double *rtd = (double *)smraw;                                      // [d][d] R^T (if staged)
-  double *srd = rtd + (rot_in_smem ? (size_t)d * d : 0);              // [kLutPairs][d] if rotating
-  float *sr = (float *)(srd + (rotation ? (size_t)kLutPairs * d : 0));  // [kLutPairs][d]
-  float *sy = sr + (size_t)kLutPairs * d;                             // [kLutPairs][d]
+  extern __shared__ __align__(16) float smf[];
+  float *rt = smf;                                              // [d][d] R^T (if staged)
+  float *sr = smf + (rot_in_smem ? (size_t)d * d : 0);          // [kLutPairs][d]
+  float *sy = sr + (size_t)kLutPairs * d;                       // [kLutPairs][d]
   const int p0 = blockIdx.x * kLutPairs;
   const int np = min(kLutPairs, npairs - p0);
   for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
     const int p = e / d, t = e - p * d;
     const int pair = p0 + p;
     const float qv = queries[(size_t)(pair / nslots) * d + t];
-    const float r = coarse ? __fsub_rn(qv, coarse[(size_t)cells[pair] * d + t]) : qv;
-    sr[e] = r;
-    if (rotation) srd[e] = (double)r;
+    sr[e] = coarse ? __fsub_rn(qv, coarse[(size_t)cells[pair] * d + t]) : qv;
   }
   if (rotation && rot_in_smem)
     for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
       const int i = e / d, k = e - i * d;
-      rtd[(size_t)k * d + i] = (double)rotation[e];
+      rt[(size_t)k * d + i] = rotation[e];
     }
   __syncthreads();
   const float *y = sr;
@@ -305,30 +271,25 @@ __global__ void __launch_bounds__(256) k_residual_lut(
       const int quads = d >> 2;
       for (int task = threadIdx.x; task < np * quads; task += blockDim.x) {
         const int p = task / quads, i0 = (task - p * quads) * 4;
-        const double *r = srd + (size_t)p * d;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const float *r = sr + (size_t)p * d;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
         for (int k = 0; k < d; k++) {
-          const double rv = r[k];
-          const double2 c01 = *(const double2 *)(rtd + (size_t)k * d + i0);
-          const double2 c23 = *(const double2 *)(rtd + (size_t)k * d + i0 + 2);
-          a0 += c01.x * rv;
-          a1 += c01.y * rv;
-          a2 += c23.x * rv;
-          a3 += c23.y * rv;
+          const float rv = r[k];
+          const float4 c = *(const float4 *)(rt + (size_t)k * d + i0);
+          a0 = __fmaf_rn(c.x, rv, a0);
+          a1 = __fmaf_rn(c.y, rv, a1);
+          a2 = __fmaf_rn(c.z, rv, a2);
+          a3 = __fmaf_rn(c.w, rv, a3);
         }
-        float *o = sy + (size_t)p * d + i0;
-        o[0] = (float)a0;
-        o[1] = (float)a1;
-        o[2] = (float)a2;
-        o[3] = (float)a3;
+        *(float4 *)(sy + (size_t)p * d + i0) = make_float4(a0, a1, a2, a3);
       }
     } else {
       for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
         const int p = e / d, i = e - p * d;
-        const double *r = srd + (size_t)p * d;
-        double acc = 0.0;
-        for (int k = 0; k < d; k++) acc += (double)rotation[(size_t)i * d + k] * r[k];
-        sy[e] = (float)acc;
+        const float *r = sr + (size_t)p * d;
+        float acc = 0.f;
+        for (int k = 0; k < d; k++) acc = __fmaf_rn(rotation[(size_t)i * d + k], r[k], acc);
+        sy[e] = acc;
       }
     }
     __syncthreads();
@@ -588,12 +549,17 @@ void launch_compute_tables(const float *codebooks, int m, int dsub, const float 
 void launch_probe(const float *coarseT, int K, int d, const float *queries, int nq, int ma,
                   int64_t *cells, cudaStream_t st) {
   if (nq <= 0) return;
-  int p2 = 1;
-  while (p2 < ma) p2 <<= 1;
-  const size_t smem = (size_t)kProbeQ * kProbeTile * 8 + (size_t)kProbeQ * 2 * std::max(ma, p2) * 8 +
-                      (size_t)kProbeQ * d * 4;
+  int vcap = 1;
+  while (vcap < ma + kSelBuf) vcap <<= 1;
+  int tile = kProbeTile;
+  size_t smem = 0;
+  for (;; tile >>= 1) {
+    smem = (size_t)kProbeQ * tile * 8 + (size_t)kProbeQ * vcap * 8 + (size_t)kProbeQ * d * 4;
+    if (smem <= 220 * 1024 || tile <= 256) break;
+  }
   cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_probe<<<(nq + kProbeQ - 1) / kProbeQ, 512, smem, st>>>(coarseT, K, d, queries, nq, ma, cells);
+  k_probe<<<(nq + kProbeQ - 1) / kProbeQ, 256, smem, st>>>(coarseT, K, d, queries, nq, ma, tile,
+                                                          vcap, cells);
 }
 
 void launch_residual_lut(const qadc_b200_index *idx, const float *queries, const int64_t *cells,
@@ -601,10 +567,9 @@ void launch_residual_lut(const qadc_b200_index *idx, const float *queries, const
   if (nq <= 0) return;
   const int npairs = nq * nslots, d = idx->d;
   const bool rot = idx->rotation != nullptr;
-  const int rot_smem = rot && (size_t)d * d * 8 <= 128 * 1024;
-  // per pair: float residual, and with a rotation a float64 copy + output
-  const size_t per_pair = (size_t)d * (rot ? 8 + 4 + 4 : 4 + 4);
-  const size_t fixed = rot_smem ? (size_t)d * d * 8 : 0;
+  const int rot_smem = rot && (size_t)d * d * 4 <= 64 * 1024;
+  const size_t per_pair = (size_t)d * 8;  // residual + rotated, fp32
+  const size_t fixed = rot_smem ? (size_t)d * d * 4 : 0;
   const size_t smem = fixed + kLutPairs * per_pair;
   cudaFuncSetAttribute(k_residual_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_residual_lut<<<(npairs + kLutPairs - 1) / kLutPairs, 256, smem, st>>>(

@@ -388,3 +388,20 @@ def test_ivf_search_vs_oracle_at_scale(gpu, ma):
     ni, nd, nn, _ = orc.search_batch(qs, cb, Rm, coarse, ma, flat, R, 1000)
     assert np.array_equal(nat.ids, ni)
     assert np.array_equal(_bits(nat.distances), _bits(nd))
+
+
+@pytest.mark.parametrize("K,ma", [(300, 1), (300, 64), (300, 300), (5000, 16), (5000, 130),
+                                  (9000, 64)])
+def test_probe_vs_oracle_many_sizes(gpu, K, ma):
+    """Probe order (einsum d2, ties -> lower cell) for multi-tile K and
+    ma beyond one selection buffer, including forced distance ties."""
+    from paper_1704_07355_b200 import datagen, ivf
+    cen = datagen.mixture_numpy(datagen.SIFT_LIKE, K, seed=K, stream=1)
+    cen[K // 3] = cen[K // 2]  # duplicate centroid -> exact d2 tie
+    index = ivf.IvfIndex(d=128, m=16, b=4, coarse=ivf.Codebook(cen), lists=[None] * K,
+                         layout=ivf.LAYOUT_STANDARD)
+    qs = datagen.mixture_numpy(datagen.SIFT_LIKE, 6, seed=K, stream=3)
+    qs[0] = cen[K // 2]
+    for q in qs:
+        want, _ = orc.probe(cen, q, ma)
+        assert np.array_equal(ivf.probe(index, q, ma).cells, want)
