@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU work of the bounded reference sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--recall", type=int, default=0,
+                   help="report R@1/10/100 on this many queries (exact GPU ground truth)")
     return p.parse_args()
 
 
@@ -216,6 +218,50 @@ def cpu_reference_run_ivf(cfg, pq, coarse, codes_np, ids_np, row_off, qs, R, ini
     codes_scanned = int(np.asarray(flat[3])[cells].sum())
     return (codes_scanned / wall, f"{nq} of {qs.shape[0]} queries, nprobe={ma}",
             "reference" if use_ref else "port", nthreads, (oi, od, on), wall)
+
+
+def measure_recall(cfg, pq, n, qs, ids, codes=None):
+    """R@{1,10,100} (reference bench.py:110-122) against exact float64
+    nearest neighbours of the same GPU-drawn base (regenerated chunk by
+    chunk with the shard generator's seeds). For a flat index (`codes`
+    given) the float-table ADC top-100 of the same codes is measured too,
+    so the quantized-table recall loss (the paper's QADC vs ADC figure)
+    sits beside it."""
+    import torch
+
+    from paper_1704_07355_b200 import datagen
+    from paper_1704_07355_b200.adc import compute_tables
+    from paper_1704_07355_b200.recall import ground_truth, recall_at
+    from paper_1704_07355_b200.workload import CORPUS, SEED
+
+    def chunks():
+        step = 4 * datagen.CHUNK
+        for c0 in range(0, n, step):
+            k = min(step, n - c0)
+            yield c0, datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000, centre_seed=CORPUS,
+                                            stream=datagen.STREAM_BASE * 100 + c0 // step)
+    gt = ground_truth(chunks(), qs, depth=1)[:, 0]
+    out = {f"R@{r}": recall_at(ids, gt, r) for r in (1, 10, 100)}
+    if codes is not None:
+        T = torch.from_numpy(np.stack([compute_tables(pq, q).tables for q in qs])).cuda()
+        best_d, best_i = None, None
+        for c0 in range(0, n, 1 << 21):
+            c = codes[c0:c0 + (1 << 21)]
+            sub = torch.stack([c & 15, c >> 4], 2).reshape(c.shape[0], -1).long()
+            acc = torch.zeros((T.shape[0], c.shape[0]), device="cuda")
+            for j in range(pq.m):
+                acc += T[:, j, :][:, sub[:, j]]
+            dd, ii = torch.topk(acc, min(100, c.shape[0]), dim=1, largest=False)
+            ii = ii + c0
+            if best_d is not None:
+                dd, ii = torch.cat([best_d, dd], 1), torch.cat([best_i, ii], 1)
+                o = torch.topk(dd, 100, dim=1, largest=False).indices
+                dd, ii = torch.gather(dd, 1, o), torch.gather(ii, 1, o)
+            best_d, best_i = dd, ii
+        o = torch.argsort(best_d, dim=1, stable=True)
+        fi = torch.gather(best_i, 1, o).cpu().numpy()
+        out["adc_float"] = {f"R@{r}": recall_at(fi, gt, r) for r in (1, 10, 100)}
+    return out | {"queries": int(qs.shape[0])}
 
 
 # ---------------------------------------------------------------- arms
@@ -395,6 +441,9 @@ def run_b200(args):
             out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                                    "sample": sample, "seconds": round(wall, 2)}
             out["parity_vs_cpu_reference"] = {"queries": k, "bit_exact": exact}
+    if out is not None and args.recall and world == 1:
+        out["recall"] = measure_recall(cfg, pq, n, qs[: args.recall], out_i.numpy()[: args.recall],
+                                       codes=None if ivf_cfg is not None else codes)
     if world > 1:
         dist.destroy_process_group()
     return out

@@ -173,7 +173,9 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
       cells = cells_in;
     } else {
       if ((rc = cells_b.alloc(npairs, st))) return cuda_fail(cudaGetLastError(), "alloc cells");
-      launch_probe(idx->coarseT, idx->K, idx->d, queries, nq, ma, cells_b.p, st);
+      if (!(idx->cnorm && launch_probe_fast(idx->coarseT, idx->coarse, idx->cnorm, idx->K,
+                                            idx->d, queries, nq, ma, cells_b.p, st)))
+        launch_probe(idx->coarseT, idx->K, idx->d, queries, nq, ma, cells_b.p, st);
       QADC_CUDA(cudaGetLastError());
       ss.launches++;
       cells = cells_b.p;
@@ -520,7 +522,9 @@ int index_common(int d, int m, int nlists, const float *coarse, bool coarse_dev,
     QADC_CUDA(cudaMalloc(&idx->coarseT, cb));
     QADC_CUDA(cudaMemcpy(idx->coarse, coarse, cb, ck));
     k_transpose<<<gridn((int64_t)nlists * d), 256>>>(idx->coarse, nlists, d, idx->coarseT);
-    idx->bytes += 2 * (int64_t)cb;
+    QADC_CUDA(cudaMalloc(&idx->cnorm, (size_t)nlists * 4));
+    launch_cnorm(idx->coarse, nlists, d, idx->cnorm, 0);
+    idx->bytes += 2 * (int64_t)cb + (int64_t)nlists * 4;
   }
   const size_t bb = (size_t)m * 16 * (d / m) * 4;
   QADC_CUDA(cudaMalloc(&idx->codebooks, bb));
@@ -546,7 +550,7 @@ extern "C" void qadc_b200_index_destroy(qadc_b200_index *idx) {
   if (idx->own_prefix) {
     cudaFree(idx->pcodes); cudaFree(idx->pids); cudaFree(idx->pchunk_off); cudaFree(idx->planes);
   }
-  cudaFree(idx->coarse); cudaFree(idx->coarseT); cudaFree(idx->codebooks); cudaFree(idx->rotation);
+  cudaFree(idx->coarse); cudaFree(idx->coarseT); cudaFree(idx->cnorm); cudaFree(idx->codebooks); cudaFree(idx->rotation);
   cudaFree(idx->codes); cudaFree(idx->valid); cudaFree(idx->ids); cudaFree(idx->chunk_list);
   cudaFree(idx->chunk_off); cudaFree(idx->lanes); cudaFree(idx->count); cudaFree(idx->scan_count);
   delete idx;
@@ -753,7 +757,12 @@ extern "C" int qadc_b200_probe(const float *coarse, int K, int d, const float *q
   float *cT = nullptr;
   QADC_CUDA(cudaMallocAsync(&cT, (size_t)K * d * 4, st));
   k_transpose<<<gridn((int64_t)K * d), 256, 0, st>>>(coarse, K, d, cT);
-  launch_probe(cT, K, d, queries, nq, ma, cells, st);
+  float *cn = nullptr;
+  QADC_CUDA(cudaMallocAsync(&cn, (size_t)K * 4, st));
+  launch_cnorm(coarse, K, d, cn, st);
+  if (!launch_probe_fast(cT, coarse, cn, K, d, queries, nq, ma, cells, st))
+    launch_probe(cT, K, d, queries, nq, ma, cells, st);
+  cudaFreeAsync(cn, st);
   cudaFreeAsync(cT, st);
   if (residuals)
     k_residuals<<<gridn((int64_t)nq * ma * d), 256, 0, st>>>(queries, coarse, cells, nq, ma, d,

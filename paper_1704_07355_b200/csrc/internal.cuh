@@ -23,6 +23,7 @@ struct qadc_b200_index {
   int64_t max_list_chunks = 0;
   float *coarse = nullptr;     // [K][d]
   float *coarseT = nullptr;    // [d][K] (coalesced probe reads)
+  float *cnorm = nullptr;      // [K] |c|^2 (probe pre-selection bounds)
   float *codebooks = nullptr;  // [m][16][dsub]
   float *rotation = nullptr;   // [d][d] or null
   uint32_t *codes = nullptr;   // [total_chunks][m][32]
@@ -68,6 +69,11 @@ void launch_compute_tables(const float *codebooks, int m, int dsub,
                            const float *y, int npairs, float *out, cudaStream_t st);
 void launch_probe(const float *coarseT, int K, int d, const float *queries,
                   int nq, int ma, int64_t *cells, cudaStream_t st);
+void launch_cnorm(const float *coarse, int K, int d, float *cn, cudaStream_t st);
+// FFMA pre-selection + exact re-rank probe; false = not applicable (caller
+// uses launch_probe).
+bool launch_probe_fast(const float *coarseT, const float *coarse, const float *cn, int K, int d,
+                       const float *queries, int nq, int ma, int64_t *cells, cudaStream_t st);
 void launch_residual_lut(const qadc_b200_index *idx, const float *queries,
                          const int64_t *cells, int nq, int nslots,
                          float *lut, cudaStream_t st);

@@ -228,6 +228,231 @@ __global__ void __launch_bounds__(256) k_probe(const float *__restrict__ coarseT
   }
 }
 
+// ---------------- fast probe: FFMA pre-selection + exact re-rank ----------------
+// The exact order needs einsum-order d2 only for cells that can reach the
+// top ma. Pass 1 bounds every cell's einsum d2 from an FFMA dot product:
+//   A = fl(|c|^2 - 2 q.c),  |A + |q|^2 - D| <= (d u + 4u)(|q|^2 + |c|^2)
+//   |E - D| <= (d/2 + 12) u (|q|^2 + |c|^2)     (E: einsum fp32, D: exact)
+// with u = 2^-24; the margin (2.5 d + 200) u (|q|^2 + |c|^2) covers both,
+// so E lies in [L, U] = A + |q|^2 -/+ margin for every cell. With U* the
+// ma-th smallest U, every cell of the true top ma has L <= E <= U*, and
+// pass 2 recomputes the exact einsum d2 only for cells with L <= U*, then
+// selects exactly by (d2, cell). A candidate overflow falls back to the
+// exact scan of all cells for that query.
+constexpr int kFastQ = 8;
+constexpr int kFastTile = 1024;  // 256 threads x 4 cells
+constexpr int kCandCap = 512;
+
+__global__ void k_cnorm(const float *__restrict__ coarse, int K, int d, float *__restrict__ cn) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < d; t++) {
+      const double v = coarse[(size_t)k * d + t];
+      acc += v * v;
+    }
+    cn[k] = (float)acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_probe_fast(
+    const float *__restrict__ coarseT, const float *__restrict__ coarse,
+    const float *__restrict__ cn, int K, int d, const float *__restrict__ queries, int nq, int ma,
+    int vcap, float *__restrict__ Lbuf, int64_t *__restrict__ cells) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t *sel = (uint64_t *)smem;                             // [kFastQ][vcap]
+  float *ub = (float *)(sel + (size_t)kFastQ * vcap);           // [kFastQ][kFastTile] U
+  float *sqT = ub + (size_t)kFastQ * kFastTile;                 // [d][kFastQ]
+  __shared__ float s_qn[kFastQ];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q0 = blockIdx.x * kFastQ;
+  const int nqb = min(kFastQ, nq - q0);
+  for (int e = threadIdx.x; e < kFastQ * d; e += blockDim.x) {
+    const int t = e / kFastQ, q = e - t * kFastQ;
+    sqT[e] = q < nqb ? queries[(size_t)(q0 + q) * d + t] : 0.f;
+  }
+  __syncthreads();
+  if (threadIdx.x < kFastQ) {
+    double acc = 0.0;
+    for (int t = 0; t < d; t++) {
+      const double v = sqT[t * kFastQ + threadIdx.x];
+      acc += v * v;
+    }
+    s_qn[threadIdx.x] = (float)acc;
+  }
+  __syncthreads();
+  const double mu = (2.5 * d + 200.0) * 5.9604644775390625e-08;  // margin factor
+  int nb = 0, bn = 0;
+  uint64_t T = ~0ull;
+  for (int base = 0; base < K; base += kFastTile) {
+    const int k0 = base + 4 * threadIdx.x;
+    float acc[4][kFastQ];
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+#pragma unroll
+      for (int q = 0; q < kFastQ; q++) acc[c][q] = 0.f;
+    if (k0 < K) {
+      const bool vec = (k0 + 3 < K) && ((K & 3) == 0);
+#pragma unroll 4
+      for (int t = 0; t < d; t++) {
+        float cv[4];
+        if (vec) {
+          const float4 c4 = *(const float4 *)(coarseT + (size_t)t * K + k0);
+          cv[0] = c4.x; cv[1] = c4.y; cv[2] = c4.z; cv[3] = c4.w;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; c++) cv[c] = k0 + c < K ? coarseT[(size_t)t * K + k0 + c] : 0.f;
+        }
+        const float4 qa = *(const float4 *)(sqT + t * kFastQ);
+        const float4 qb = *(const float4 *)(sqT + t * kFastQ + 4);
+        const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+#pragma unroll
+          for (int q = 0; q < kFastQ; q++) acc[c][q] = __fmaf_rn(cv[c], qv[q], acc[c][q]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      const int k = k0 + c;
+      const int slot = 4 * threadIdx.x + c;
+      const float cnk = k < K ? cn[k] : 0.f;
+#pragma unroll
+      for (int q = 0; q < kFastQ; q++) {
+        float Uk = __int_as_float(0x7f800000);
+        if (k < K && q < nqb) {
+          const float A = __fmaf_rn(-2.f, acc[c][q], cnk);
+          const double base_d = (double)A + (double)s_qn[q];
+          const double mg = mu * ((double)s_qn[q] + (double)cnk);
+          const float U = __double2float_ru(base_d + mg);
+          const float L = fmaxf(__double2float_rd(base_d - mg), 0.f);
+          Uk = fmaxf(U, 0.f);
+          Lbuf[(size_t)(q0 + q) * K + k] = L;
+        }
+        ub[(size_t)q * kFastTile + slot] = Uk;
+      }
+    }
+    __syncthreads();
+    if (w < nqb) {
+      const float *uq = ub + (size_t)w * kFastTile;
+      uint64_t *v = sel + (size_t)w * vcap;
+      for (int i0 = 0; i0 < kFastTile && base + i0 < K; i0 += 32) {
+        const int k = base + i0 + lane;
+        const uint64_t key = k < K ? ((uint64_t)__float_as_uint(uq[i0 + lane]) << 32) | (uint32_t)k
+                                   : ~0ull;
+        const unsigned bal = __ballot_sync(0xffffffffu, key < T);
+        if (bal) {
+          if (bn + __popc(bal) > kSelBuf) warp_merge(v, nb, bn, ma, T);
+          const bool take2 = key < T;
+          const unsigned bal2 = __ballot_sync(0xffffffffu, take2);
+          if (take2) v[nb + bn + __popc(bal2 & ((1u << lane) - 1))] = key;
+          bn += __popc(bal2);
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+  }
+  __threadfence_block();
+  if (w >= nqb) return;
+  uint64_t *v = sel + (size_t)w * vcap;
+  warp_merge(v, nb, bn, ma, T);
+  const float Ustar = __uint_as_float((uint32_t)(v[ma - 1] >> 32));
+  // pass 2: candidates with L <= U* (reads this CTA's own Lbuf writes)
+  uint64_t *cq = (uint64_t *)(ub + (size_t)w * kFastTile);  // own U row, now free
+  const float *Lq = Lbuf + (size_t)(q0 + w) * K;
+  int nc = 0;
+  bool overflow = false;
+  for (int i0 = 0; i0 < K; i0 += 32) {
+    const int k = i0 + lane;
+    const bool take = k < K && Lq[k] <= Ustar;
+    const unsigned bal = __ballot_sync(0xffffffffu, take);
+    if (nc + __popc(bal) > kCandCap) { overflow = true; break; }
+    if (take) cq[nc + __popc(bal & ((1u << lane) - 1))] = (uint64_t)k;
+    nc += __popc(bal);
+  }
+  __syncwarp();
+  const float *qcol = sqT;  // query w at sqT[t * kFastQ + w]
+  if (!overflow) {
+    for (int i = lane; i < nc; i += 32) {
+      const int k = (int)cq[i];
+      const float *crow = coarse + (size_t)k * d;
+      float a4[4] = {0.f, 0.f, 0.f, 0.f};
+      int t0 = 0;
+      for (; d - t0 >= 16; t0 += 16)
+#pragma unroll
+        for (int vv = 3; vv >= 0; vv--)
+#pragma unroll
+          for (int l = 0; l < 4; l++) {
+            const int t = t0 + 4 * vv + l;
+            const float df = __fsub_rn(crow[t], qcol[t * kFastQ + w]);
+            a4[l] = __fadd_rn(a4[l], __fmul_rn(df, df));
+          }
+      for (; t0 < d; t0 += 4)
+#pragma unroll
+        for (int l = 0; l < 4; l++) {
+          float pr = 0.f;
+          if (t0 + l < d) {
+            const float df = __fsub_rn(crow[t0 + l], qcol[(t0 + l) * kFastQ + w]);
+            pr = __fmul_rn(df, df);
+          }
+          a4[l] = __fadd_rn(a4[l], pr);
+        }
+      const float E = __fadd_rn(__fadd_rn(a4[0], a4[1]), __fadd_rn(a4[2], a4[3]));
+      cq[i] = ((uint64_t)__float_as_uint(E) << 32) | (uint32_t)k;
+    }
+    __syncwarp();
+    int p2 = 1;
+    while (p2 < nc) p2 <<= 1;
+    for (int i = nc + lane; i < p2; i += 32) cq[i] = ~0ull;
+    __syncwarp();
+    warp_sort_u64(cq, p2);
+    for (int i = lane; i < ma; i += 32) cells[(size_t)(q0 + w) * ma + i] = (int64_t)(cq[i] & 0xffffffffu);
+    return;
+  }
+  // overflow: exact einsum over every cell, exact running selection
+  nb = 0;
+  bn = 0;
+  T = ~0ull;
+  for (int i0 = 0; i0 < K; i0 += 32) {
+    const int k = i0 + lane;
+    uint64_t key = ~0ull;
+    if (k < K) {
+      const float *crow = coarse + (size_t)k * d;
+      float a4[4] = {0.f, 0.f, 0.f, 0.f};
+      int t0 = 0;
+      for (; d - t0 >= 16; t0 += 16)
+        for (int vv = 3; vv >= 0; vv--)
+          for (int l = 0; l < 4; l++) {
+            const int t = t0 + 4 * vv + l;
+            const float df = __fsub_rn(crow[t], qcol[t * kFastQ + w]);
+            a4[l] = __fadd_rn(a4[l], __fmul_rn(df, df));
+          }
+      for (; t0 < d; t0 += 4)
+        for (int l = 0; l < 4; l++) {
+          float pr = 0.f;
+          if (t0 + l < d) {
+            const float df = __fsub_rn(crow[t0 + l], qcol[(t0 + l) * kFastQ + w]);
+            pr = __fmul_rn(df, df);
+          }
+          a4[l] = __fadd_rn(a4[l], pr);
+        }
+      key = ((uint64_t)__float_as_uint(__fadd_rn(__fadd_rn(a4[0], a4[1]), __fadd_rn(a4[2], a4[3]))) << 32) |
+            (uint32_t)k;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, key < T);
+    if (bal) {
+      if (bn + __popc(bal) > kSelBuf) warp_merge(v, nb, bn, ma, T);
+      const bool take2 = key < T;
+      const unsigned bal2 = __ballot_sync(0xffffffffu, take2);
+      if (take2) v[nb + bn + __popc(bal2 & ((1u << lane) - 1))] = key;
+      bn += __popc(bal2);
+      __syncwarp();
+    }
+  }
+  warp_merge(v, nb, bn, ma, T);
+  for (int i = lane; i < ma; i += 32) cells[(size_t)(q0 + w) * ma + i] = (int64_t)(v[i] & 0xffffffffu);
+}
+
 // ---------------- residual + rotation + LUT (adc.py:108-111, 141-148,
 // ivf.py:181-182) ----------------
 // One CTA per (query, probe slot). residual = q - C[cell] in fp32; OPQ
@@ -267,7 +492,32 @@ __global__ void __launch_bounds__(256) k_residual_lut(
   __syncthreads();
   const float *y = sr;
   if (rotation) {
-    if (rot_in_smem && (d & 3) == 0) {
+    if (rot_in_smem && (d & 3) == 0 && np == kLutPairs) {
+      // thread tile: 4 consecutive outputs x 4 pairs (16 accumulators), each
+      // k step = one float4 of R^T and four broadcast residual values
+      const int quads = d >> 2;
+      for (int task = threadIdx.x; task < (kLutPairs / 4) * quads; task += blockDim.x) {
+        const int pg = task / quads, i0 = (task - pg * quads) * 4;
+        const float *r0 = sr + (size_t)(pg * 4) * d;
+        float a[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) a[u][0] = a[u][1] = a[u][2] = a[u][3] = 0.f;
+        for (int k = 0; k < d; k++) {
+          const float4 c = *(const float4 *)(rt + (size_t)k * d + i0);
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const float rv = r0[(size_t)u * d + k];
+            a[u][0] = __fmaf_rn(c.x, rv, a[u][0]);
+            a[u][1] = __fmaf_rn(c.y, rv, a[u][1]);
+            a[u][2] = __fmaf_rn(c.z, rv, a[u][2]);
+            a[u][3] = __fmaf_rn(c.w, rv, a[u][3]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          *(float4 *)(sy + (size_t)(pg * 4 + u) * d + i0) = make_float4(a[u][0], a[u][1], a[u][2], a[u][3]);
+      }
+    } else if (rot_in_smem && (d & 3) == 0) {
       const int quads = d >> 2;
       for (int task = threadIdx.x; task < np * quads; task += blockDim.x) {
         const int p = task / quads, i0 = (task - p * quads) * 4;
@@ -385,14 +635,18 @@ __global__ void __launch_bounds__(256) k_qmax(const uint32_t *__restrict__ codes
 // clipped to 0..127 (delta == 0: v <= qmin -> 0 else 127). Emits the byte
 // tables as 4 words per sub-quantizer (entries 0-7 | 8-15), and the fp32
 // casts of qmin / delta the Cython boundary makes (_kernels.pyx:82-83).
-__global__ void k_quantize(const float *__restrict__ lut, int m,
-                           const float *__restrict__ qmax_q, int nslots,
-                           const double *__restrict__ qmin_in, const double *__restrict__ qmax_in,
-                           uint32_t *__restrict__ qt, float *__restrict__ qmin_f,
-                           float *__restrict__ delta_f, double *__restrict__ delta_out,
-                           uint8_t *__restrict__ qt_bytes) {
-  __shared__ float red[64];
-  const int pair = blockIdx.x;
+// One warp per (query, slot) pair, 8 pairs per CTA.
+__global__ void __launch_bounds__(256) k_quantize(const float *__restrict__ lut, int m, int npairs,
+                                                  const float *__restrict__ qmax_q, int nslots,
+                                                  const double *__restrict__ qmin_in,
+                                                  const double *__restrict__ qmax_in,
+                                                  uint32_t *__restrict__ qt, float *__restrict__ qmin_f,
+                                                  float *__restrict__ delta_f,
+                                                  double *__restrict__ delta_out,
+                                                  uint8_t *__restrict__ qt_bytes) {
+  const int lane = threadIdx.x & 31;
+  const int pair = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (pair >= npairs) return;
   const float *t = lut + (size_t)pair * m * 16;
   double qmin, qmax;
   if (qmin_in) {
@@ -400,21 +654,20 @@ __global__ void k_quantize(const float *__restrict__ lut, int m,
     qmax = qmax_in[pair];
   } else {
     float mn = FLT_MAX;
-    for (int e = threadIdx.x; e < m * 16; e += blockDim.x) mn = fminf(mn, t[e]);
-    red[threadIdx.x] = mn;
-    __syncthreads();
-    for (int s = 32; s > 0; s >>= 1) {
-      if ((int)threadIdx.x < s) red[threadIdx.x] = fminf(red[threadIdx.x], red[threadIdx.x + s]);
-      __syncthreads();
-    }
+    for (int e = lane; e < m * 16; e += 32) mn = fminf(mn, t[e]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     qmax = (double)qmax_q[pair / nslots];
-    qmin = fmin((double)red[0], qmax);
+    qmin = fmin((double)mn, qmax);
   }
   const double delta = __ddiv_rn(__dsub_rn(qmax, qmin), (double)kQuantBins);
-  for (int w = threadIdx.x; w < m * 4; w += blockDim.x) {
+  for (int w = lane; w < m * 4; w += 32) {
+    const float4 v4 = *(const float4 *)(t + w * 4);
+    const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
     uint32_t word = 0;
+#pragma unroll
     for (int b = 0; b < 4; b++) {
-      const double v = (double)t[w * 4 + b];
+      const double v = (double)vv[b];
       double qq;
       if (delta > 0) {
         qq = floor(__ddiv_rn(__dsub_rn(v, qmin), delta));
@@ -428,7 +681,7 @@ __global__ void k_quantize(const float *__restrict__ lut, int m,
     }
     if (qt) qt[(size_t)pair * m * 4 + w] = word;
   }
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     if (qmin_f) qmin_f[pair] = __double2float_rn(qmin);
     if (delta_f) delta_f[pair] = __double2float_rn(delta);
     if (delta_out) delta_out[pair] = delta;
@@ -562,6 +815,29 @@ void launch_probe(const float *coarseT, int K, int d, const float *queries, int 
                                                           vcap, cells);
 }
 
+void launch_cnorm(const float *coarse, int K, int d, float *cn, cudaStream_t st) {
+  k_cnorm<<<(K + 255) / 256, 256, 0, st>>>(coarse, K, d, cn);
+}
+
+bool launch_probe_fast(const float *coarseT, const float *coarse, const float *cn, int K, int d,
+                       const float *queries, int nq, int ma, int64_t *cells, cudaStream_t st) {
+  if (nq <= 0) return true;
+  if (ma > kCandCap / 2 || ma > K) return false;
+  int vcap = 1;
+  while (vcap < ma + kSelBuf) vcap <<= 1;
+  static_assert(kCandCap * 8 <= kFastTile * 4, "candidates reuse a U row");
+  const size_t smem = (size_t)kFastQ * vcap * 8 + (size_t)kFastQ * kFastTile * 4 +
+                      (size_t)kFastQ * d * 4;
+  if (smem > 220 * 1024) return false;
+  float *Lbuf = nullptr;
+  if (cudaMallocAsync(&Lbuf, (size_t)nq * K * 4, st) != cudaSuccess) return false;
+  cudaFuncSetAttribute(k_probe_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_probe_fast<<<(nq + kFastQ - 1) / kFastQ, 256, smem, st>>>(coarseT, coarse, cn, K, d, queries,
+                                                             nq, ma, vcap, Lbuf, cells);
+  cudaFreeAsync(Lbuf, st);
+  return true;
+}
+
 void launch_residual_lut(const qadc_b200_index *idx, const float *queries, const int64_t *cells,
                          int nq, int nslots, float *lut, cudaStream_t st) {
   if (nq <= 0) return;
@@ -592,8 +868,9 @@ void launch_quantize(const float *lut, int npairs, int m, const float *qmax_per_
                      const double *qmin_in, const double *qmax_in, uint32_t *qt, float *qmin_f,
                      float *delta_f, double *delta_out, uint8_t *qt_bytes_out, cudaStream_t st) {
   if (npairs <= 0) return;
-  k_quantize<<<npairs, 64, 0, st>>>(lut, m, qmax_per_query, nslots, qmin_in, qmax_in, qt, qmin_f,
-                                    delta_f, delta_out, qt_bytes_out);
+  k_quantize<<<(npairs + 7) / 8, 256, 0, st>>>(lut, m, npairs, qmax_per_query, nslots, qmin_in,
+                                                qmax_in, qt, qmin_f, delta_f, delta_out,
+                                                qt_bytes_out);
 }
 
 void launch_prefix(const qadc_b200_index *idx, const uint32_t *qt, const float *qmin_f,

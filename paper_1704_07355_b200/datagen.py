@@ -39,9 +39,12 @@ SIFT_LIKE = Mixture(d=128, components=256, centre_high=100.0, sigma=10.0)
 GIST_LIKE = Mixture(d=960, components=512, centre_high=1.0, sigma=0.05)
 
 
-def mixture_numpy(mix: Mixture, n: int, seed: int, stream: int) -> np.ndarray:
-    """n vectors (float32) drawn chunk by chunk, reproducible per chunk."""
-    cen = mix.centres(seed)
+def mixture_numpy(mix: Mixture, n: int, seed: int, stream: int,
+                  centre_seed: int | None = None) -> np.ndarray:
+    """n vectors (float32) drawn chunk by chunk, reproducible per chunk.
+    `centre_seed` (default: seed) picks the mixture's centres, so learn,
+    base and query splits of one corpus share them."""
+    cen = mix.centres(seed if centre_seed is None else centre_seed)
     out = np.empty((n, mix.d), dtype=np.float32)
     for c0 in range(0, n, CHUNK):
         k = min(CHUNK, n - c0)
@@ -53,11 +56,12 @@ def mixture_numpy(mix: Mixture, n: int, seed: int, stream: int) -> np.ndarray:
     return out
 
 
-def mixture_torch(mix: Mixture, n: int, seed: int, stream: int, device="cuda"):
+def mixture_torch(mix: Mixture, n: int, seed: int, stream: int, device="cuda",
+                  centre_seed: int | None = None):
     """Same distribution drawn on the GPU (torch Philox), chunk-seeded."""
     import torch
 
-    cen = torch.from_numpy(mix.centres(seed)).to(device)
+    cen = torch.from_numpy(mix.centres(seed if centre_seed is None else centre_seed)).to(device)
     out = torch.empty((n, mix.d), dtype=torch.float32, device=device)
     g = torch.Generator(device=device)
     for c0 in range(0, n, CHUNK):

@@ -40,6 +40,9 @@ CONFIGS = {
 }
 
 SEED = 1
+# every split (learn: bench_data/make_*.py, base, queries) draws around the
+# centres of corpus 0, so queries come from the base's distribution
+CORPUS = 0
 
 
 class _PQ:
@@ -71,7 +74,7 @@ def shard_codes(cfg: FlatConfig, pq: _PQ, n: int, shard: int, device="cuda"):
     step = datagen.CHUNK
     for c0 in range(0, n, 4 * step):
         k = min(4 * step, n - c0)
-        X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + shard,
+        X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + shard, centre_seed=CORPUS,
                                   stream=datagen.STREAM_BASE * 100 + c0 // (4 * step),
                                   device=device)
         out[c0:c0 + k] = encode_device(pq, X)
@@ -80,7 +83,8 @@ def shard_codes(cfg: FlatConfig, pq: _PQ, n: int, shard: int, device="cuda"):
 
 
 def queries(cfg: FlatConfig, q: int | None = None) -> np.ndarray:
-    return datagen.mixture_numpy(cfg.mix, q or cfg.q, seed=SEED, stream=datagen.STREAM_QUERY)
+    return datagen.mixture_numpy(cfg.mix, q or cfg.q, seed=SEED, stream=datagen.STREAM_QUERY,
+                                 centre_seed=CORPUS)
 
 
 def build_shard_index(cfg: FlatConfig, pq: _PQ, n: int, rank: int, world: int, prefix: int):
@@ -149,7 +153,7 @@ def build_ivf_index(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, shard: 
     labels = torch.empty(n, dtype=torch.int64, device=device)
     for c0 in range(0, n, chunk):
         k = min(chunk, n - c0)
-        X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + shard,
+        X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + shard, centre_seed=CORPUS,
                                   stream=datagen.STREAM_BASE * 100 + c0 // chunk, device=device)
         lab = assign_device(coarse, X)
         labels[c0:c0 + k] = lab

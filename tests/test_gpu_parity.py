@@ -405,3 +405,32 @@ def test_probe_vs_oracle_many_sizes(gpu, K, ma):
     for q in qs:
         want, _ = orc.probe(cen, q, ma)
         assert np.array_equal(ivf.probe(index, q, ma).cells, want)
+
+
+@pytest.mark.parametrize("K,ma,distinct", [(4096, 16, 4096), (4096, 64, 20), (1003, 8, 3),
+                                           (70000, 32, 70000)])
+def test_probe_batch_bounds_and_tie_fallback(gpu, K, ma, distinct):
+    """Batched native probe (nq not a multiple of the 8-query CTA) against
+    the oracle. `distinct` < K repeats centroids so that hundreds of cells
+    share the exact same d2: the FFMA pre-selection then keeps more
+    candidates than its buffer and the exact all-cells fallback runs."""
+    import torch
+    from paper_1704_07355_b200 import _native, datagen
+    base = datagen.mixture_numpy(datagen.SIFT_LIKE, distinct, seed=K + distinct, stream=1)
+    cen = np.ascontiguousarray(base[np.arange(K) % distinct])
+    qs = datagen.mixture_numpy(datagen.SIFT_LIKE, 13, seed=K, stream=4)
+    qs[1] = cen[5]
+    qs[2] = 0.0
+    dev = torch.device("cuda")
+    cd, qd = torch.from_numpy(cen).to(dev), torch.from_numpy(qs).to(dev)
+    cells = torch.empty((13, ma), dtype=torch.int64, device=dev)
+    res = torch.empty((13, ma, 128), dtype=torch.float32, device=dev)
+    lib = _native.load_library()
+    _native.check(lib.qadc_b200_probe(_native.dptr(cd), K, 128, _native.dptr(qd), 13, ma,
+                                      _native.dptr(cells), _native.dptr(res),
+                                      torch.cuda.current_stream().cuda_stream), "probe")
+    got = cells.cpu().numpy()
+    for i in range(13):
+        want, wres = orc.probe(cen, qs[i], ma)
+        assert np.array_equal(got[i], want), i
+        assert np.array_equal(_bits(res[i].cpu().numpy()), _bits(wres))
