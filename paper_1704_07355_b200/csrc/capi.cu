@@ -1,6 +1,7 @@
 // C ABI of libqadc_b200 (include/qadc_b200.h): the reference kernel ABI
 // (scan_kernels.h:15-46) re-implemented on sm_100a, plus the batched
 // device-resident search (adc.py:114-187 for many queries at once).
+#include <cstdio>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -164,7 +165,9 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   DevBuf<unsigned long long> ncodes;
   DevBuf<int64_t> fsat_id, cand_id;
   DevBuf<int32_t> pair_q, pair_t;
-  DevBuf<WorkItem> items;
+  DevBuf<WorkItem> items, items_ord;
+  DevBuf<uint8_t> pair_depth;
+  DevBuf<unsigned> cls;
   int rc = 0;
 
   const int64_t *cells = nullptr;
@@ -196,12 +199,18 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
       cand_mid.alloc((int64_t)nq * cap_g, st) || cand_id.alloc((int64_t)nq * cap_g, st) ||
       pair_q.alloc(npairs, st) || pair_t.alloc(npairs, st) || n_items.alloc(1, st) ||
       counter.alloc(1, st) || scratch.alloc(6 * (int64_t)nl + 8, st) || overflow.alloc(nq, st) ||
-      ncodes.alloc(1, st))
+      ncodes.alloc(1, st) || pair_depth.alloc(npairs, st))
     return cuda_fail(cudaGetLastError(), "alloc workspace");
+  // tuning knobs (defaults are the measured best): byte-sum depth cap and
+  // the half-tile loop for tiles with <= QT/2 queries
+  static const int max_depth = std::min(16, std::max(2, scan_env_int("QADC_B200_MAX_DEPTH", 16)));
+  static const int no_half = scan_env_int("QADC_B200_NO_HALF", 0);
+  static const int variant_stats = scan_env_int("QADC_B200_VARIANT_STATS", 0);
+  static const int no_order = scan_env_int("QADC_B200_NO_ORDER", 0);
 
   launch_qmax(idx, lut, cells, nq, nslots, R, init, qmax_b.p, st);
   launch_quantize(lut, (int)npairs, m, qmax_b.p, nslots, nullptr, nullptr, qt_b.p, qmin_f.p,
-                  delta_f.p, nullptr, nullptr, st);
+                  delta_f.p, nullptr, nullptr, st, max_depth, pair_depth.p);
   launch_prefix(idx, qt_b.p, qmin_f.p, delta_f.p, cells, nq, nslots, R, init, M_bits.p, fsat_n.p,
                 fsat_mid.p, fsat_id.p, st);
   k_init_bounds<<<gridn(nq), 256, 0, st>>>(M_bits.p, M_override, hist_w.p, nq);
@@ -230,7 +239,11 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   if (items.alloc(max_items, st)) return cuda_fail(cudaGetLastError(), "alloc items");
   build_work(idx, cells, nq, nslots, qt_tile, range_chunks, pair_q.p, pair_t.p, items.p, n_items.p,
              scratch.p, max_items, st);
-  ss.launches += 4;
+  if (items_ord.alloc(max_items, st) || cls.alloc(order_items_scratch(max_items), st))
+    return cuda_fail(cudaGetLastError(), "alloc items");
+  order_items(items.p, n_items.p, max_items, pair_t.p, pair_depth.p, no_half ? 0 : qt_tile / 2,
+              cls.p, items_ord.p, st);
+  ss.launches += 7;
 
   // ---- scan ----
   cudaMemsetAsync(cand_n.p, 0, sizeof(unsigned) * nq, st);
@@ -242,7 +255,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   a.codes = idx->codes;
   a.valid = idx->valid;
   a.ids = idx->ids;
-  a.items = items.p;
+  a.items = no_order ? items.p : items_ord.p;
   a.n_items = n_items.p;
   a.item_counter = counter.p;
   a.pair_q = pair_q.p;
@@ -283,6 +296,12 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   QADC_CUDA(cudaMemcpyAsync(&h_codes, ncodes.p, sizeof(h_codes), cudaMemcpyDeviceToHost, st));
   QADC_CUDA(cudaStreamSynchronize(st));
   if (depth == 0) ss.codes += (int64_t)h_codes;
+  if (variant_stats) {
+    unsigned v[8];
+    cudaMemcpy(v, cls.p, sizeof(v), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "qadc_b200 scan items by variant (full D16 D8 D4 D2 | half D16 D8 D4 D2):"
+            " %u %u %u %u | %u %u %u %u\n", v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+  }
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   ss.scan_us += ms * 1e3;

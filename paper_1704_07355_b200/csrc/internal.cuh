@@ -83,7 +83,8 @@ void launch_qmax(const qadc_b200_index *idx, const float *lut,
 void launch_quantize(const float *lut, int npairs, int m, const float *qmax_per_query,
                      int nslots, const double *qmin_in, const double *qmax_in,
                      uint32_t *qt, float *qmin_f, float *delta_f,
-                     double *delta_out, uint8_t *qt_bytes_out, cudaStream_t st);
+                     double *delta_out, uint8_t *qt_bytes_out, cudaStream_t st,
+                     int max_depth = 16, uint8_t *pair_depth = nullptr);
 void launch_prefix(const qadc_b200_index *idx, const uint32_t *qt,
                    const float *qmin_f, const float *delta_f,
                    const int64_t *cells, int nq, int nslots, int R, int init,
@@ -95,7 +96,7 @@ struct WorkItem {
   int32_t list;
   int32_t pair_begin;   // index into the list-grouped pair arrays
   int32_t pair_count;   // <= QT
-  int32_t pad;
+  int32_t variant;      // depth | half << 8 | class << 16 (order_items)
   int64_t chunk_begin;  // absolute chunk index
   int64_t chunk_end;
 };
@@ -127,6 +128,7 @@ struct ScanArgs {
 constexpr int kHistBins = 1024;                 // 32 coarse x 32 fine
 constexpr int kHistWords = kHistBins + 32;      // fine bins, then coarse sums
 int scan_qt_per_cta(int m);
+int scan_env_int(const char *name, int dflt);
 void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st);
 // Work-list construction (device side): returns item upper bound.
 int64_t build_work(const qadc_b200_index *idx, const int64_t *cells, int nq,
@@ -134,6 +136,16 @@ int64_t build_work(const qadc_b200_index *idx, const int64_t *cells, int nq,
                    int32_t *pair_q, int32_t *pair_t, WorkItem *items,
                    int *n_items, int *scratch_list_pairs, int64_t max_items,
                    cudaStream_t st);
+
+// Tag every item with its scan loop variant (byte-sum depth = min over its
+// pairs' depth, half tile or not) and reorder items class by class, so the
+// CTAs running at any moment share one loop body (instruction cache).
+// scratch: order_items_scratch(max_items) unsigned, [0, 8) = items per
+// class afterwards. qh: pair_count <= qh runs the half loop.
+int64_t order_items_scratch(int64_t max_items);
+void order_items(const WorkItem *items, const int *n_items, int64_t max_items,
+                 const int32_t *pair_t, const uint8_t *pair_depth, int qh, unsigned *scratch,
+                 WorkItem *out, cudaStream_t st);
 
 // ---- select.cu ----
 int select_capacity();

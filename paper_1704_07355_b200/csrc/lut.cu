@@ -643,10 +643,17 @@ __global__ void __launch_bounds__(256) k_quantize(const float *__restrict__ lut,
                                                   uint32_t *__restrict__ qt, float *__restrict__ qmin_f,
                                                   float *__restrict__ delta_f,
                                                   double *__restrict__ delta_out,
-                                                  uint8_t *__restrict__ qt_bytes) {
+                                                  uint8_t *__restrict__ qt_bytes, int max_depth,
+                                                  uint8_t *__restrict__ pair_depth) {
+  __shared__ unsigned s_rmax[8][kMaxM];
   const int lane = threadIdx.x & 31;
   const int pair = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (pair >= npairs) return;
+  unsigned *rmax = s_rmax[threadIdx.x >> 5];
+  if (pair_depth) {
+    for (int j = lane; j < m; j += 32) rmax[j] = 0;
+    __syncwarp();
+  }
   const float *t = lut + (size_t)pair * m * 16;
   double qmin, qmax;
   if (qmin_in) {
@@ -680,6 +687,30 @@ __global__ void __launch_bounds__(256) k_quantize(const float *__restrict__ lut,
       if (qt_bytes) qt_bytes[(size_t)pair * m * 16 + w * 4 + b] = (uint8_t)byte;
     }
     if (qt) qt[(size_t)pair * m * 4 + w] = word;
+    if (pair_depth) {
+      const uint32_t mx = __vmaxu4(word, word >> 16);
+      atomicMax(&rmax[w >> 2], max(mx & 255u, (mx >> 8) & 255u));
+    }
+  }
+  if (pair_depth) {
+    // byte-sum depth of this pair's scan: the largest D in {16, 8, 4, 2}
+    // (<= max_depth) such that every aligned group of D sub-quantizers has
+    // row maxima summing to <= 255, so D byte lanes add without carry
+    // (D = 2 always holds: entries are <= 127)
+    __syncwarp();
+    if (lane == 0) {
+      int dd = max_depth;
+      for (; dd > 2; dd >>= 1) {
+        bool ok = true;
+        for (int j0 = 0; j0 < m && ok; j0 += dd) {
+          unsigned sum = 0;
+          for (int j = j0; j < min(j0 + dd, m); j++) sum += rmax[j];
+          ok = sum <= 255u;
+        }
+        if (ok) break;
+      }
+      pair_depth[pair] = (uint8_t)dd;
+    }
   }
   if (lane == 0) {
     if (qmin_f) qmin_f[pair] = __double2float_rn(qmin);
@@ -866,11 +897,12 @@ void launch_qmax(const qadc_b200_index *idx, const float *lut, const int64_t *ce
 
 void launch_quantize(const float *lut, int npairs, int m, const float *qmax_per_query, int nslots,
                      const double *qmin_in, const double *qmax_in, uint32_t *qt, float *qmin_f,
-                     float *delta_f, double *delta_out, uint8_t *qt_bytes_out, cudaStream_t st) {
+                     float *delta_f, double *delta_out, uint8_t *qt_bytes_out, cudaStream_t st,
+                     int max_depth, uint8_t *pair_depth) {
   if (npairs <= 0) return;
   k_quantize<<<(npairs + 7) / 8, 256, 0, st>>>(lut, m, npairs, qmax_per_query, nslots, qmin_in,
                                                 qmax_in, qt, qmin_f, delta_f, delta_out,
-                                                qt_bytes_out);
+                                                qt_bytes_out, max_depth, pair_depth);
 }
 
 void launch_prefix(const qadc_b200_index *idx, const uint32_t *qt, const float *qmin_f,

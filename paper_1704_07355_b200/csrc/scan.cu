@@ -45,8 +45,6 @@ struct Smem {
   unsigned mc[kWarps][16];
   int bn[kWarps][16];
   unsigned hist[256];
-  int depth;
-  uint8_t rmax[16 * kMaxM];
 };
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -482,41 +480,16 @@ k_scan(const __grid_constant__ ScanArgs a) {
     if (threadIdx.x == 0) {
       s.pair_count = it.pair_count;
       s.chunk_begin = it.chunk_begin;
-      s.depth = 16;
-    }
-    __syncthreads();
-    // byte-sum depth of this tile: the largest D in {16, 8, 4, 2} such that
-    // every aligned group of D sub-quantizers has sum of row maxima <= 255
-    // for every query (D = 2 always holds: entries are <= 127)
-    for (int e = threadIdx.x; e < QT * m; e += blockDim.x) {
-      const uint4 v = s_tab[e];
-      uint32_t mx = __vmaxu4(__vmaxu4(v.x, v.y), __vmaxu4(v.z, v.w));
-      mx = max(max(mx & 255u, (mx >> 8) & 255u), max((mx >> 16) & 255u, mx >> 24));
-      s.rmax[e] = (uint8_t)mx;
-    }
-    __syncthreads();
-    if (threadIdx.x < QT) {
-      const int q = threadIdx.x;
-      int dd = 16;
-      for (; dd > 2; dd >>= 1) {
-        bool ok = true;
-        for (int j0 = 0; j0 < m && ok; j0 += dd) {
-          int sum = 0;
-          for (int j = j0; j < min(j0 + dd, m); j++) sum += s.rmax[q * m + j];
-          ok = sum <= 255;
-        }
-        if (ok) break;
-      }
-      atomicMin(&s.depth, dd);
     }
     __syncthreads();
     const int nq_tile = s.pair_count;
-    const int depth = s.depth;
+    const int depth = it.variant & 255;  // order_items: min pair depth of the tile
     // ---- warp loop over chunks (one specialization per byte-sum depth) ----
     // tiles with at most half the query slots in use (the last tile of an
     // inverted list) run the QT/2 loop instead of computing empty slots
     constexpr int QH = QT / 2 > 0 ? QT / 2 : 1;
-    if (QH < QT && nq_tile <= QH) {
+    const bool half = QH < QT && ((it.variant >> 8) & 1);
+    if (half) {
       switch (depth) {
         case 16: chunk_loop<16, MC, QH>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
         case 8: chunk_loop<8, MC, QH>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
@@ -667,7 +640,7 @@ __global__ void k_emit_items(const int *__restrict__ list_pairs, const int *__re
         wi.list = L;
         wi.pair_begin = pair_off[L] + t * qt_tile;
         wi.pair_count = min(qt_tile, p - t * qt_tile);
-        wi.pad = 0;
+        wi.variant = 0;
         wi.chunk_begin = c0 + r * range_chunks;
         wi.chunk_end = min(c0 + nch, wi.chunk_begin + range_chunks);
         items[o++] = wi;
@@ -676,10 +649,93 @@ __global__ void k_emit_items(const int *__restrict__ list_pairs, const int *__re
   }
 }
 
+// Stable partition of the items by loop variant (class), 256 items per
+// block: class + per-block class counts, a scan over blocks, then a scatter
+// that keeps the original order inside each class (list / tile / range
+// order is what keeps concurrently running CTAs on shared L2 lines).
+__global__ void k_item_class(WorkItem *__restrict__ items, const int *__restrict__ n_items,
+                             const int32_t *__restrict__ pair_t,
+                             const uint8_t *__restrict__ pair_depth, int qh,
+                             unsigned *__restrict__ blk_cnt) {
+  __shared__ unsigned cnt[8];
+  if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < *n_items) {
+    const WorkItem it = items[i];
+    int d = 16;
+    for (int q = 0; q < it.pair_count; q++) d = min(d, (int)pair_depth[pair_t[it.pair_begin + q]]);
+    const int half = it.pair_count <= qh ? 1 : 0;
+    const int cls = half * 4 + (d >= 16 ? 0 : d >= 8 ? 1 : d >= 4 ? 2 : 3);
+    items[i].variant = d | (half << 8) | (cls << 16);
+    atomicAdd(&cnt[cls], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) blk_cnt[blockIdx.x * 8 + threadIdx.x] = cnt[threadIdx.x];
+}
+
+__global__ void k_item_offsets(unsigned *__restrict__ blk_cnt, int nblk, unsigned *__restrict__ cls_n) {
+  __shared__ unsigned tot[8];
+  const int c = threadIdx.x;
+  if (c < 8) {
+    unsigned t = 0;
+    for (int b = 0; b < nblk; b++) t += blk_cnt[b * 8 + c];
+    tot[c] = t;
+    cls_n[c] = t;
+  }
+  __syncthreads();
+  if (c < 8) {
+    unsigned o = 0;
+    for (int k = 0; k < c; k++) o += tot[k];
+    for (int b = 0; b < nblk; b++) {
+      const unsigned v = blk_cnt[b * 8 + c];
+      blk_cnt[b * 8 + c] = o;
+      o += v;
+    }
+  }
+}
+
+__global__ void k_item_scatter(const WorkItem *__restrict__ in, const int *__restrict__ n_items,
+                               const unsigned *__restrict__ blk_off, WorkItem *__restrict__ out) {
+  __shared__ unsigned char cls_of[256];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ok = i < *n_items;
+  WorkItem it;
+  int cls = 8;
+  if (ok) {
+    it = in[i];
+    cls = (it.variant >> 16) & 7;
+  }
+  cls_of[threadIdx.x] = (unsigned char)cls;
+  __syncthreads();
+  if (!ok) return;
+  unsigned r = 0;
+  for (int k = 0; k < (int)threadIdx.x; k++) r += cls_of[k] == cls;
+  out[blk_off[blockIdx.x * 8 + cls] + r] = it;
+}
+
 }  // namespace
+
+int64_t order_items_scratch(int64_t max_items) { return ((max_items + 255) / 256) * 8 + 16; }
+
+void order_items(const WorkItem *items, const int *n_items, int64_t max_items,
+                 const int32_t *pair_t, const uint8_t *pair_depth, int qh, unsigned *scratch,
+                 WorkItem *out, cudaStream_t st) {
+  const int nblk = (int)std::max<int64_t>((max_items + 255) / 256, 1);
+  unsigned *cls_n = scratch, *blk = scratch + 16;
+  k_item_class<<<nblk, 256, 0, st>>>(const_cast<WorkItem *>(items), n_items, pair_t, pair_depth,
+                                     qh, blk);
+  k_item_offsets<<<1, 32, 0, st>>>(blk, nblk, cls_n);
+  k_item_scatter<<<nblk, 256, 0, st>>>(items, n_items, blk, out);
+}
 
 // Queries per tile: 8 by default (selector construction amortized over 8
 // queries at 96 registers, 5 CTAs/SM); QADC_B200_QT=4|16 overrides (tuning).
+int scan_env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 int scan_qt_per_cta(int m) {
   static int env = -1;
   if (env < 0) {
