@@ -273,6 +273,8 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   a.cap_l = (std::max(R + 128, 256) + 31) / 32 * 32;
   a.m = m;
   a.R = R;
+  static const int bound_every = std::max(1, scan_env_int("QADC_B200_BOUND_EVERY", 32));
+  a.bound_every = bound_every;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

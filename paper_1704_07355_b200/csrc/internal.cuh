@@ -123,6 +123,7 @@ struct ScanArgs {
   int cap_l;               // per-warp per-query buffer capacity
   int m;
   int R;
+  int bound_every;         // appended candidates between global-histogram bound reads
 };
 
 constexpr int kHistBins = 1024;                 // 32 coarse x 32 fine

@@ -40,11 +40,12 @@ struct Smem {
   int query[16];
   float qmin[16];
   float delta[16];
+  float hinv[16];  // 1 / histogram bucket width of the query (0: no histogram)
   int thr[kWarps][16];
   unsigned kbias[kWarps][16];
   unsigned mc[kWarps][16];
   int bn[kWarps][16];
-  unsigned hist[256];
+  int pend[kWarps][16];  // appended since this warp last read the global histogram
 };
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -93,13 +94,6 @@ __device__ __forceinline__ unsigned hist_bound(const ScanArgs &a, int query) {
   const unsigned hit2 = __ballot_sync(kFull, base + fi >= R);
   const int b = k * 32 + (hit2 ? __ffs(hit2) - 1 : 31);
   return fbits(__fmul_rn((float)(b + 2), hw));
-}
-
-__device__ __forceinline__ void hist_add(const ScanArgs &a, int query, float hw, float mid) {
-  const int b = min((int)(mid / hw), kHistBins - 1);
-  unsigned *h = a.hist + (size_t)query * kHistWords;
-  atomicAdd(&h[b], 1u);
-  atomicAdd(&h[kHistBins + (b >> 5)], 1u);
 }
 
 // Global append of every buffered entry of (warp, q) whose midpoint is <=
@@ -181,66 +175,79 @@ __device__ __noinline__ void compact_buffer(const ScanArgs &a, Smem &s, uint32_t
   __syncwarp();
 }
 
-// Append this lane's surviving codes (mask8 bit k = code 8*lane + k of the
-// chunk; byte k of vals = its lane distance) to (warp, q)'s buffer.
-__device__ __noinline__ void append(const ScanArgs &a, Smem &s, uint32_t *buf, int w, int q,
-                                    uint32_t mask8, uint32_t v0, uint32_t v1, int chunk_local) {
-  const int lane = threadIdx.x & 31;
-  int cnt = __popc(mask8);
-  int incl = cnt;
+// Warp-wide count of the set bits of every lane's 4-bit mask: codes in
+// lanes below this one, and in the whole warp.
+__device__ __forceinline__ void count4(uint32_t m4, int &before, int &total) {
+  const unsigned lt = (1u << (threadIdx.x & 31)) - 1;
+  before = 0;
+  total = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += y;
+  for (int k = 0; k < 4; k++) {
+    const unsigned b = __ballot_sync(kFull, (m4 >> k) & 1u);
+    before += __popc(b & lt);
+    total += __popc(b);
   }
-  int total = __shfl_sync(kFull, incl, 31);
+}
+
+// Append this lane's surviving codes (mask4 bit k = code base_idx + k of
+// the item; byte k of vals = its lane distance) to (warp, q)'s buffer.
+__device__ __noinline__ void append(const ScanArgs &a, Smem &s, uint32_t *buf, int w, int q,
+                                    uint32_t mask4, uint32_t vals, uint32_t base_idx) {
+  const int lane = threadIdx.x & 31;
+  int before, total;
+  count4(mask4, before, total);
   int n = s.bn[w][q];
   if (n + total > a.cap_l) {  // n > cap_l - 128 >= R
     if (n >= a.R) compact_buffer(a, s, buf, w, q);
     // re-filter with the (possibly) tightened threshold
     const int thr = s.thr[w][q];
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const int v = (int)(((k < 4 ? v0 : v1) >> (8 * (k & 3))) & 255);
-      if (v > thr) mask8 &= ~(1u << k);
-    }
-    cnt = __popc(mask8);
-    incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += y;
-    }
-    total = __shfl_sync(kFull, incl, 31);
+    for (int k = 0; k < 4; k++)
+      if ((int)((vals >> (8 * k)) & 255u) > thr) mask4 &= ~(1u << k);
+    count4(mask4, before, total);
     n = s.bn[w][q];
     if (n + total > a.cap_l) {
       flush_buffer(a, s, buf, w, q);
       n = 0;
     }
   }
-  int off = n + incl - cnt;
-  const uint32_t base_idx = (uint32_t)chunk_local * kChunkCodes + 8u * lane;
+  int off = n + before;
   const int query = s.query[q];
-  const float hw = a.hist_w[query], qmin = s.qmin[q], delta = s.delta[q];
+  const float hinv = s.hinv[q], qmin = s.qmin[q], delta = s.delta[q];
+  unsigned *h = a.hist + (size_t)query * kHistWords;
 #pragma unroll
-  for (int k = 0; k < 8; k++) {
-    if (mask8 & (1u << k)) {
-      const uint32_t v = ((k < 4 ? v0 : v1) >> (8 * (k & 3))) & 255u;
+  for (int k = 0; k < 4; k++) {
+    if (mask4 & (1u << k)) {
+      const uint32_t v = (vals >> (8 * k)) & 255u;
       buf[off++] = (v << 24) | (base_idx + k);
-      if (hw > 0.f) hist_add(a, query, hw, midpoint(qmin, delta, (int)v));
+      if (hinv > 0.f) {
+        // bucket floor(mid / w) up to one bucket either way (hist_bound's
+        // (b + 2) * w keeps one bucket of slack)
+        const int b = min((int)__fmul_rn(midpoint(qmin, delta, (int)v), hinv), kHistBins - 1);
+        atomicAdd(&h[b], 1u);
+        atomicAdd(&h[kHistBins + (b >> 5)], 1u);
+      }
     }
   }
+  const int pend = s.pend[w][q] + total;
   __syncwarp();
-  if (lane == 0) s.bn[w][q] = n + total;
+  if (lane == 0) {
+    s.bn[w][q] = n + total;
+    s.pend[w][q] = pend >= a.bound_every ? 0 : pend;
+  }
   // the union of all warps' candidates may now bound the query tighter
-  const unsigned mb = hist_bound(a, query);
-  if (lane == 0 && mb < s.mc[w][q]) {
-    atomicMin(&a.M_bits[query], mb);
-    s.mc[w][q] = mb;
-    const int t = q_threshold(__uint_as_float(mb), qmin, delta);
-    if (t < s.thr[w][q]) {
-      s.thr[w][q] = t;
-      s.kbias[w][q] = kbias_of(t);
+  // (read once per bound_every appended candidates: the histogram read and
+  // its two warp scans cost more than the appends themselves)
+  if (pend >= a.bound_every) {
+    const unsigned mb = hist_bound(a, query);
+    if (lane == 0 && mb < s.mc[w][q]) {
+      atomicMin(&a.M_bits[query], mb);
+      s.mc[w][q] = mb;
+      const int t = q_threshold(__uint_as_float(mb), qmin, delta);
+      if (t < s.thr[w][q]) {
+        s.thr[w][q] = t;
+        s.kbias[w][q] = kbias_of(t);
+      }
     }
   }
   __syncwarp();
@@ -260,10 +267,11 @@ __device__ __noinline__ void candidates(const ScanArgs &a, Smem &s, uint32_t *bu
   mask8 &= valid8;
   const uint32_t v0 = prmt(E0, O0, 0x6240), v1 = prmt(E1, O1, 0x6240);  // low bytes
   // at most 4 codes per lane per append: the buffer needs R + 128 slots
+  const uint32_t base_idx = (uint32_t)chunk_local * kChunkCodes + 8u * (threadIdx.x & 31);
   if (__any_sync(kFull, (mask8 & 0x0fu) != 0))
-    append(a, s, buf, w, q, mask8 & 0x0fu, v0, v1, chunk_local);
+    append(a, s, buf, w, q, mask8 & 0x0fu, v0, base_idx);
   if (__any_sync(kFull, (mask8 & 0xf0u) != 0))
-    append(a, s, buf, w, q, mask8 & 0xf0u, v0, v1, chunk_local);
+    append(a, s, buf, w, q, mask8 >> 4, v1, base_idx + 4);
 }
 
 // Refresh each query's threshold from the global bound (lanes in parallel).
@@ -463,18 +471,22 @@ k_scan(const __grid_constant__ ScanArgs a) {
         s.query[q] = query;
         s.qmin[q] = a.qmin_f[t];
         s.delta[q] = a.delta_f[t];
+        const float hw = a.hist_w[query];
+        s.hinv[q] = hw > 0.f ? __frcp_rn(hw) : 0.f;
         mb = *(volatile unsigned *)&a.M_bits[query];
         thr = q_threshold(__uint_as_float(mb), s.qmin[q], s.delta[q]);
       } else {
         s.query[q] = 0;
         s.qmin[q] = 0.f;
         s.delta[q] = 0.f;
+        s.hinv[q] = 0.f;
       }
       for (int ww = 0; ww < kWarps; ww++) {
         s.thr[ww][q] = thr;
         s.kbias[ww][q] = kbias_of(thr);
         s.mc[ww][q] = mb;
         s.bn[ww][q] = 0;
+        s.pend[ww][q] = 0;
       }
     }
     if (threadIdx.x == 0) {
@@ -505,24 +517,37 @@ k_scan(const __grid_constant__ ScanArgs a) {
       }
     }
     // ---- end of item: CTA-level bound per query (the R-th smallest value
-    // over all four warps' buffers lowers the global M), then publish ----
+    // over all four warps' buffers lowers the global M), all queries of the
+    // tile in one pass: 256 bins as packed 16-bit pairs (<= 4 * cap_l
+    // entries per query), then one warp per query scans them ----
     __syncthreads();
-    for (int q = 0; q < nq_tile; q++) {
-      int tot = 0;
-      for (int ww = 0; ww < kWarps; ww++) tot += s.bn[ww][q];
-      if (tot < a.R) continue;  // uniform: s.bn is stable after the barrier
-      for (int i = threadIdx.x; i < 256; i += blockDim.x) s.hist[i] = 0;
+    {
+      uint32_t *s_h = s_buf + (size_t)kWarps * QT * a.cap_l;  // [QT][128]
+      for (int i = threadIdx.x; i < QT * 128; i += blockDim.x) s_h[i] = 0;
       __syncthreads();
-      for (int ww = 0; ww < kWarps; ww++) {
-        const int n = s.bn[ww][q];
-        const uint32_t *b = s_buf + ((size_t)ww * QT + q) * a.cap_l;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&s.hist[b[i] >> 24], 1u);
+      for (int q = 0; q < nq_tile; q++) {
+        int tot = 0;
+        for (int ww = 0; ww < kWarps; ww++) tot += s.bn[ww][q];
+        if (tot < a.R) continue;  // uniform: s.bn is stable after the barrier
+        for (int ww = 0; ww < kWarps; ww++) {
+          const int n = s.bn[ww][q];
+          const uint32_t *b = s_buf + ((size_t)ww * QT + q) * a.cap_l;
+          for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint32_t v = b[i] >> 24;
+            atomicAdd(&s_h[q * 128 + (v >> 1)], 1u << ((v & 1u) * 16));
+          }
+        }
       }
       __syncthreads();
-      if (w == 0) {
+      for (int q = w; q < nq_tile; q += kWarps) {
+        int tot = 0;
+        for (int ww = 0; ww < kWarps; ww++) tot += s.bn[ww][q];
+        if (tot < a.R) continue;
+        const uint4 h4 = *(const uint4 *)&s_h[q * 128 + lane * 4];  // bins 8*lane .. +7
+        const uint32_t hw[4] = {h4.x, h4.y, h4.z, h4.w};
         unsigned c = 0;
 #pragma unroll
-        for (int i = 0; i < 8; i++) c += s.hist[lane * 8 + i];
+        for (int i = 0; i < 4; i++) c += (hw[i] & 0xffffu) + (hw[i] >> 16);
         unsigned incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -534,13 +559,12 @@ k_scan(const __grid_constant__ ScanArgs a) {
           unsigned cum = incl - c;
           int t = lane * 8;
           for (int i = 0; i < 8; i++, t++) {
-            cum += s.hist[t];
+            cum += (hw[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
             if (cum >= (unsigned)a.R) break;
           }
           atomicMin(&a.M_bits[s.query[q]], fbits(midpoint(s.qmin[q], s.delta[q], t)));
         }
       }
-      __syncthreads();
     }
     for (int q = 0; q < nq_tile; q++) flush_buffer(a, s, wbuf + q * a.cap_l, w, q);
     __syncthreads();
@@ -550,7 +574,7 @@ k_scan(const __grid_constant__ ScanArgs a) {
 template <int MC, int QT>
 void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
   const int m = MC ? MC : a.m;
-  const size_t smem = (size_t)QT * m * 16 + (size_t)kWarps * QT * a.cap_l * 4;
+  const size_t smem = (size_t)QT * m * 16 + (size_t)kWarps * QT * a.cap_l * 4 + (size_t)QT * 512;
   cudaFuncSetAttribute(k_scan<MC, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan<MC, QT>, kWarps * 32, smem);
