@@ -198,7 +198,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
       hist.alloc((int64_t)nq * kHistWords, st) || hist_w.alloc(nq, st) || cand_n.alloc(nq, st) ||
       cand_mid.alloc((int64_t)nq * cap_g, st) || cand_id.alloc((int64_t)nq * cap_g, st) ||
       pair_q.alloc(npairs, st) || pair_t.alloc(npairs, st) || n_items.alloc(1, st) ||
-      counter.alloc(1, st) || scratch.alloc(6 * (int64_t)nl + 8, st) || overflow.alloc(nq, st) ||
+      counter.alloc(1, st) || scratch.alloc(build_work_scratch(nl, nslots), st) || overflow.alloc(nq, st) ||
       ncodes.alloc(1, st) || pair_depth.alloc(npairs, st))
     return cuda_fail(cudaGetLastError(), "alloc workspace");
   // tuning knobs (defaults are the measured best): byte-sum depth cap and
@@ -242,8 +242,8 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   if (items_ord.alloc(max_items, st) || cls.alloc(order_items_scratch(max_items), st))
     return cuda_fail(cudaGetLastError(), "alloc items");
   order_items(items.p, n_items.p, max_items, pair_t.p, pair_depth.p, no_half ? 0 : qt_tile / 2,
-              cls.p, items_ord.p, st);
-  ss.launches += 7;
+              nslots, cls.p, items_ord.p, st);
+  ss.launches += 8;
 
   // ---- scan ----
   cudaMemsetAsync(cand_n.p, 0, sizeof(unsigned) * nq, st);

@@ -131,7 +131,8 @@ constexpr int kHistWords = kHistBins + 32;      // fine bins, then coarse sums
 int scan_qt_per_cta(int m);
 int scan_env_int(const char *name, int dflt);
 void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st);
-// Work-list construction (device side): returns item upper bound.
+// Work-list construction (device side). scratch: build_work_scratch ints.
+int64_t build_work_scratch(int nlists, int nslots);
 int64_t build_work(const qadc_b200_index *idx, const int64_t *cells, int nq,
                    int nslots, int qt_tile, int64_t range_chunks,
                    int32_t *pair_q, int32_t *pair_t, WorkItem *items,
@@ -145,8 +146,8 @@ int64_t build_work(const qadc_b200_index *idx, const int64_t *cells, int nq,
 // class afterwards. qh: pair_count <= qh runs the half loop.
 int64_t order_items_scratch(int64_t max_items);
 void order_items(const WorkItem *items, const int *n_items, int64_t max_items,
-                 const int32_t *pair_t, const uint8_t *pair_depth, int qh, unsigned *scratch,
-                 WorkItem *out, cudaStream_t st);
+                 const int32_t *pair_t, const uint8_t *pair_depth, int qh, int nslots,
+                 unsigned *scratch, WorkItem *out, cudaStream_t st);
 
 // ---- select.cu ----
 int select_capacity();

@@ -175,36 +175,39 @@ __device__ __noinline__ void compact_buffer(const ScanArgs &a, Smem &s, uint32_t
   __syncwarp();
 }
 
-// Warp-wide count of the set bits of every lane's 4-bit mask: codes in
+// Warp-wide count of the set bits of every lane's K-bit mask: codes in
 // lanes below this one, and in the whole warp.
-__device__ __forceinline__ void count4(uint32_t m4, int &before, int &total) {
+template <int K>
+__device__ __forceinline__ void count_bits(uint32_t mk, int &before, int &total) {
   const unsigned lt = (1u << (threadIdx.x & 31)) - 1;
   before = 0;
   total = 0;
 #pragma unroll
-  for (int k = 0; k < 4; k++) {
-    const unsigned b = __ballot_sync(kFull, (m4 >> k) & 1u);
+  for (int k = 0; k < K; k++) {
+    const unsigned b = __ballot_sync(kFull, (mk >> k) & 1u);
     before += __popc(b & lt);
     total += __popc(b);
   }
 }
 
-// Append this lane's surviving codes (mask4 bit k = code base_idx + k of
-// the item; byte k of vals = its lane distance) to (warp, q)'s buffer.
+// Append this lane's surviving codes (mask bit k = code base_idx + k of
+// the item; byte k of v0:v1 = its lane distance) to (warp, q)'s buffer.
+// K = 8: the caller checked that the buffer has room; K = 4: at most 128
+// codes, the buffer keeps R + 128 slots (compact / flush when full).
+template <int K>
 __device__ __noinline__ void append(const ScanArgs &a, Smem &s, uint32_t *buf, int w, int q,
-                                    uint32_t mask4, uint32_t vals, uint32_t base_idx) {
+                                    uint32_t mask4, uint32_t vals, uint32_t vals_hi,
+                                    uint32_t base_idx, int before, int total) {
   const int lane = threadIdx.x & 31;
-  int before, total;
-  count4(mask4, before, total);
   int n = s.bn[w][q];
-  if (n + total > a.cap_l) {  // n > cap_l - 128 >= R
+  if (K == 4 && n + total > a.cap_l) {  // n > cap_l - 128 >= R
     if (n >= a.R) compact_buffer(a, s, buf, w, q);
     // re-filter with the (possibly) tightened threshold
     const int thr = s.thr[w][q];
 #pragma unroll
     for (int k = 0; k < 4; k++)
       if ((int)((vals >> (8 * k)) & 255u) > thr) mask4 &= ~(1u << k);
-    count4(mask4, before, total);
+    count_bits<4>(mask4, before, total);
     n = s.bn[w][q];
     if (n + total > a.cap_l) {
       flush_buffer(a, s, buf, w, q);
@@ -216,9 +219,9 @@ __device__ __noinline__ void append(const ScanArgs &a, Smem &s, uint32_t *buf, i
   const float hinv = s.hinv[q], qmin = s.qmin[q], delta = s.delta[q];
   unsigned *h = a.hist + (size_t)query * kHistWords;
 #pragma unroll
-  for (int k = 0; k < 4; k++) {
+  for (int k = 0; k < K; k++) {
     if (mask4 & (1u << k)) {
-      const uint32_t v = (vals >> (8 * k)) & 255u;
+      const uint32_t v = ((k < 4 ? vals : vals_hi) >> (8 * (k & 3))) & 255u;
       buf[off++] = (v << 24) | (base_idx + k);
       if (hinv > 0.f) {
         // bucket floor(mid / w) up to one bucket either way (hist_bound's
@@ -266,12 +269,18 @@ __device__ __noinline__ void candidates(const ScanArgs &a, Smem &s, uint32_t *bu
            << 4;
   mask8 &= valid8;
   const uint32_t v0 = prmt(E0, O0, 0x6240), v1 = prmt(E1, O1, 0x6240);  // low bytes
-  // at most 4 codes per lane per append: the buffer needs R + 128 slots
   const uint32_t base_idx = (uint32_t)chunk_local * kChunkCodes + 8u * (threadIdx.x & 31);
-  if (__any_sync(kFull, (mask8 & 0x0fu) != 0))
-    append(a, s, buf, w, q, mask8 & 0x0fu, v0, base_idx);
-  if (__any_sync(kFull, (mask8 & 0xf0u) != 0))
-    append(a, s, buf, w, q, mask8 >> 4, v1, base_idx + 4);
+  int before, total;
+  count_bits<8>(mask8, before, total);
+  if (s.bn[w][q] + total <= a.cap_l) {  // common case: all 8 codes per lane at once
+    if (total) append<8>(a, s, buf, w, q, mask8, v0, v1, base_idx, before, total);
+    return;
+  }
+  // at most 4 codes per lane per append: the buffer needs R + 128 slots
+  count_bits<4>(mask8 & 0x0fu, before, total);
+  if (total) append<4>(a, s, buf, w, q, mask8 & 0x0fu, v0, 0, base_idx, before, total);
+  count_bits<4>(mask8 >> 4, before, total);
+  if (total) append<4>(a, s, buf, w, q, mask8 >> 4, v1, 0, base_idx + 4, before, total);
 }
 
 // Refresh each query's threshold from the global bound (lanes in parallel).
@@ -584,9 +593,27 @@ void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
 
 // ---- work list construction ----
 
-__global__ void k_count_pairs(const int64_t *__restrict__ cells, int npairs, int *list_pairs) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x)
-    atomicAdd(&list_pairs[cells ? cells[i] : 0], 1);
+__global__ void k_count_pairs(const int64_t *__restrict__ cells, int npairs, int nslots,
+                              int *list_pairs, int *slot_cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
+    const int L = cells ? (int)cells[i] : 0;
+    atomicAdd(&list_pairs[L], 1);
+    atomicAdd(&slot_cnt[(size_t)L * nslots + i % nslots], 1);
+  }
+}
+
+// Per list: exclusive scan of its pair counts over probe slots, so a
+// list's pairs are laid out by probe rank (its tiles then group queries
+// for which this list is near the front of the probe order).
+__global__ void k_slot_offsets(int *slot_cnt, int nlists, int nslots) {
+  for (int L = blockIdx.x * blockDim.x + threadIdx.x; L < nlists; L += gridDim.x * blockDim.x) {
+    int o = 0;
+    for (int k = 0; k < nslots; k++) {
+      const int c = slot_cnt[(size_t)L * nslots + k];
+      slot_cnt[(size_t)L * nslots + k] = o;
+      o += c;
+    }
+  }
 }
 
 // Single CTA: exclusive scans of pairs and items over the lists.
@@ -637,11 +664,12 @@ __global__ void k_scan_lists(const int *__restrict__ list_pairs, const int64_t *
 }
 
 __global__ void k_scatter_pairs(const int64_t *__restrict__ cells, int npairs, int nslots,
-                                const int *__restrict__ pair_off, int *fill, int32_t *pair_q,
-                                int32_t *pair_t) {
+                                const int *__restrict__ pair_off, const int *__restrict__ slot_off,
+                                int *slot_fill, int32_t *pair_q, int32_t *pair_t) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
     const int L = cells ? (int)cells[i] : 0;
-    const int pos = pair_off[L] + atomicAdd(&fill[L], 1);
+    const size_t ls = (size_t)L * nslots + i % nslots;
+    const int pos = pair_off[L] + slot_off[ls] + atomicAdd(&slot_fill[ls], 1);
     pair_q[pos] = i / nslots;
     pair_t[pos] = i;
   }
@@ -673,83 +701,99 @@ __global__ void k_emit_items(const int *__restrict__ list_pairs, const int *__re
   }
 }
 
-// Stable partition of the items by loop variant (class), 256 items per
-// block: class + per-block class counts, a scan over blocks, then a scatter
-// that keeps the original order inside each class (list / tile / range
-// order is what keeps concurrently running CTAs on shared L2 lines).
+// Stable partition of the items into buckets (probe rank, loop variant),
+// 256 items per block: bucket + per-block bucket counts, a scan over
+// blocks, then a scatter that keeps the original order inside each bucket
+// (list / tile / range order keeps concurrently running CTAs on shared L2
+// lines). Rank-major order scans every query's nearest cells first, so its
+// bound has converged before the far cells; variant contiguity keeps one
+// loop body hot in the instruction cache.
+constexpr int kRankBuckets = 16;
+constexpr int kBuckets = kRankBuckets * 8;
+
 __global__ void k_item_class(WorkItem *__restrict__ items, const int *__restrict__ n_items,
                              const int32_t *__restrict__ pair_t,
-                             const uint8_t *__restrict__ pair_depth, int qh,
-                             unsigned *__restrict__ blk_cnt) {
-  __shared__ unsigned cnt[8];
-  if (threadIdx.x < 8) cnt[threadIdx.x] = 0;
+                             const uint8_t *__restrict__ pair_depth, int qh, int nslots,
+                             int rank_buckets, unsigned *__restrict__ blk_cnt) {
+  __shared__ unsigned cnt[kBuckets];
+  for (int k = threadIdx.x; k < kBuckets; k += blockDim.x) cnt[k] = 0;
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < *n_items) {
     const WorkItem it = items[i];
-    int d = 16;
-    for (int q = 0; q < it.pair_count; q++) d = min(d, (int)pair_depth[pair_t[it.pair_begin + q]]);
+    int d = 16, rank = nslots;
+    for (int q = 0; q < it.pair_count; q++) {
+      const int t = pair_t[it.pair_begin + q];
+      d = min(d, (int)pair_depth[t]);
+      rank = min(rank, t % nslots);
+    }
     const int half = it.pair_count <= qh ? 1 : 0;
     const int cls = half * 4 + (d >= 16 ? 0 : d >= 8 ? 1 : d >= 4 ? 2 : 3);
-    items[i].variant = d | (half << 8) | (cls << 16);
-    atomicAdd(&cnt[cls], 1u);
+    const int bucket = min(rank, rank_buckets - 1) * 8 + cls;
+    items[i].variant = d | (half << 8) | (bucket << 16);
+    atomicAdd(&cnt[bucket], 1u);
   }
   __syncthreads();
-  if (threadIdx.x < 8) blk_cnt[blockIdx.x * 8 + threadIdx.x] = cnt[threadIdx.x];
+  for (int k = threadIdx.x; k < kBuckets; k += blockDim.x)
+    blk_cnt[(size_t)blockIdx.x * kBuckets + k] = cnt[k];
 }
 
 __global__ void k_item_offsets(unsigned *__restrict__ blk_cnt, int nblk, unsigned *__restrict__ cls_n) {
-  __shared__ unsigned tot[8];
-  const int c = threadIdx.x;
-  if (c < 8) {
-    unsigned t = 0;
-    for (int b = 0; b < nblk; b++) t += blk_cnt[b * 8 + c];
-    tot[c] = t;
-    cls_n[c] = t;
-  }
+  __shared__ unsigned tot[kBuckets];
+  const int c = threadIdx.x;  // one thread per bucket
+  unsigned t = 0;
+  for (int b = 0; b < nblk; b++) t += blk_cnt[(size_t)b * kBuckets + c];
+  tot[c] = t;
   __syncthreads();
   if (c < 8) {
-    unsigned o = 0;
-    for (int k = 0; k < c; k++) o += tot[k];
-    for (int b = 0; b < nblk; b++) {
-      const unsigned v = blk_cnt[b * 8 + c];
-      blk_cnt[b * 8 + c] = o;
-      o += v;
-    }
+    unsigned v = 0;
+    for (int r = 0; r < kRankBuckets; r++) v += tot[r * 8 + c];
+    cls_n[c] = v;  // items per loop variant
+  }
+  unsigned o = 0;
+  for (int k = 0; k < c; k++) o += tot[k];
+  for (int b = 0; b < nblk; b++) {
+    const unsigned v = blk_cnt[(size_t)b * kBuckets + c];
+    blk_cnt[(size_t)b * kBuckets + c] = o;
+    o += v;
   }
 }
 
 __global__ void k_item_scatter(const WorkItem *__restrict__ in, const int *__restrict__ n_items,
                                const unsigned *__restrict__ blk_off, WorkItem *__restrict__ out) {
-  __shared__ unsigned char cls_of[256];
+  __shared__ unsigned char bucket_of[256];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool ok = i < *n_items;
   WorkItem it;
-  int cls = 8;
+  int bk = 255;
   if (ok) {
     it = in[i];
-    cls = (it.variant >> 16) & 7;
+    bk = (it.variant >> 16) & 255;
   }
-  cls_of[threadIdx.x] = (unsigned char)cls;
+  bucket_of[threadIdx.x] = (unsigned char)bk;
   __syncthreads();
   if (!ok) return;
   unsigned r = 0;
-  for (int k = 0; k < (int)threadIdx.x; k++) r += cls_of[k] == cls;
-  out[blk_off[blockIdx.x * 8 + cls] + r] = it;
+  for (int k = 0; k < (int)threadIdx.x; k++) r += bucket_of[k] == bk;
+  out[blk_off[(size_t)blockIdx.x * kBuckets + bk] + r] = it;
 }
 
 }  // namespace
 
-int64_t order_items_scratch(int64_t max_items) { return ((max_items + 255) / 256) * 8 + 16; }
+int64_t order_items_scratch(int64_t max_items) {
+  return ((max_items + 255) / 256) * kBuckets + 16;
+}
 
 void order_items(const WorkItem *items, const int *n_items, int64_t max_items,
-                 const int32_t *pair_t, const uint8_t *pair_depth, int qh, unsigned *scratch,
-                 WorkItem *out, cudaStream_t st) {
+                 const int32_t *pair_t, const uint8_t *pair_depth, int qh, int nslots,
+                 unsigned *scratch, WorkItem *out, cudaStream_t st) {
   const int nblk = (int)std::max<int64_t>((max_items + 255) / 256, 1);
   unsigned *cls_n = scratch, *blk = scratch + 16;
+  static const int rank_buckets =
+      std::min(kRankBuckets, std::max(1, scan_env_int("QADC_B200_RANK_BUCKETS", 2)));
   k_item_class<<<nblk, 256, 0, st>>>(const_cast<WorkItem *>(items), n_items, pair_t, pair_depth,
-                                     qh, blk);
-  k_item_offsets<<<1, 32, 0, st>>>(blk, nblk, cls_n);
+                                     qh, nslots, rank_buckets, blk);
+  k_item_offsets<<<1, kBuckets, 0, st>>>(blk, nblk, cls_n);
   k_item_scatter<<<nblk, 256, 0, st>>>(items, n_items, blk, out);
 }
 
@@ -786,6 +830,10 @@ void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st) {
   }
 }
 
+int64_t build_work_scratch(int nlists, int nslots) {
+  return 6 * (int64_t)nlists + 8 + 2 * (int64_t)nlists * nslots;
+}
+
 int64_t build_work(const qadc_b200_index *idx, const int64_t *cells, int nq, int nslots,
                    int qt_tile, int64_t range_chunks, int32_t *pair_q, int32_t *pair_t,
                    WorkItem *items, int *n_items, int *scratch, int64_t max_items,
@@ -793,15 +841,18 @@ int64_t build_work(const qadc_b200_index *idx, const int64_t *cells, int nq, int
   (void)max_items;
   const int nl = idx->nlists;
   const int npairs = nq * nslots;
-  int *list_pairs = scratch, *pair_off = scratch + nl, *fill = scratch + 2 * nl;
+  int *list_pairs = scratch, *pair_off = scratch + nl;
   int64_t *item_off = (int64_t *)(scratch + 4 * nl + 2);  // 8-byte aligned region
+  int *slot_off = scratch + 6 * nl + 8, *slot_fill = slot_off + (size_t)nl * nslots;
   cudaMemsetAsync(list_pairs, 0, sizeof(int) * nl, st);
-  cudaMemsetAsync(fill, 0, sizeof(int) * nl, st);
+  cudaMemsetAsync(slot_off, 0, sizeof(int) * 2 * (size_t)nl * nslots, st);
   const int g = std::min(std::max((npairs + 255) / 256, 1), 4096);
-  k_count_pairs<<<g, 256, 0, st>>>(cells, npairs, list_pairs);
+  k_count_pairs<<<g, 256, 0, st>>>(cells, npairs, nslots, list_pairs, slot_off);
+  k_slot_offsets<<<(nl + 255) / 256, 256, 0, st>>>(slot_off, nl, nslots);
   k_scan_lists<<<1, 1024, 0, st>>>(list_pairs, idx->chunk_off, nl, qt_tile, range_chunks, pair_off,
                                    item_off, n_items);
-  k_scatter_pairs<<<g, 256, 0, st>>>(cells, npairs, nslots, pair_off, fill, pair_q, pair_t);
+  k_scatter_pairs<<<g, 256, 0, st>>>(cells, npairs, nslots, pair_off, slot_off, slot_fill, pair_q,
+                                     pair_t);
   k_emit_items<<<(nl + 127) / 128, 128, 0, st>>>(list_pairs, pair_off, item_off, idx->chunk_off,
                                                  nl, qt_tile, range_chunks, items);
   return 0;
