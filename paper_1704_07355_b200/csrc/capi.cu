@@ -275,6 +275,9 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   a.R = R;
   static const int bound_every = std::max(1, scan_env_int("QADC_B200_BOUND_EVERY", 32));
   a.bound_every = bound_every;
+  // long items (>= 64 chunks per item on average) run the linear loop
+  static const int linear_env = scan_env_int("QADC_B200_LINEAR", -1);
+  a.linear = linear_env >= 0 ? linear_env : (avg_chunks >= 64 ? 1 : 0);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

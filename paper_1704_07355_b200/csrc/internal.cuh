@@ -124,6 +124,7 @@ struct ScanArgs {
   int m;
   int R;
   int bound_every;         // appended candidates between global-histogram bound reads
+  int linear;              // 1: linear fixed-m loop (long items), 0: interleaved loop
 };
 
 constexpr int kHistBins = 1024;                 // 32 coarse x 32 fine

@@ -81,7 +81,12 @@ __global__ void k_chunk_list(const int64_t *__restrict__ chunk_off, int nlists,
 
 int common_alloc(qadc_b200_index *idx, cudaStream_t st) {
   const int64_t tc = idx->total_chunks;
-  QADC_CUDA(cudaMalloc(&idx->codes, (size_t)std::max<int64_t>(tc, 1) * idx->m * 32 * 4));
+  // one chunk of zeroed padding: the scan's linear prefetch reads up to 12
+  // rows past the last chunk it scans
+  const size_t chunk_bytes = (size_t)idx->m * 32 * 4;
+  QADC_CUDA(cudaMalloc(&idx->codes, (size_t)(std::max<int64_t>(tc, 1) + 1) * chunk_bytes));
+  QADC_CUDA(cudaMemsetAsync((char *)idx->codes + (size_t)std::max<int64_t>(tc, 1) * chunk_bytes, 0,
+                            chunk_bytes, st));
   QADC_CUDA(cudaMalloc(&idx->valid, (size_t)std::max<int64_t>(tc, 1) * 32));
   QADC_CUDA(cudaMalloc(&idx->ids, (size_t)std::max<int64_t>(tc, 1) * kChunkCodes * 8));
   QADC_CUDA(cudaMalloc(&idx->chunk_list, (size_t)std::max<int64_t>(tc, 1) * 4));

@@ -441,7 +441,86 @@ __device__ __forceinline__ void chunk_loop(const ScanArgs &a, Smem &s, const Wor
   }
 }
 
-template <int MC, int QT>
+// Fixed-m chunk loop (MC % 8 == 0, byte-sum depth D >= 8): each warp takes
+// a CONTIGUOUS run of the item's chunks, so its code words form one linear
+// stream of 32-word rows. The body covers 8 sub-quantizers with two
+// register sets in ping-pong (A: rows r..r+3, B: rows r+4..r+7), each
+// loaded half a body before use; no register moves, no per-row address
+// selection, one pointer increment per 8 rows. The prefetch runs up to 12
+// rows past the warp's last chunk (the code array keeps one chunk of
+// padding).
+template <int D, int MC, int QT>
+__device__ __forceinline__ void chunk_loop_lin(const ScanArgs &a, Smem &s, const WorkItem &it,
+                                               uint32_t *wbuf, uint32_t tab_sa, uint32_t one,
+                                               int nq_tile) {
+  static_assert(MC % 8 == 0 && D >= 8 && MC % D == 0, "linear loop shape");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t n = it.chunk_end - it.chunk_begin;
+  const int64_t per = (n + kWarps - 1) / kWarps;
+  const int64_t g0 = it.chunk_begin + min(n, w * per);
+  const int64_t g1 = it.chunk_begin + min(n, (w + 1) * per);
+  if (g0 >= g1) return;
+  const uint32_t *p = a.codes + (size_t)g0 * MC * 32 + lane;
+  uint32_t A[4] = {__ldg(p), __ldg(p + 32), __ldg(p + 64), __ldg(p + 96)};
+  uint32_t B[4];
+  int iter = 0;
+  for (int64_t g = g0; g < g1; g++, iter++) {
+    if ((iter & 3) == 3) refresh(a, s, w, nq_tile);
+    const uint32_t valid8 = a.valid[g * 32 + lane];
+    uint32_t acc_a[QT][2], acc_o[QT][2], sacc[QT][2];
+#pragma unroll
+    for (int q = 0; q < QT; q++)
+      acc_a[q][0] = acc_a[q][1] = acc_o[q][0] = acc_o[q][1] = sacc[q][0] = sacc[q][1] = 0;
+#pragma unroll 1
+    for (int j = 0; j < MC; j += 8) {
+#pragma unroll
+      for (int r = 0; r < 4; r++) B[r] = __ldg(p + 128 + 32 * r);
+      pair_lookups<QT>(A[0], A[1], j, MC, tab_sa, one, sacc);
+      pair_lookups<QT>(A[2], A[3], j + 2, MC, tab_sa, one, sacc);
+#pragma unroll
+      for (int r = 0; r < 4; r++) A[r] = __ldg(p + 256 + 32 * r);
+      pair_lookups<QT>(B[0], B[1], j + 4, MC, tab_sa, one, sacc);
+      pair_lookups<QT>(B[2], B[3], j + 6, MC, tab_sa, one, sacc);
+      p += 256;
+      if ((j + 8) % D == 0) widen<QT>(one, sacc, acc_a, acc_o);
+    }
+    // ---- threshold test: 16-bit lanes, bit 15 clear <=> lane <= thr ----
+    uint32_t hitq = 0;
+#pragma unroll
+    for (int q = 0; q < QT; q++) {
+      const unsigned kb = s.kbias[w][q];
+      const uint32_t O0 = acc_o[q][0], E0 = acc_a[q][0] - (O0 << 8);
+      const uint32_t O1 = acc_o[q][1], E1 = acc_a[q][1] - (O1 << 8);
+      const uint32_t all = (E0 + kb) & (O0 + kb) & (E1 + kb) & (O1 + kb);
+      hitq |= ((all & 0x80008000u) != 0x80008000u) ? (1u << q) : 0u;
+    }
+    hitq = __reduce_or_sync(kFull, hitq);
+    if (hitq) {
+      const int chunk_local = (int)(g - it.chunk_begin);
+#pragma unroll
+      for (int q = 0; q < QT; q++) {
+        if (hitq & (1u << q)) {
+          const uint32_t O0 = acc_o[q][0], E0 = acc_a[q][0] - (O0 << 8);
+          const uint32_t O1 = acc_o[q][1], E1 = acc_a[q][1] - (O1 << 8);
+          candidates(a, s, wbuf + q * a.cap_l, w, q, E0, O0, E1, O1, valid8, chunk_local);
+        }
+      }
+    }
+  }
+}
+
+// Loop variant of one tile: the linear fixed-m loop where it applies.
+template <int D, int MC, int QT, bool LIN>
+__device__ __forceinline__ void run_chunks(const ScanArgs &a, Smem &s, const WorkItem &it,
+                                           uint32_t *wbuf, int m, uint32_t tab_sa, uint32_t one,
+                                           int nq_tile) {
+  if constexpr (LIN && MC > 0 && MC % 8 == 0 && D >= 8)
+    chunk_loop_lin<D, MC, QT>(a, s, it, wbuf, tab_sa, one, nq_tile);
+  else
+    chunk_loop<D, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile);
+}
+
+template <int MC, int QT, bool LIN>
 __global__ void __launch_bounds__(kWarps * 32, QT >= 16 ? 3 : (QT >= 8 ? 5 : 6))
 k_scan(const __grid_constant__ ScanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -512,17 +591,17 @@ k_scan(const __grid_constant__ ScanArgs a) {
     const bool half = QH < QT && ((it.variant >> 8) & 1);
     if (half) {
       switch (depth) {
-        case 16: chunk_loop<16, MC, QH>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
-        case 8: chunk_loop<8, MC, QH>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
-        case 4: chunk_loop<4, MC, QH>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
-        default: chunk_loop<2, MC, QH>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        case 16: run_chunks<16, MC, QH, LIN>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        case 8: run_chunks<8, MC, QH, LIN>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        case 4: run_chunks<4, MC, QH, LIN>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        default: run_chunks<2, MC, QH, LIN>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
       }
     } else {
       switch (depth) {
-        case 16: chunk_loop<16, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
-        case 8: chunk_loop<8, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
-        case 4: chunk_loop<4, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
-        default: chunk_loop<2, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        case 16: run_chunks<16, MC, QT, LIN>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        case 8: run_chunks<8, MC, QT, LIN>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        case 4: run_chunks<4, MC, QT, LIN>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
+        default: run_chunks<2, MC, QT, LIN>(a, s, it, wbuf, m, tab_sa, one, nq_tile); break;
       }
     }
     // ---- end of item: CTA-level bound per query (the R-th smallest value
@@ -580,15 +659,24 @@ k_scan(const __grid_constant__ ScanArgs a) {
   }
 }
 
-template <int MC, int QT>
+template <int MC, int QT, bool LIN>
 void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
   const int m = MC ? MC : a.m;
   const size_t smem = (size_t)QT * m * 16 + (size_t)kWarps * QT * a.cap_l * 4 + (size_t)QT * 512;
-  cudaFuncSetAttribute(k_scan<MC, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_scan<MC, QT, LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan<MC, QT>, kWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan<MC, QT, LIN>, kWarps * 32, smem);
   per_sm = std::max(per_sm, 1);
-  k_scan<MC, QT><<<nsm * per_sm, kWarps * 32, smem, st>>>(a);
+  k_scan<MC, QT, LIN><<<nsm * per_sm, kWarps * 32, smem, st>>>(a);
+}
+
+// Long items (exhaustive lists) run the linear fixed-m loop for depths
+// >= 8; short items (inverted lists) keep the interleaved loop, which
+// measured faster there.
+template <int MC, int QT>
+void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
+  if (MC > 0 && a.linear) launch_t<MC, QT, true>(a, nsm, st);
+  else launch_t<MC, QT, false>(a, nsm, st);
 }
 
 // ---- work list construction ----
