@@ -10,12 +10,14 @@ entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_char_p, c_float, c_int, c_int64, c_uint, c_void_p
 from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libqadc_b200.so"
+LIB_PATH = Path(os.environ.get("QADC_B200_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "libqadc_b200.so")
 
 QADC_KERNEL_B200 = 3
 MAX_M = 128

@@ -741,7 +741,12 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
     on = dn.p;
   }
   SearchStats ss;
-  const int cap_g = (int)std::min<int64_t>(std::max<int64_t>(8192, 8LL * R), 1 << 20);
+  // per-query candidate capacity: at least 8192 / 8R, and up to 64K while
+  // the lists stay within ~512 MB (small batches with heavy ties at the
+  // boundary level then never need the rerun pass)
+  const int64_t cap_mem = (512LL << 20) / 12 / std::max(nq, 1);
+  const int cap_g = (int)std::min<int64_t>(
+      std::max<int64_t>({8192, 8LL * R, std::min<int64_t>(65536, cap_mem)}), 1 << 20);
   int rc = search_impl(idx, q, nq, R, ma, init, lin, cin, oi, od, on, st, ss, nullptr, cap_g, 0,
                        (flags & QADC_B200_NO_FSAT) != 0);
   if (rc) return rc;

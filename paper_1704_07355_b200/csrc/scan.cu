@@ -763,28 +763,28 @@ __global__ void k_scatter_pairs(const int64_t *__restrict__ cells, int npairs, i
   }
 }
 
+// One CTA per list, threads over the list's (range, tile) items.
 __global__ void k_emit_items(const int *__restrict__ list_pairs, const int *__restrict__ pair_off,
                              const int64_t *__restrict__ item_off, const int64_t *__restrict__ chunk_off,
                              int nlists, int qt_tile, int64_t range_chunks, WorkItem *items) {
-  for (int L = blockIdx.x * blockDim.x + threadIdx.x; L < nlists; L += gridDim.x * blockDim.x) {
+  for (int L = blockIdx.x; L < nlists; L += gridDim.x) {
     const int p = list_pairs[L];
     if (p == 0) continue;
     const int64_t c0 = chunk_off[L], nch = chunk_off[L + 1] - c0;
     if (nch == 0) continue;
     const int tiles = (p + qt_tile - 1) / qt_tile;
     const int64_t ranges = (nch + range_chunks - 1) / range_chunks;
-    int64_t o = item_off[L];
-    for (int64_t r = 0; r < ranges; r++) {
-      for (int t = 0; t < tiles; t++) {
-        WorkItem wi;
-        wi.list = L;
-        wi.pair_begin = pair_off[L] + t * qt_tile;
-        wi.pair_count = min(qt_tile, p - t * qt_tile);
-        wi.variant = 0;
-        wi.chunk_begin = c0 + r * range_chunks;
-        wi.chunk_end = min(c0 + nch, wi.chunk_begin + range_chunks);
-        items[o++] = wi;
-      }
+    for (int64_t k = threadIdx.x; k < ranges * tiles; k += blockDim.x) {
+      const int64_t r = k / tiles;
+      const int t = (int)(k - r * tiles);
+      WorkItem wi;
+      wi.list = L;
+      wi.pair_begin = pair_off[L] + t * qt_tile;
+      wi.pair_count = min(qt_tile, p - t * qt_tile);
+      wi.variant = 0;
+      wi.chunk_begin = c0 + r * range_chunks;
+      wi.chunk_end = min(c0 + nch, wi.chunk_begin + range_chunks);
+      items[item_off[L] + k] = wi;
     }
   }
 }
@@ -941,7 +941,7 @@ int64_t build_work(const qadc_b200_index *idx, const int64_t *cells, int nq, int
                                    item_off, n_items);
   k_scatter_pairs<<<g, 256, 0, st>>>(cells, npairs, nslots, pair_off, slot_off, slot_fill, pair_q,
                                      pair_t);
-  k_emit_items<<<(nl + 127) / 128, 128, 0, st>>>(list_pairs, pair_off, item_off, idx->chunk_off,
+  k_emit_items<<<std::min(nl, 65535), 128, 0, st>>>(list_pairs, pair_off, item_off, idx->chunk_off,
                                                  nl, qt_tile, range_chunks, items);
   return 0;
 }

@@ -270,26 +270,31 @@ def test_edge_cases_vs_oracle(gpu):
             assert np.array_equal(res.counts, on), (n, R)
 
 
-def test_massive_ties_vs_oracle(gpu):
-    """Identical codes everywhere: every lane ties; the exact (distance, id)
-    order must still pick the lowest ids (overflow / large-select paths)."""
+@pytest.mark.parametrize("n", [60_000, 200_000])
+def test_massive_ties_vs_oracle(gpu, n):
+    """Three code patterns only (about n, n/7 and n/40 copies): every lane
+    ties with thousands of others; the exact (distance, id) order must
+    still pick the lowest ids. Covers the select kernel's radix path (ties
+    sorted in shared memory, and the id-radix passes beyond that) and, at
+    n = 200000, the candidate-capacity rerun."""
     import torch
 
     from paper_1704_07355_b200.device import DeviceIndex
     from paper_1704_07355_b200.qadc import transpose_list
-    n, m, d = 60_000, 16, 64
+    m, d = 16, 64
     rng = np.random.default_rng(5)
     cb = (rng.random((m, 16, d // m)) * 10).astype(np.float32)
     codes = np.full((n, m // 2), 0x21, np.uint8)
     codes[::7] = 0x43
+    codes[::40] = 0x65
     idx = DeviceIndex.from_device_rows(d, m, torch.from_numpy(codes).cuda(),
                                        torch.tensor([0, n], device="cuda"),
                                        torch.from_numpy(cb).cuda())
     tl = transpose_list(codes, np.arange(n, dtype=np.int64))
     flat = (tl.blocks.reshape(-1), np.array([0, tl.blocks.shape[0]], np.int64), tl.ids,
             np.array([n], np.int64))
-    qs = (rng.random((4, d)) * 10).astype(np.float32)
-    for R in (10, 100):
+    qs = (rng.random((6, d)) * 10).astype(np.float32)
+    for R in (10, 100, 1500):
         res = idx.search(qs, R, init=1000)
         oi, od, on, _ = orc.search_batch(qs, cb, None, None, 1, flat, R, 1000)
         assert np.array_equal(res.ids, oi)
