@@ -556,6 +556,9 @@ int index_common(int d, int m, int nlists, const float *coarse, bool coarse_dev,
   if (rotation) {
     QADC_CUDA(cudaMalloc(&idx->rotation, (size_t)d * d * 4));
     QADC_CUDA(cudaMemcpy(idx->rotation, rotation, (size_t)d * d * 4, mk));
+    QADC_CUDA(cudaMalloc(&idx->rotationT, (size_t)d * d * 4));
+    k_transpose<<<gridn((int64_t)d * d), 256>>>(idx->rotation, d, d, idx->rotationT);
+    QADC_CUDA(cudaGetLastError());
   }
   QADC_CUDA(cudaMalloc(&idx->chunk_off, (nlists + 1) * 8));
   QADC_CUDA(cudaMalloc(&idx->lanes, nlists * 8));
@@ -574,7 +577,7 @@ extern "C" void qadc_b200_index_destroy(qadc_b200_index *idx) {
   if (idx->own_prefix) {
     cudaFree(idx->pcodes); cudaFree(idx->pids); cudaFree(idx->pchunk_off); cudaFree(idx->planes);
   }
-  cudaFree(idx->coarse); cudaFree(idx->coarseT); cudaFree(idx->cnorm); cudaFree(idx->codebooks); cudaFree(idx->rotation);
+  cudaFree(idx->coarse); cudaFree(idx->coarseT); cudaFree(idx->cnorm); cudaFree(idx->codebooks); cudaFree(idx->rotation); cudaFree(idx->rotationT);
   cudaFree(idx->codes); cudaFree(idx->valid); cudaFree(idx->ids); cudaFree(idx->chunk_list);
   cudaFree(idx->chunk_off); cudaFree(idx->lanes); cudaFree(idx->count); cudaFree(idx->scan_count);
   delete idx;

@@ -26,6 +26,7 @@ struct qadc_b200_index {
   float *cnorm = nullptr;      // [K] |c|^2 (probe pre-selection bounds)
   float *codebooks = nullptr;  // [m][16][dsub]
   float *rotation = nullptr;   // [d][d] or null
+  float *rotationT = nullptr;  // [d][d] R^T (coalesced float4 rows for the residual rotation)
   uint32_t *codes = nullptr;   // [total_chunks][m][32]
   uint8_t *valid = nullptr;    // [total_chunks][32]
   int64_t *ids = nullptr;      // [total_chunks * 256], -1 padding

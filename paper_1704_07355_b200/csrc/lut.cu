@@ -469,12 +469,11 @@ constexpr int kLutPairs = 16;  // (query, slot) pairs per CTA
 // one pair from one broadcast r[k].
 __global__ void __launch_bounds__(256) k_residual_lut(
     const float *__restrict__ queries, const float *__restrict__ coarse,
-    const float *__restrict__ rotation, const float *__restrict__ codebooks,
-    const int64_t *__restrict__ cells, int d, int m, int nslots, int npairs, int rot_in_smem,
-    float *__restrict__ lut) {
+    const float *__restrict__ rotation, const float *__restrict__ rotT,
+    const float *__restrict__ codebooks, const int64_t *__restrict__ cells, int d, int m,
+    int nslots, int npairs, float *__restrict__ lut) {
   extern __shared__ __align__(16) float smf[];
-  float *rt = smf;                                              // [d][d] R^T (if staged)
-  float *sr = smf + (rot_in_smem ? (size_t)d * d : 0);          // [kLutPairs][d]
+  float *sr = smf;                                              // [kLutPairs][d]
   float *sy = sr + (size_t)kLutPairs * d;                       // [kLutPairs][d]
   const int p0 = blockIdx.x * kLutPairs;
   const int np = min(kLutPairs, npairs - p0);
@@ -484,17 +483,13 @@ __global__ void __launch_bounds__(256) k_residual_lut(
     const float qv = queries[(size_t)(pair / nslots) * d + t];
     sr[e] = coarse ? __fsub_rn(qv, coarse[(size_t)cells[pair] * d + t]) : qv;
   }
-  if (rotation && rot_in_smem)
-    for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
-      const int i = e / d, k = e - i * d;
-      rt[(size_t)k * d + i] = rotation[e];
-    }
   __syncthreads();
   const float *y = sr;
   if (rotation) {
-    if (rot_in_smem && (d & 3) == 0 && np == kLutPairs) {
+    if ((d & 3) == 0 && np == kLutPairs) {
       // thread tile: 4 consecutive outputs x 4 pairs (16 accumulators), each
-      // k step = one float4 of R^T and four broadcast residual values
+      // k step = one float4 row segment of R^T (L1-resident, coalesced
+      // across the warp) and four broadcast residual values
       const int quads = d >> 2;
       for (int task = threadIdx.x; task < (kLutPairs / 4) * quads; task += blockDim.x) {
         const int pg = task / quads, i0 = (task - pg * quads) * 4;
@@ -502,8 +497,9 @@ __global__ void __launch_bounds__(256) k_residual_lut(
         float a[4][4];
 #pragma unroll
         for (int u = 0; u < 4; u++) a[u][0] = a[u][1] = a[u][2] = a[u][3] = 0.f;
+#pragma unroll 4
         for (int k = 0; k < d; k++) {
-          const float4 c = *(const float4 *)(rt + (size_t)k * d + i0);
+          const float4 c = __ldg((const float4 *)(rotT + (size_t)k * d + i0));
 #pragma unroll
           for (int u = 0; u < 4; u++) {
             const float rv = r0[(size_t)u * d + k];
@@ -517,28 +513,12 @@ __global__ void __launch_bounds__(256) k_residual_lut(
         for (int u = 0; u < 4; u++)
           *(float4 *)(sy + (size_t)(pg * 4 + u) * d + i0) = make_float4(a[u][0], a[u][1], a[u][2], a[u][3]);
       }
-    } else if (rot_in_smem && (d & 3) == 0) {
-      const int quads = d >> 2;
-      for (int task = threadIdx.x; task < np * quads; task += blockDim.x) {
-        const int p = task / quads, i0 = (task - p * quads) * 4;
-        const float *r = sr + (size_t)p * d;
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-        for (int k = 0; k < d; k++) {
-          const float rv = r[k];
-          const float4 c = *(const float4 *)(rt + (size_t)k * d + i0);
-          a0 = __fmaf_rn(c.x, rv, a0);
-          a1 = __fmaf_rn(c.y, rv, a1);
-          a2 = __fmaf_rn(c.z, rv, a2);
-          a3 = __fmaf_rn(c.w, rv, a3);
-        }
-        *(float4 *)(sy + (size_t)p * d + i0) = make_float4(a0, a1, a2, a3);
-      }
     } else {
       for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
         const int p = e / d, i = e - p * d;
         const float *r = sr + (size_t)p * d;
         float acc = 0.f;
-        for (int k = 0; k < d; k++) acc = __fmaf_rn(rotation[(size_t)i * d + k], r[k], acc);
+        for (int k = 0; k < d; k++) acc = __fmaf_rn(rotT[(size_t)k * d + i], r[k], acc);
         sy[e] = acc;
       }
     }
@@ -873,15 +853,11 @@ void launch_residual_lut(const qadc_b200_index *idx, const float *queries, const
                          int nq, int nslots, float *lut, cudaStream_t st) {
   if (nq <= 0) return;
   const int npairs = nq * nslots, d = idx->d;
-  const bool rot = idx->rotation != nullptr;
-  const int rot_smem = rot && (size_t)d * d * 4 <= 64 * 1024;
-  const size_t per_pair = (size_t)d * 8;  // residual + rotated, fp32
-  const size_t fixed = rot_smem ? (size_t)d * d * 4 : 0;
-  const size_t smem = fixed + kLutPairs * per_pair;
+  const size_t smem = (size_t)kLutPairs * d * 8;  // residual + rotated, fp32
   cudaFuncSetAttribute(k_residual_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_residual_lut<<<(npairs + kLutPairs - 1) / kLutPairs, 256, smem, st>>>(
-      queries, idx->K ? idx->coarse : nullptr, idx->rotation, idx->codebooks, cells, d, idx->m,
-      nslots, npairs, rot_smem, lut);
+      queries, idx->K ? idx->coarse : nullptr, idx->rotation, idx->rotationT, idx->codebooks,
+      cells, d, idx->m, nslots, npairs, lut);
 }
 
 void launch_qmax(const qadc_b200_index *idx, const float *lut, const int64_t *cells, int nq,
