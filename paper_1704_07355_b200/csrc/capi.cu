@@ -229,6 +229,30 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   int64_t rcp = 16;
   while (rcp < range_chunks && rcp < 16384) rcp <<= 1;
   range_chunks = rcp;
+  const int cap_l = (std::max(R + 128, 256) + 31) / 32 * 32;
+  const int linear = scan_env_int("QADC_B200_LINEAR", -1) >= 0 ? scan_env_int("QADC_B200_LINEAR", 0)
+                                                                 : (avg_chunks >= 64 ? 1 : 0);
+  if (nl == 1 && idx->total_chunks > 0) {
+    // one exhaustive list: equal-size items, so the persistent CTAs finish
+    // together only if the item count fills whole waves. Pick the range
+    // count r minimising waves x (chunks per item + per-item overhead).
+    const int64_t tiles = (npairs + qt_tile - 1) / qt_tile;
+    const int64_t ctas = scan_resident_ctas(m, cap_l, nsm, linear);
+    const int64_t ch = idx->total_chunks;
+    int64_t best_r = 1;
+    double best = 1e300;
+    for (int64_t r = 1; r <= std::min<int64_t>(ch, 4096); r++) {
+      const int64_t per = (ch + r - 1) / r;
+      if (per < 16 && r > 1) break;
+      const int64_t waves = (tiles * r + ctas - 1) / ctas;
+      const double cost = (double)waves * (double)(per + 4);
+      if (cost < best * 0.999) {
+        best = cost;
+        best_r = r;
+      }
+    }
+    range_chunks = (ch + best_r - 1) / best_r;
+  }
   for (int L = 0; L < nl; L++) {
     const int64_t nch = idx->h_chunk_off[L + 1] - idx->h_chunk_off[L];
     const int64_t r = (nch + range_chunks - 1) / range_chunks;
@@ -270,14 +294,12 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   a.hist = hist.p;
   a.hist_w = hist_w.p;
   a.cap_g = cap_g;
-  a.cap_l = (std::max(R + 128, 256) + 31) / 32 * 32;
+  a.cap_l = cap_l;
   a.m = m;
   a.R = R;
   static const int bound_every = std::max(1, scan_env_int("QADC_B200_BOUND_EVERY", 32));
   a.bound_every = bound_every;
-  // long items (>= 64 chunks per item on average) run the linear loop
-  static const int linear_env = scan_env_int("QADC_B200_LINEAR", -1);
-  a.linear = linear_env >= 0 ? linear_env : (avg_chunks >= 64 ? 1 : 0);
+  a.linear = linear;  // long items (>= 64 chunks per list on average)
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

@@ -131,6 +131,8 @@ struct ScanArgs {
 constexpr int kHistBins = 1024;                 // 32 coarse x 32 fine
 constexpr int kHistWords = kHistBins + 32;      // fine bins, then coarse sums
 int scan_qt_per_cta(int m);
+// Resident scan CTAs on the device (occupancy x SMs) for this shape.
+int scan_resident_ctas(int m, int cap_l, int nsm, int linear);
 int scan_env_int(const char *name, int dflt);
 void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st);
 // Work-list construction (device side). scratch: build_work_scratch ints.

@@ -670,6 +670,16 @@ void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
   k_scan<MC, QT, LIN><<<nsm * per_sm, kWarps * 32, smem, st>>>(a);
 }
 
+template <int MC, int QT, bool LIN>
+int resident_t(int m_rt, int cap_l, int nsm) {
+  const int m = MC ? MC : m_rt;
+  const size_t smem = (size_t)QT * m * 16 + (size_t)kWarps * QT * cap_l * 4 + (size_t)QT * 512;
+  cudaFuncSetAttribute(k_scan<MC, QT, LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan<MC, QT, LIN>, kWarps * 32, smem);
+  return nsm * std::max(per_sm, 1);
+}
+
 // Long items (exhaustive lists) run the linear fixed-m loop for depths
 // >= 8; short items (inverted lists) keep the interleaved loop, which
 // measured faster there.
@@ -916,6 +926,23 @@ void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st) {
     else if (a.m == 32) launch_t<32, 4>(a, nsm, st);
     else launch_t<0, 4>(a, nsm, st);
   }
+}
+
+int scan_resident_ctas(int m, int cap_l, int nsm, int linear) {
+  const int qt = scan_qt_per_cta(m);
+  const bool lin = linear != 0;
+  if (qt == 16) {
+    if (m == 32) return lin ? resident_t<32, 16, true>(m, cap_l, nsm) : resident_t<32, 16, false>(m, cap_l, nsm);
+    return resident_t<0, 16, false>(m, cap_l, nsm);
+  }
+  if (qt == 8) {
+    if (m == 16) return lin ? resident_t<16, 8, true>(m, cap_l, nsm) : resident_t<16, 8, false>(m, cap_l, nsm);
+    if (m == 32) return lin ? resident_t<32, 8, true>(m, cap_l, nsm) : resident_t<32, 8, false>(m, cap_l, nsm);
+    return resident_t<0, 8, false>(m, cap_l, nsm);
+  }
+  if (m == 16) return lin ? resident_t<16, 4, true>(m, cap_l, nsm) : resident_t<16, 4, false>(m, cap_l, nsm);
+  if (m == 32) return lin ? resident_t<32, 4, true>(m, cap_l, nsm) : resident_t<32, 4, false>(m, cap_l, nsm);
+  return resident_t<0, 4, false>(m, cap_l, nsm);
 }
 
 int64_t build_work_scratch(int nlists, int nslots) {
