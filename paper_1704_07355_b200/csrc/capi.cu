@@ -245,12 +245,16 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
       const int64_t per = (ch + r - 1) / r;
       if (per < 16 && r > 1) break;
       const int64_t waves = (tiles * r + ctas - 1) / ctas;
-      const double cost = (double)waves * (double)(per + 4);
+      // per-item overhead ~20 chunk-times (measured: prologue, end-of-item
+      // barrier and flush)
+      const double cost = (double)waves * (double)(per + 20);
       if (cost < best * 0.999) {
         best = cost;
         best_r = r;
       }
     }
+    static const int r_env = scan_env_int("QADC_B200_RANGES", 0);
+    if (r_env > 0) best_r = std::min<int64_t>(r_env, ch);
     range_chunks = (ch + best_r - 1) / best_r;
   }
   for (int L = 0; L < nl; L++) {

@@ -133,6 +133,65 @@ __device__ __noinline__ void flush_buffer(const ScanArgs &a, Smem &s, uint32_t *
   __syncwarp();
 }
 
+// End-of-item flush of all of this warp's buffers (one per tile query):
+// the queries' bounds are read in parallel (lane q), the survivors are
+// counted per query, ONE atomicAdd per query claims their slots (lanes in
+// parallel), then the entries are written. Two global round trips per
+// item instead of two per query.
+__device__ __noinline__ void flush_all(const ScanArgs &a, Smem &s, uint32_t *wbuf, int w,
+                                       int nq_tile) {
+  const int lane = threadIdx.x & 31;
+  float Ml = 0.f;
+  if (lane < nq_tile) Ml = __uint_as_float(*(volatile unsigned *)&a.M_bits[s.query[lane]]);
+  unsigned mycnt = 0;
+  for (int q = 0; q < nq_tile; q++) {
+    const int n = s.bn[w][q];
+    if (n == 0) continue;
+    const uint32_t *buf = wbuf + q * a.cap_l;
+    const float Mg = __shfl_sync(kFull, Ml, q);
+    const float qmin = s.qmin[q], delta = s.delta[q];
+    unsigned c = 0;
+    for (int i = lane; i < n; i += 32) c += midpoint(qmin, delta, (int)(buf[i] >> 24)) <= Mg;
+    c = __reduce_add_sync(kFull, c);
+    if (lane == q) mycnt = c;
+  }
+  unsigned pos = 0;
+  if (lane < nq_tile && mycnt) pos = atomicAdd(&a.cand_n[s.query[lane]], mycnt);
+  for (int q = 0; q < nq_tile; q++) {
+    const int n = s.bn[w][q];
+    if (n == 0) continue;
+    const uint32_t *buf = wbuf + q * a.cap_l;
+    const float Mg = __shfl_sync(kFull, Ml, q);
+    unsigned base = __shfl_sync(kFull, pos, q);
+    const int query = s.query[q];
+    const float qmin = s.qmin[q], delta = s.delta[q];
+    for (int b0 = 0; b0 < n; b0 += 32) {
+      const int i = b0 + lane;
+      bool keep = false;
+      float mid = 0.f;
+      uint32_t e = 0;
+      if (i < n) {
+        e = buf[i];
+        mid = midpoint(qmin, delta, (int)(e >> 24));
+        keep = mid <= Mg;
+      }
+      const unsigned bal = __ballot_sync(kFull, keep);
+      if (keep) {
+        const unsigned slot = base + __popc(bal & ((1u << lane) - 1));
+        if (slot < (unsigned)a.cap_g) {
+          const size_t o = (size_t)query * a.cap_g + slot;
+          a.cand_mid[o] = mid;
+          a.cand_id[o] = a.ids[s.chunk_begin * kChunkCodes + (e & 0xffffffu)];
+        }
+      }
+      base += __popc(bal);
+    }
+  }
+  __syncwarp();
+  if (lane < nq_tile) s.bn[w][lane] = 0;
+  __syncwarp();
+}
+
 // Tighten (warp, q)'s threshold to the R-th smallest buffered value and
 // drop entries above it. Requires bn >= R.
 __device__ __noinline__ void compact_buffer(const ScanArgs &a, Smem &s, uint32_t *buf, int w, int q) {
@@ -533,8 +592,8 @@ k_scan(const __grid_constant__ ScanArgs a) {
   const uint32_t tab_sa = (uint32_t)__cvta_generic_to_shared(s_tab);
   const uint32_t one = (uint32_t)(a.R > 0);  // runtime 1 (keeps IMAD on the FMA pipe)
   const int n_items = *a.n_items;
+  if (threadIdx.x == 0) s.item = atomicAdd(a.item_counter, 1);
   for (;;) {
-    if (threadIdx.x == 0) s.item = atomicAdd(a.item_counter, 1);
     __syncthreads();
     const int item = s.item;
     if (item >= n_items) break;
@@ -582,6 +641,8 @@ k_scan(const __grid_constant__ ScanArgs a) {
       s.chunk_begin = it.chunk_begin;
     }
     __syncthreads();
+    // claim the next item now: the atomic's latency hides behind this item
+    if (threadIdx.x == 0) s.item = atomicAdd(a.item_counter, 1);
     const int nq_tile = s.pair_count;
     const int depth = it.variant & 255;  // order_items: min pair depth of the tile
     // ---- warp loop over chunks (one specialization per byte-sum depth) ----
@@ -654,7 +715,7 @@ k_scan(const __grid_constant__ ScanArgs a) {
         }
       }
     }
-    for (int q = 0; q < nq_tile; q++) flush_buffer(a, s, wbuf + q * a.cap_l, w, q);
+    flush_all(a, s, wbuf, w, nq_tile);
     __syncthreads();
   }
 }
