@@ -67,6 +67,9 @@ def lib():
         L.orc_search_batch.argtypes = [_f32p, c_int, c_int, c_int, _f32p, _f32p, _f32p, c_int,
                                        c_int, _u8p, _i64p, _i64p, _i64p, c_int, c_int, _f32p,
                                        _i64p, c_void_p, c_int, c_int, _i64p, _f32p, _i32p, _f64p]
+        L.orc_search_batch_sharded.argtypes = [
+            _f32p, c_int, c_int, c_int, _f32p, _f32p, _f32p, c_int, c_int, _u8p, _i64p, _i64p,
+            _u8p, _i64p, _i64p, _i64p, c_int, c_int, c_int, c_int, _i64p, _f32p, _i32p]
         _orc = L
     return _orc
 
@@ -212,3 +215,36 @@ def search_batch(queries, codebooks, rotation, coarse, ma, flat, R, init, lut_in
                            _p(out_i, c_int64), _p(out_d, c_float), out_n.ctypes.data_as(_i32p),
                            _p(diag, c_double))
     return out_i, out_d, out_n, diag
+
+
+def search_batch_sharded(queries, codebooks, rotation, coarse, ma, flat, prefix, R, init,
+                         with_fsat=True, nthreads=None):
+    """One shard's adc.search(method='qadc') results (C restatement,
+    order-free form): `flat` = the shard's (blocks, blk_off, ids, count),
+    `prefix` = (blocks, blk_off, ids, global_count) of the GLOBAL first
+    codes of every list. Merging all shards' outputs by (dist, id) equals
+    search_batch on the unsharded index."""
+    blocks, blk_off, ids, _ = flat
+    pblocks, pblk_off, pids, pcount = (np.ascontiguousarray(a) for a in prefix)
+    q = np.ascontiguousarray(queries, np.float32)
+    nq, d = q.shape
+    cb = np.ascontiguousarray(codebooks, np.float32)
+    m = cb.shape[0]
+    rot = None if rotation is None else np.ascontiguousarray(rotation, np.float32)
+    cent = None if coarse is None else np.ascontiguousarray(coarse, np.float32)
+    K = 0 if cent is None else cent.shape[0]
+    out_i = np.empty((nq, R), np.int64)
+    out_d = np.empty((nq, R), np.float32)
+    out_n = np.empty(nq, np.int32)
+    lib().orc_search_batch_sharded(
+        _p(q, c_float), nq, d, m, _p(cb, c_float), _p(rot, c_float), _p(cent, c_float), K, ma,
+        _p(np.ascontiguousarray(blocks, np.uint8), c_uint8),
+        _p(np.ascontiguousarray(blk_off, np.int64), c_int64),
+        _p(np.ascontiguousarray(ids, np.int64), c_int64),
+        _p(pblocks.astype(np.uint8, copy=False), c_uint8),
+        _p(pblk_off.astype(np.int64, copy=False), c_int64),
+        _p(pids.astype(np.int64, copy=False), c_int64),
+        _p(pcount.astype(np.int64, copy=False), c_int64), R, init, int(bool(with_fsat)),
+        nthreads or (os.cpu_count() or 1), _p(out_i, c_int64), _p(out_d, c_float),
+        out_n.ctypes.data_as(_i32p))
+    return out_i, out_d, out_n

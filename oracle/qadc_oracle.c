@@ -554,3 +554,167 @@ void orc_search_batch(const float *queries, int nq, int d, int m,
     }
     pthread_mutex_destroy(&a.mu);
 }
+
+/* ---------- sharded search: one shard of every list + global prefixes ----------
+ *
+ * a shard holds part of each inverted list (range sharding:
+ * a contiguous id range of every list; list sharding: whole lists, the
+ * rest empty). The reference heap's result over the FULL lists equals
+ * the top-R by (mid, id) of {valid lanes with q < 255} U F_sat, where
+ * F_sat = the saturated (q == 255) lanes among the first R valid lanes of
+ * the probe-order stream (orc_qadc_scan above admits a
+ * q == 255 lane only while the heap is not full). Lanes split over shards
+ * therefore merge exactly if every shard computes qmax and F_sat from the
+ * GLOBAL first codes of each list (pblocks / pblk_off / pids, pcount = the
+ * global list lengths) and only one shard (with_fsat) contributes F_sat.
+ * This is the order-free restatement of that semantics: tests check it
+ * against the heap restatement (orc_search_batch) on unsharded indexes
+ * and on merged shards. */
+static void search_one_sharded(int qi, const float *queries, int d, int m,
+                               const float *codebooks, const float *rotation,
+                               const float *cent, int K, int ma,
+                               const uint8_t *blocks, const int64_t *blk_off,
+                               const int64_t *ids, const uint8_t *pblocks,
+                               const int64_t *pblk_off, const int64_t *pids,
+                               const int64_t *pcount, int R, int init,
+                               int with_fsat, int64_t *out_ids, float *out_d,
+                               int32_t *out_n)
+{
+    int dsub = d / m, mrows = m / 2, nslots = cent ? ma : 1, s, i, size = 0;
+    int need = R;
+    const float *q = queries + (size_t)qi * d;
+    int64_t *cells = (int64_t *)malloc(sizeof(int64_t) * (size_t)nslots);
+    float *res = (float *)malloc(sizeof(float) * (size_t)nslots * d);
+    float *y = (float *)malloc(sizeof(float) * (size_t)d);
+    float *hd = (float *)malloc(sizeof(float) * (size_t)R);
+    int64_t *hi = (int64_t *)malloc(sizeof(int64_t) * (size_t)R);
+    float tab[128 * 16];
+    uint8_t qt[128 * 16], lane_d[16];
+    double qmax = 0.0;
+
+    if (!cent) {
+        cells[0] = 0;
+        memcpy(res, q, sizeof(float) * (size_t)d);
+    } else {
+        orc_probe(cent, K, d, q, ma, cells, res);
+    }
+    for (s = 0; s < nslots; s++) {
+        int64_t c = cells[s], bi;
+        const uint8_t *pb = pblocks + (size_t)pblk_off[c] * mrows * 16;
+        const int64_t *pid = pids + (size_t)pblk_off[c] * 16;
+        int64_t pnb = pblk_off[c + 1] - pblk_off[c];
+        const uint8_t *cb = blocks + (size_t)blk_off[c] * mrows * 16;
+        const int64_t *cid = ids + (size_t)blk_off[c] * 16;
+        int64_t nb = blk_off[c + 1] - blk_off[c];
+        const float *r = res + (size_t)s * d;
+        float tmin, fqmin, fdelta;
+        double qmin, delta;
+        if (rotation) {
+            orc_rotate(rotation, d, r, y);
+            r = y;
+        }
+        orc_compute_tables(codebooks, m, dsub, r, tab);
+        if (s == 0)
+            qmax = (double)orc_find_qmax(tab, m, pb, pcount[c], R, init);
+        tmin = tab[0];
+        for (i = 1; i < m * 16; i++)
+            if (tab[i] < tmin)
+                tmin = tab[i];
+        qmin = (double)tmin < qmax ? (double)tmin : qmax;
+        delta = orc_quantize_tables(tab, m, qmin, qmax, qt);
+        fqmin = (float)qmin;
+        fdelta = (float)delta;
+        /* F_sat: the first R valid lanes of the global stream */
+        for (bi = 0; with_fsat && need > 0 && bi < pnb; bi++) {
+            lane_sums(pb + (size_t)bi * mrows * 16, mrows, qt, lane_d);
+            for (i = 0; i < 16 && need > 0; i++) {
+                if (pid[bi * 16 + i] < 0)
+                    continue;
+                need--;
+                if (lane_d[i] == 255)
+                    size = heap_push(hd, hi, size, R,
+                                     fqmin + (255.0f + 0.5f) * fdelta,
+                                     pid[bi * 16 + i]);
+            }
+        }
+        /* this shard's lanes of the cell */
+        for (bi = 0; bi < nb; bi++) {
+            lane_sums(cb + (size_t)bi * mrows * 16, mrows, qt, lane_d);
+            for (i = 0; i < 16; i++) {
+                if (cid[bi * 16 + i] < 0 || lane_d[i] == 255)
+                    continue;
+                size = heap_push(hd, hi, size, R,
+                                 fqmin + ((float)lane_d[i] + 0.5f) * fdelta,
+                                 cid[bi * 16 + i]);
+            }
+        }
+    }
+    orc_heap_extract(hd, hi, size);
+    for (i = 0; i < R; i++) {
+        out_ids[(size_t)qi * R + i] = i < size ? hi[i] : -1;
+        out_d[(size_t)qi * R + i] = i < size ? hd[i] : INFINITY;
+    }
+    out_n[qi] = size;
+    free(cells);
+    free(res);
+    free(y);
+    free(hd);
+    free(hi);
+}
+
+typedef struct {
+    const float *queries; int nq, d, m; const float *codebooks, *rotation, *cent;
+    int K, ma; const uint8_t *blocks; const int64_t *blk_off, *ids;
+    const uint8_t *pblocks; const int64_t *pblk_off, *pids, *pcount;
+    int R, init, with_fsat; int64_t *out_ids; float *out_d; int32_t *out_n;
+    int next; pthread_mutex_t mu;
+} sharded_args;
+
+static void *sharded_worker(void *p)
+{
+    sharded_args *a = (sharded_args *)p;
+    for (;;) {
+        int qi;
+        pthread_mutex_lock(&a->mu);
+        qi = a->next++;
+        pthread_mutex_unlock(&a->mu);
+        if (qi >= a->nq)
+            return NULL;
+        search_one_sharded(qi, a->queries, a->d, a->m, a->codebooks, a->rotation,
+                           a->cent, a->K, a->ma, a->blocks, a->blk_off, a->ids,
+                           a->pblocks, a->pblk_off, a->pids, a->pcount, a->R,
+                           a->init, a->with_fsat, a->out_ids, a->out_d,
+                           a->out_n);
+    }
+}
+
+void orc_search_batch_sharded(const float *queries, int nq, int d, int m,
+                              const float *codebooks, const float *rotation,
+                              const float *cent, int K, int ma,
+                              const uint8_t *blocks, const int64_t *blk_off,
+                              const int64_t *ids, const uint8_t *pblocks,
+                              const int64_t *pblk_off, const int64_t *pids,
+                              const int64_t *pcount, int R, int init,
+                              int with_fsat, int nthreads, int64_t *out_ids,
+                              float *out_d, int32_t *out_n)
+{
+    sharded_args a;
+    pthread_t th[256];
+    int t, nt = nthreads < 1 ? 1 : (nthreads > 256 ? 256 : nthreads);
+    a.queries = queries; a.nq = nq; a.d = d; a.m = m; a.codebooks = codebooks;
+    a.rotation = rotation; a.cent = cent; a.K = K; a.ma = ma; a.blocks = blocks;
+    a.blk_off = blk_off; a.ids = ids; a.pblocks = pblocks; a.pblk_off = pblk_off;
+    a.pids = pids; a.pcount = pcount; a.R = R; a.init = init;
+    a.with_fsat = with_fsat; a.out_ids = out_ids; a.out_d = out_d;
+    a.out_n = out_n; a.next = 0;
+    pthread_mutex_init(&a.mu, NULL);
+    if (nt == 1) {
+        sharded_worker(&a);
+    } else {
+        for (t = 0; t < nt; t++)
+            pthread_create(&th[t], NULL, sharded_worker, &a);
+        for (t = 0; t < nt; t++)
+            pthread_join(th[t], NULL);
+    }
+    pthread_mutex_destroy(&a.mu);
+}

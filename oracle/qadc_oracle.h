@@ -94,6 +94,25 @@ void orc_search_batch(const float *queries, int nq, int d, int m,
                       int64_t *out_ids, float *out_d, int32_t *out_n,
                       double *diag);
 
+/*
+ * Sharded search, order-free restatement of the heap
+ * semantics: the shard's lists (blocks / blk_off / ids, any subset of each
+ * list's lanes) are scanned; qmax and F_sat come from the GLOBAL first
+ * codes of each list (pblocks / pblk_off / pids; pcount = global list
+ * lengths); only with_fsat != 0 contributes F_sat. Probe and LUT as in
+ * orc_search_batch (no injection). Merging every shard's (nq, R) output by
+ * (dist, id) gives orc_search_batch's result on the unsharded index.
+ */
+void orc_search_batch_sharded(const float *queries, int nq, int d, int m,
+                              const float *codebooks, const float *rotation,
+                              const float *cent, int K, int ma,
+                              const uint8_t *blocks, const int64_t *blk_off,
+                              const int64_t *ids, const uint8_t *pblocks,
+                              const int64_t *pblk_off, const int64_t *pids,
+                              const int64_t *pcount, int R, int init,
+                              int with_fsat, int nthreads, int64_t *out_ids,
+                              float *out_d, int32_t *out_n);
+
 #ifdef __cplusplus
 }
 #endif
