@@ -42,6 +42,7 @@ METRICS = {
     "cfg1": "Quick ADC codes scanned/s (whole job) at configs[1]: exhaustive, m=32x4-bit, N=1e7/GPU, Q=1000, R=100",
     "cfg2": "Quick ADC codes scanned/s (whole job) at configs[2]: IVF K=4096 + OPQ, m=32x4-bit, Q=1e4, R=100",
     "cfg3": "Quick ADC codes scanned/s (whole job) at configs[3]: exhaustive, d=960, m=32x4-bit, N=1e6, Q=1000, R=100",
+    "cfg4": "Quick ADC codes scanned/s (whole job) at configs[4]: IVF K=65536 + OPQ, m=32x4-bit, N=1e9 range-sharded, Q=1e4, nprobe=64, R=100",
 }
 METRIC = METRICS["cfg1"]
 UNIT = "codes/s"
@@ -53,9 +54,10 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3"])
+    p.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
     p.add_argument("--nprobe", type=int, default=None, help="IVF configs: probed cells (ma)")
-    p.add_argument("--n", type=int, default=None, help="codes per GPU (default: the config's N)")
+    p.add_argument("--n", type=int, default=None,
+                   help="codes per GPU (exhaustive) / in total (IVF); default: the config's N")
     p.add_argument("--queries", type=int, default=None)
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU work of the bounded reference sample")
@@ -192,32 +194,69 @@ def flat_lists(codes_np, ids_np, row_off):
             np.asarray(count, np.int64))
 
 
-def cpu_reference_run_ivf(cfg, pq, coarse, codes_np, ids_np, row_off, qs, R, init, ma, seconds,
+def probed_sub_index(pq, coarse, rows, ids, row_off, qs, ma):
+    """Reference-layout lists (oracle input) holding only the lists the
+    given queries probe (every other list empty): the oracle's result and
+    work for these queries are those of the full index. Rows come from the
+    GPU index's row-ordered lists. Returns (flat, codes scanned)."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_1704_07355_b200.qadc import transpose_list
+
+    cells = np.stack([orc.probe(coarse, q, ma)[0] for q in qs])
+    want = np.zeros(row_off.shape[0] - 1, bool)
+    want[np.unique(cells)] = True
+    off = row_off.cpu().numpy()
+    sizes = np.diff(off)
+    sel = torch.from_numpy(np.nonzero(want)[0])
+    from paper_1704_07355_b200.shard import _ranges
+    idx = _ranges(row_off[:-1][sel.to(row_off.device)], row_off[1:][sel.to(row_off.device)]
+                  - row_off[:-1][sel.to(row_off.device)])
+    r_h, i_h = rows[idx].cpu().numpy(), ids[idx].cpu().numpy()
+    blocks, bids, boff, count = [], [], [0], []
+    o = 0
+    for L in range(want.shape[0]):
+        k = int(sizes[L]) if want[L] else 0
+        if k:
+            tl = transpose_list(r_h[o:o + k], i_h[o:o + k])
+            blocks.append(tl.blocks.reshape(-1))
+            bids.append(tl.ids)
+            boff.append(boff[-1] + tl.blocks.shape[0])
+            o += k
+        else:
+            boff.append(boff[-1])
+        count.append(k)
+    flat = (np.concatenate(blocks) if blocks else np.zeros(0, np.uint8), np.asarray(boff, np.int64),
+            np.concatenate(bids) if bids else np.zeros(0, np.int64), np.asarray(count, np.int64))
+    return flat, int(sizes[cells].sum())
+
+
+def cpu_reference_run_ivf(cfg, pq, coarse, rows, ids, row_off, qs, R, init, ma, seconds,
                           nthreads=None):
     """IVF variant of cpu_reference_run: probe, OPQ rotation, tables, qmax
     and quantization restated (oracle/), block scan = the reference's own
-    compiled qadc_scan_u8 (oracle/_ref)."""
+    compiled qadc_scan_u8 (oracle/_ref), on a bounded query sample over the
+    lists those queries probe."""
     from oracle import oracle as orc
 
-    flat = flat_lists(codes_np, ids_np, row_off)
     use_ref = orc.ref_lib() is not None
     nthreads = nthreads or os.cpu_count() or 1
-    probe = qs[: max(1, min(nthreads, qs.shape[0]))]
+    probe = qs[: max(1, min(2 * nthreads, qs.shape[0]))]
+    flat, _ = probed_sub_index(pq, coarse, rows, ids, row_off, probe, ma)
     t0 = time.perf_counter()
     orc.search_batch(probe, pq.codebooks, pq.rotation, coarse, ma, flat, R, init,
                      use_ref_scan=use_ref, nthreads=nthreads)
     per_q = (time.perf_counter() - t0) / probe.shape[0]
     nq = int(max(probe.shape[0], min(qs.shape[0], seconds / max(per_q, 1e-6))))
     sample = qs[:nq]
+    flat, codes_scanned = probed_sub_index(pq, coarse, rows, ids, row_off, sample, ma)
     t0 = time.perf_counter()
     oi, od, on, _ = orc.search_batch(sample, pq.codebooks, pq.rotation, coarse, ma, flat, R, init,
                                      use_ref_scan=use_ref, nthreads=nthreads)
     wall = time.perf_counter() - t0
-    sizes = np.diff(flat[1]) * 16
-    cells = np.array([orc.probe(coarse, q, ma)[0] for q in sample])
-    codes_scanned = int(np.asarray(flat[3])[cells].sum())
-    return (codes_scanned / wall, f"{nq} of {qs.shape[0]} queries, nprobe={ma}",
-            "reference" if use_ref else "port", nthreads, (oi, od, on), wall)
+    return (codes_scanned / wall, f"{nq} of {qs.shape[0]} queries, nprobe={ma}, over the lists "
+            "they probe", "reference" if use_ref else "port", nthreads, (oi, od, on), wall)
 
 
 def measure_recall(cfg, pq, n, qs, ids, codes=None):
@@ -281,22 +320,28 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     _native.require_device()
-    from paper_1704_07355_b200.workload import IVF_CONFIGS, build_ivf_index, load_ivf_model
+    from paper_1704_07355_b200.workload import (IVF_CONFIGS, build_ivf_index,
+                                                build_sharded_ivf_index, load_ivf_model)
     ivf_cfg = IVF_CONFIGS.get(args.config)
     cfg = ivf_cfg or CONFIGS[args.config]
     n = args.n or cfg.n
     nq = args.queries or cfg.q
     R, init = cfg.R, cfg.init
     ma = 1
+    t_build = time.perf_counter()
     if ivf_cfg is not None:
-        if world > 1:
-            raise SystemExit("IVF list sharding across ranks is not wired into bench.py yet")
         ma = args.nprobe or ivf_cfg.nprobe
         pq, coarse = load_ivf_model(ivf_cfg)
-        index, sizes, codes, order, row_off = build_ivf_index(ivf_cfg, pq, coarse, n)
+        if world > 1:
+            index, rows, row_ids, row_off = build_sharded_ivf_index(
+                ivf_cfg, pq, coarse, n, rank, world, prefix=max(init, R))
+        else:
+            index, sizes, rows, row_ids, row_off = build_ivf_index(ivf_cfg, pq, coarse, n)
     else:
         pq = load_pq(cfg)
         index, codes = build_shard_index(cfg, pq, n, rank, world, prefix=max(init, R))
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
     qs = queries(cfg, nq)
     q_dev = torch.from_numpy(qs).cuda()
     q_pin = torch.from_numpy(qs).pin_memory()
@@ -369,9 +414,14 @@ def run_b200(args):
     ms_e2e = max_over_ranks(e2.elapsed_time(e3) / args.steps)
 
     # codes scanned per step = sum over (query, probed list) of len(list),
-    # counted by the library (stats["codes"]); all ranks together
+    # counted by the library on each rank's own codes (stats["codes"]),
+    # summed over ranks
     per_rank_codes = codes_scanned / args.steps
-    total_codes = per_rank_codes * world if ivf_cfg is None else per_rank_codes
+    total_codes = per_rank_codes
+    if world > 1:
+        t = torch.tensor([per_rank_codes], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        total_codes = float(t.item())
     value = total_codes / (ms_dev * 1e-3)
     e2e_value = total_codes / (ms_e2e * 1e-3)
 
@@ -384,7 +434,7 @@ def run_b200(args):
     achieved = lookups / scan_s / 1e9
     pk = measured_peaks()
     # codes of every DISTINCT list touched once per batch
-    hbm_bytes = n * pq.m / 2
+    hbm_bytes = index.ncodes * pq.m / 2
     roof = {
         "bound": "int",
         "achieved": round(achieved, 2),
@@ -406,14 +456,22 @@ def run_b200(args):
         out = {
             "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (BASELINE mixture generator drawn on GPU; reference-trained PQ)",
-            "config": {"workload": cfg.name, "N_per_gpu": n, "N_total": n * world, "Q": nq,
+            "higher_is_better": True, "scaling": "weak" if ivf_cfg is None else "strong",
+            "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (BASELINE mixture generator drawn on GPU; " + (
+                "reference-trained PQ)" if ivf_cfg is None or ivf_cfg.coarse_file else
+                "GPU-trained coarse K=%d + residual PQ, seeded; see DESIGN.md)" % ivf_cfg.K),
+            "config": {"workload": cfg.name,
+                       "N_per_gpu": n if ivf_cfg is None else index.ncodes,
+                       "N_total": n * world if ivf_cfg is None else n, "Q": nq,
                        "R": R, "init": init, "m": pq.m, "d": pq.d, "nprobe": ma,
+                       "sharding": "range (weak)" if ivf_cfg is None else
+                       ivf_cfg.sharding + " (strong)",
                        "codes_scanned_per_step": int(total_codes),
-                       "l2": "inputs larger than L2 (codes %.0f MB > 126 MB)" % (n * pq.m / 2e6)
-                       if n * pq.m / 2 > 126e6 else
-                       "index %.0f MB fits L2: steady-state (L2-warm) throughput" % (n * pq.m / 2e6)},
+                       "index_build_s": round(t_build, 1),
+                       "l2": "inputs larger than L2 (codes %.0f MB > 126 MB)" % (hbm_bytes / 1e6)
+                       if hbm_bytes > 126e6 else
+                       "index %.0f MB fits L2: steady-state (L2-warm) throughput" % (hbm_bytes / 1e6)},
             "qps": nq / (ms_dev * 1e-3),
             "e2e": {"value": e2e_value, "unit": UNIT, "qps": nq / (ms_e2e * 1e-3),
                     "ms_per_step": ms_e2e, "h2d_bytes_per_step": int(nq * pq.d * 4),
@@ -425,14 +483,13 @@ def run_b200(args):
             "reruns": reruns,
         }
         if world == 1 and not args.no_cpu_baseline:
-            codes_np = codes.cpu().numpy()
             if ivf_cfg is not None:
                 v, sample, kind, cores, (oi, od, on), wall = cpu_reference_run_ivf(
-                    ivf_cfg, pq, coarse, codes_np, order.cpu().numpy(), row_off.cpu().numpy(),
-                    qs, R, init, ma, args.cpu_seconds)
+                    ivf_cfg, pq, coarse, rows, row_ids, row_off, qs, R, init, ma,
+                    args.cpu_seconds)
             else:
                 v, sample, kind, cores, (oi, od, on), wall = cpu_reference_run(
-                    cfg, codes_np, n, qs, R, init, args.cpu_seconds)
+                    cfg, codes.cpu().numpy(), n, qs, R, init, args.cpu_seconds)
             k = oi.shape[0]
             gi_np, gd_np = out_i.numpy()[:k], out_d.numpy()[:k]
             exact = int(sum(np.array_equal(gi_np[i], oi[i]) and
@@ -455,12 +512,14 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    from paper_1704_07355_b200.workload import CONFIGS, load_pq, queries
+    from paper_1704_07355_b200.workload import (CONFIGS, IVF_CONFIGS, build_ivf_index, load_ivf_model,
+                                                load_pq, queries)
 
-    cfg = CONFIGS[args.config]
+    ivf_cfg = IVF_CONFIGS.get(args.config)
+    cfg = ivf_cfg or CONFIGS[args.config]
     n = args.n or cfg.n
     nq = args.queries or cfg.q
-    pq = load_pq(cfg)
+    ma = (args.nprobe or ivf_cfg.nprobe) if ivf_cfg is not None else 1
     # index construction is setup, not the timed path: encode on the GPU if
     # one is visible (same index the B200 arm scans), else fail loudly
     import torch
@@ -468,25 +527,37 @@ def run_reference(args):
     from paper_1704_07355_b200.workload import shard_codes
     if not torch.cuda.is_available():
         return {"impl": "reference", "unavailable": "index setup needs the GPU encoder"}
-    codes_np = shard_codes(cfg, pq, n, 0).cpu().numpy()
     qs = queries(cfg, nq)
+    if ivf_cfg is not None:
+        pq, coarse = load_ivf_model(ivf_cfg)
+        _, _, rows, row_ids, row_off = build_ivf_index(ivf_cfg, pq, coarse, n)
+
+        def one(seconds):
+            return cpu_reference_run_ivf(ivf_cfg, pq, coarse, rows, row_ids, row_off, qs, cfg.R,
+                                         cfg.init, ma, seconds)
+    else:
+        pq = load_pq(cfg)
+        codes_np = shard_codes(cfg, pq, n, 0).cpu().numpy()
+
+        def one(seconds):
+            return cpu_reference_run(cfg, codes_np, n, qs, cfg.R, cfg.init, seconds)
     vals, walls = [], []
     desc = kind = cores = None
     per_step = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
     for i in range(args.warmup + args.steps):
-        v, desc, kind, cores, _, wall = cpu_reference_run(cfg, codes_np, n, qs, cfg.R, cfg.init,
-                                                          per_step)
+        v, desc, kind, cores, _, wall = one(per_step)
         if i >= args.warmup:
             vals.append(v)
             walls.append(wall)
     value = statistics.median(vals)
     return {
-        "impl": "reference", "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup,
+        "impl": "reference", "metric": METRICS[args.config], "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(walls) * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (BASELINE mixture generator; reference-trained PQ)",
-        "config": {"workload": cfg.name, "N_per_gpu": n, "Q": nq, "R": cfg.R, "init": cfg.init},
+        "scaling": "weak" if ivf_cfg is None else "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (BASELINE mixture generator; same index as the B200 arm)",
+        "config": {"workload": cfg.name, "N_per_gpu": n, "Q": nq, "R": cfg.R, "init": cfg.init,
+                   "nprobe": ma},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -18,7 +18,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libqadc_b200.so"
-SOURCES = ["layout.cu", "lut.cu", "scan.cu", "select.cu", "simple.cu", "encode.cu", "peak.cu", "capi.cu"]
+SOURCES = ["layout.cu", "lut.cu", "probe_gemm.cu", "scan.cu", "select.cu", "simple.cu", "encode.cu",
+           "peak.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                      "-I" + str(ROOT / "include")]
@@ -58,7 +59,9 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=min(6, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     if force or _stale(LIB, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs)]
+        # cuBLAS: the tensor-core GEMM of the coarse probe (probe_gemm.cu)
+        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcublas",
+               "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

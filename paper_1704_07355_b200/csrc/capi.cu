@@ -176,8 +176,15 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
       cells = cells_in;
     } else {
       if ((rc = cells_b.alloc(npairs, st))) return cuda_fail(cudaGetLastError(), "alloc cells");
-      if (!(idx->cnorm && launch_probe_fast(idx->coarseT, idx->coarse, idx->cnorm, idx->K,
-                                            idx->d, queries, nq, ma, cells_b.p, st)))
+      static const int probe_kind = scan_env_int("QADC_B200_PROBE", 2);  // 2 gemm, 1 ffma, 0 exact
+      const bool done =
+          (probe_kind >= 2 && idx->pcsplit &&
+           launch_probe_gemm(idx->coarse, idx->pmu, idx->pcsplit, idx->pcn2, idx->K, idx->d,
+                             queries, nq, ma, cells_b.p, st)) ||
+          (probe_kind >= 1 && idx->cnorm &&
+           launch_probe_fast(idx->coarseT, idx->coarse, idx->cnorm, idx->K, idx->d, queries, nq,
+                             ma, cells_b.p, st));
+      if (!done)
         launch_probe(idx->coarseT, idx->K, idx->d, queries, nq, ma, cells_b.p, st);
       QADC_CUDA(cudaGetLastError());
       ss.launches++;
@@ -574,6 +581,11 @@ int index_common(int d, int m, int nlists, const float *coarse, bool coarse_dev,
     k_transpose<<<gridn((int64_t)nlists * d), 256>>>(idx->coarse, nlists, d, idx->coarseT);
     QADC_CUDA(cudaMalloc(&idx->cnorm, (size_t)nlists * 4));
     launch_cnorm(idx->coarse, nlists, d, idx->cnorm, 0);
+    if (probe_gemm_supported(nlists, d)) {
+      if (int rc = probe_gemm_prepare(idx->coarse, nlists, d, &idx->pmu, &idx->pcsplit, &idx->pcn2, 0))
+        return rc;
+      idx->bytes += (int64_t)nlists * (3 * d * 2 + 4) + d * 4;
+    }
     idx->bytes += 2 * (int64_t)cb + (int64_t)nlists * 4;
   }
   const size_t bb = (size_t)m * 16 * (d / m) * 4;
@@ -603,7 +615,7 @@ extern "C" void qadc_b200_index_destroy(qadc_b200_index *idx) {
   if (idx->own_prefix) {
     cudaFree(idx->pcodes); cudaFree(idx->pids); cudaFree(idx->pchunk_off); cudaFree(idx->planes);
   }
-  cudaFree(idx->coarse); cudaFree(idx->coarseT); cudaFree(idx->cnorm); cudaFree(idx->codebooks); cudaFree(idx->rotation); cudaFree(idx->rotationT);
+  cudaFree(idx->coarse); cudaFree(idx->coarseT); cudaFree(idx->cnorm); cudaFree(idx->pmu); cudaFree(idx->pcsplit); cudaFree(idx->pcn2); cudaFree(idx->codebooks); cudaFree(idx->rotation); cudaFree(idx->rotationT);
   cudaFree(idx->codes); cudaFree(idx->valid); cudaFree(idx->ids); cudaFree(idx->chunk_list);
   cudaFree(idx->chunk_off); cudaFree(idx->lanes); cudaFree(idx->count); cudaFree(idx->scan_count);
   delete idx;
@@ -818,8 +830,20 @@ extern "C" int qadc_b200_probe(const float *coarse, int K, int d, const float *q
   float *cn = nullptr;
   QADC_CUDA(cudaMallocAsync(&cn, (size_t)K * 4, st));
   launch_cnorm(coarse, K, d, cn, st);
-  if (!launch_probe_fast(cT, coarse, cn, K, d, queries, nq, ma, cells, st))
-    launch_probe(cT, K, d, queries, nq, ma, cells, st);
+  static const int probe_kind = scan_env_int("QADC_B200_PROBE", 2);
+  bool done = false;
+  if (probe_kind >= 2 && probe_gemm_supported(K, d)) {
+    float *mu = nullptr, *cn2 = nullptr;
+    void *cs = nullptr;
+    if (probe_gemm_prepare(coarse, K, d, &mu, &cs, &cn2, st) == kOk)
+      done = launch_probe_gemm(coarse, mu, cs, cn2, K, d, queries, nq, ma, cells, st);
+    cudaStreamSynchronize(st);
+    cudaFree(mu);
+    cudaFree(cs);
+    cudaFree(cn2);
+  }
+  if (!done && probe_kind >= 1) done = launch_probe_fast(cT, coarse, cn, K, d, queries, nq, ma, cells, st);
+  if (!done) launch_probe(cT, K, d, queries, nq, ma, cells, st);
   cudaFreeAsync(cn, st);
   cudaFreeAsync(cT, st);
   if (residuals)

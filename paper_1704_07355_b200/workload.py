@@ -116,57 +116,216 @@ class IvfConfig:
     name: str
     mix: datagen.Mixture
     m: int
-    n: int
+    n: int  # total codes (list-sharded and range-sharded configs alike)
     q: int
     R: int
     init: int
     K: int
     nprobe: int
-    coarse_file: str
+    coarse_file: str  # "" = coarse model trained on the GPU at setup (config 4)
     codebooks_file: str
     rotation_file: str
+    sharding: str  # "lists" (config 2) or "range" (config 4)
 
 
 IVF_CONFIGS = {
     "cfg2": IvfConfig("cfg2_ivf_opq_K4096_m32_N1e8_Q1e4", datagen.SIFT_LIKE, 32, 100_000_000,
                       10_000, 100, 1000, 4096, 16, "cfg2_coarse_K4096.npy",
-                      "cfg2_m32_codebooks.npy", "cfg2_rotation.npy"),
+                      "cfg2_m32_codebooks.npy", "cfg2_rotation.npy", "lists"),
+    "cfg4": IvfConfig("cfg4_ivf_opq_K65536_m32_N1e9_Q1e4", datagen.SIFT_LIKE, 32, 1_000_000_000,
+                      10_000, 100, 1000, 65536, 64, "", "", "cfg2_rotation.npy", "range"),
 }
+
+# config 4 base: a global grid of 10^6-vector chunks (chunk g = ids
+# g*10^6 ..), so every range shard of 1, 2, 4 or 8 GPUs draws exactly its
+# own chunks and the dataset does not depend on the GPU count
+CFG4_CHUNK = 1_000_000
 
 
 def load_ivf_model(cfg: IvfConfig):
+    if not cfg.coarse_file:
+        return train_ivf_model_gpu(cfg)
     pq = _PQ(np.load(BENCH_DATA / cfg.codebooks_file), np.load(BENCH_DATA / cfg.rotation_file))
     return pq, np.load(BENCH_DATA / cfg.coarse_file)
 
 
-def build_ivf_index(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, shard: int = 0,
-                    device="cuda", chunk: int = 1 << 22):
-    """IVF index of n base vectors drawn on the GPU: coarse assignment,
-    residual, OPQ rotation + PQ encoding (GPU encoder), lists with ids
-    ascending (ivf.py:109-151). Returns the DeviceIndex and the list sizes."""
+def assign_tensor_core(X, C, cn=None, chunk: int = 16384):
+    """Index-build coarse assignment on the tensor cores: argmin over
+    ||c||^2 - 2 x.c with TF32 cuBLAS GEMMs (cuBLAS for a plain library GEMM;
+    not the search path). Near-ties may resolve differently from the exact
+    einsum order of qadc_b200_assign; the index is whatever this produces
+    and parity is defined given the index."""
+    import torch
+
+    if cn is None:
+        cn = (C.double() ** 2).sum(1).float()
+    out = torch.empty(X.shape[0], dtype=torch.int64, device=X.device)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        Ct = C.t().contiguous()
+        for i in range(0, X.shape[0], chunk):
+            S = torch.addmm(cn, X[i:i + chunk], Ct, beta=1.0, alpha=-2.0)
+            out[i:i + chunk] = S.argmin(1)
+            del S
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return out
+
+
+def train_ivf_model_gpu(cfg: IvfConfig, n_learn: int = 1 << 21, iters: int = 8,
+                        pq_learn: int = 1 << 18, pq_iters: int = 25, seed: int = 0):
+    """Config 4 model, trained on the GPU at setup (seeded): the reference's
+    NumPy k-means cannot train K=65536 (SURVEY 7 "Config-4 index build"),
+    so coarse centroids = Lloyd k-means (seeded random-sample init, empty
+    cells re-seeded from random learn points) on 2^21 learn vectors, OPQ
+    rotation = config 2's seeded orthogonal matrix, residual PQ codebooks =
+    Lloyd (16 centroids per 4-dim subspace) on 2^18 rotated residuals.
+    The model is an INPUT of the index; parity is given the index."""
+    import torch
+
+    dev = torch.device("cuda")
+    X = datagen.mixture_torch(cfg.mix, n_learn, seed=SEED * 1000 + 999, centre_seed=CORPUS,
+                              stream=datagen.STREAM_LEARN, device=dev)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    C = X[torch.randperm(n_learn, generator=g)[: cfg.K].to(dev)].clone()
+    for _ in range(iters):
+        lab = assign_tensor_core(X, C)
+        cnt = torch.bincount(lab, minlength=cfg.K)
+        S = torch.zeros((cfg.K, cfg.mix.d), dtype=torch.float64, device=dev)
+        S.index_add_(0, lab, X.double())
+        newC = (S / cnt.clamp(min=1).unsqueeze(1).double()).float()
+        empty = (cnt == 0).nonzero().flatten()
+        if empty.numel():
+            pick = torch.randperm(n_learn, generator=g)[: empty.numel()].to(dev)
+            newC[empty] = X[pick]
+        C = newC
+    rot = np.load(BENCH_DATA / cfg.rotation_file)
+    Rt = torch.from_numpy(rot).to(dev)
+    lab = assign_tensor_core(X[:pq_learn], C)
+    Y = (X[:pq_learn] - C[lab]) @ Rt.t()
+    m, dsub = cfg.m, cfg.mix.d // cfg.m
+    Ys = Y.view(pq_learn, m, dsub).transpose(0, 1).contiguous()  # (m, n, dsub)
+    idx = torch.randperm(pq_learn, generator=g)[:16].to(dev)
+    cb = Ys[:, idx, :].clone()  # (m, 16, dsub)
+    for _ in range(pq_iters):
+        d2 = ((Ys[:, :, None, :] - cb[:, None, :, :]) ** 2).sum(-1)  # (m, n, 16)
+        a = d2.argmin(-1)
+        oh = torch.nn.functional.one_hot(a, 16).float()  # (m, n, 16)
+        cnt = oh.sum(1)  # (m, 16)
+        sums = torch.bmm(oh.transpose(1, 2), Ys)  # (m, 16, dsub)
+        cb = torch.where(cnt.unsqueeze(-1) > 0, sums / cnt.clamp(min=1).unsqueeze(-1), cb)
+    del X, Y, Ys
+    pq = _PQ(cb.cpu().numpy().astype(np.float32), rot)
+    return pq, C.cpu().numpy().astype(np.float32)
+
+
+def _sorted_rows(codes, labels, ids, K):
+    """Row-ordered lists: stable sort by cell (ids stay ascending in every
+    list, ivf.py:109-151), row offsets."""
+    import torch
+
+    order = torch.argsort(labels, stable=True)
+    sizes = torch.bincount(labels, minlength=K)
+    row_off = torch.zeros(K + 1, dtype=torch.int64, device=codes.device)
+    row_off[1:] = torch.cumsum(sizes, 0)
+    return codes[order].contiguous(), ids[order].contiguous(), row_off
+
+
+def ivf_rows(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, device="cuda",
+             chunk: int = 1 << 22, rank: int = 0, world: int = 1):
+    """Base vectors drawn on the GPU, coarse-assigned, residual + OPQ + PQ
+    encoded (GPU encoder), grouped into row-ordered lists.
+
+    Config 2 (list sharding): the whole base of n codes (every rank builds
+    it; `shard_ivf_lists` keeps the rank's lists), exact einsum-order
+    assignment (qadc_b200_assign, the reference's kmeans.assign_batch
+    semantics). Config 4 (range sharding): rank r draws the chunks of its
+    id range of the global CFG4_CHUNK grid; tensor-core assignment.
+    Returns (codes (n_r, m/2), ids (n_r,), row_off (K + 1,))."""
     import torch
 
     from .ivf import assign_device, encode_device
 
     C = torch.from_numpy(np.ascontiguousarray(coarse, dtype=np.float32)).to(device)
-    codes = torch.empty((n, pq.m // 2), dtype=torch.uint8, device=device)
-    labels = torch.empty(n, dtype=torch.int64, device=device)
-    for c0 in range(0, n, chunk):
-        k = min(chunk, n - c0)
-        X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + shard, centre_seed=CORPUS,
-                                  stream=datagen.STREAM_BASE * 100 + c0 // chunk, device=device)
-        lab = assign_device(coarse, X)
-        labels[c0:c0 + k] = lab
-        codes[c0:c0 + k] = encode_device(pq, X - C[lab])
-        del X
-    order = torch.argsort(labels, stable=True)
-    sizes = torch.bincount(labels, minlength=C.shape[0])
-    row_off = torch.zeros(C.shape[0] + 1, dtype=torch.int64, device=device)
-    row_off[1:] = torch.cumsum(sizes, 0)
-    sorted_codes = codes[order].contiguous()
-    del codes, labels
-    index = DeviceIndex.from_device_rows(
-        pq.d, pq.m, sorted_codes, row_off, torch.from_numpy(pq.codebooks).to(device),
+    if cfg.sharding == "range":
+        nch = -(-n // CFG4_CHUNK)
+        per = -(-nch // world)
+        gs = range(rank * per, min(nch, (rank + 1) * per))
+        spans = [(g * CFG4_CHUNK, min(n, (g + 1) * CFG4_CHUNK), g) for g in gs]
+        cn = (C.double() ** 2).sum(1).float()
+    else:
+        spans = [(c0, min(n, c0 + chunk), c0 // chunk) for c0 in range(0, n, chunk)]
+    tot = sum(b - a for a, b, _ in spans)
+    codes = torch.empty((tot, pq.m // 2), dtype=torch.uint8, device=device)
+    labels = torch.empty(tot, dtype=torch.int64, device=device)
+    ids = torch.empty(tot, dtype=torch.int64, device=device)
+    o = 0
+    for a, b, g in spans:
+        k = b - a
+        if cfg.sharding == "range":
+            X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + 4, centre_seed=CORPUS,
+                                      stream=datagen.STREAM_BASE * 100_000 + g, device=device)
+            lab = assign_tensor_core(X, C, cn)
+        else:
+            X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000, centre_seed=CORPUS,
+                                      stream=datagen.STREAM_BASE * 100 + g, device=device)
+            lab = assign_device(coarse, X)
+        labels[o:o + k] = lab
+        codes[o:o + k] = encode_device(pq, X - C[lab])
+        ids[o:o + k] = torch.arange(a, b, dtype=torch.int64, device=device)
+        o += k
+        del X, lab
+    rows, rid, row_off = _sorted_rows(codes, labels, ids, C.shape[0])
+    del codes, labels, ids
+    return rows, rid, row_off
+
+
+def make_ivf_index(pq: _PQ, coarse: np.ndarray, rows, ids, row_off, device="cuda"):
+    import torch
+
+    return DeviceIndex.from_device_rows(
+        pq.d, pq.m, rows, row_off, torch.from_numpy(pq.codebooks).to(device),
         rotation=torch.from_numpy(np.ascontiguousarray(pq.rotation, np.float32)).to(device),
-        coarse=C, ids=order + shard * n)
-    return index, sizes.cpu().numpy(), sorted_codes, order, row_off
+        coarse=torch.from_numpy(np.ascontiguousarray(coarse, np.float32)).to(device), ids=ids)
+
+
+def build_ivf_index(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, shard: int = 0,
+                    device="cuda", chunk: int = 1 << 22):
+    """Unsharded IVF index of n base vectors (configs 2 and 4 on one GPU).
+    Returns the DeviceIndex, list sizes, and the row-ordered (codes, ids,
+    row_off) it was built from."""
+    rows, ids, row_off = ivf_rows(cfg, pq, coarse, n, device=device, chunk=chunk)
+    index = make_ivf_index(pq, coarse, rows, ids, row_off, device)
+    sizes = (row_off[1:] - row_off[:-1]).cpu().numpy()
+    return index, sizes, rows, ids, row_off
+
+
+def build_sharded_ivf_index(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, rank: int,
+                            world: int, prefix: int, device="cuda"):
+    """This rank's shard of an IVF index plus the GLOBAL prefix of every
+    list. Config 2: greedy list sharding, every rank draws the
+    whole base and keeps its lists. Config 4: range sharding, each rank
+    draws only its id range; the prefix heads move over NCCL
+    (shard.gather_prefix). Returns (index, rows, ids, row_off) of the
+    rank's part."""
+    import torch
+
+    from . import shard
+
+    if cfg.sharding == "lists":
+        rows, ids, row_off = ivf_rows(cfg, pq, coarse, n, device=device)
+        cnt = row_off[1:] - row_off[:-1]
+        need = torch.clamp(cnt, max=prefix)
+        prow, pid = shard.take_heads(rows, ids, row_off, need)
+        poff = torch.zeros_like(row_off)
+        poff[1:] = torch.cumsum(need, 0)
+        owner = torch.from_numpy(shard.assign_lists(cnt.cpu().numpy(), world)).to(device)
+        full_count = cnt
+        rows, ids, row_off = shard.keep_lists(rows, ids, row_off, owner == rank)
+    else:
+        rows, ids, row_off = ivf_rows(cfg, pq, coarse, n, device=device, rank=rank, world=world)
+        prow, pid, poff, full_count = shard.gather_prefix(rows, ids, row_off, prefix)
+    index = make_ivf_index(pq, coarse, rows, ids, row_off, device)
+    index.set_prefix(prow.contiguous(), poff, full_count.cpu().numpy(), ids=pid.contiguous())
+    return index, rows, ids, row_off

@@ -413,7 +413,7 @@ def test_probe_vs_oracle_many_sizes(gpu, K, ma):
 
 
 @pytest.mark.parametrize("K,ma,distinct", [(4096, 16, 4096), (4096, 64, 20), (1003, 8, 3),
-                                           (70000, 32, 70000)])
+                                           (70000, 32, 70000), (65536, 64, 65536)])
 def test_probe_batch_bounds_and_tie_fallback(gpu, K, ma, distinct):
     """Batched native probe (nq not a multiple of the 8-query CTA) against
     the oracle. `distinct` < K repeats centroids so that hundreds of cells

@@ -20,6 +20,8 @@ from paper_1704_07355_b200.workload import (CONFIGS, IVF_CONFIGS, build_ivf_inde
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 n = int(float(sys.argv[2])) if len(sys.argv) > 2 else None
 nq = int(float(sys.argv[3])) if len(sys.argv) > 3 else None
+import time
+t0 = time.perf_counter()
 ivf = IVF_CONFIGS.get(name)
 cfg = ivf or CONFIGS[name]
 n = n or cfg.n
@@ -31,6 +33,8 @@ else:
     pq = load_pq(cfg)
     index = build_shard_index(cfg, pq, n, 0, 1, prefix=max(cfg.init, cfg.R))[0]
     ma = 1
+torch.cuda.synchronize()
+print(f"model+index build {time.perf_counter() - t0:.1f} s", flush=True)
 qs = torch.from_numpy(queries(cfg, nq or cfg.q)).cuda()
 for _ in range(3):
     index.search(qs, cfg.R, ma=ma, init=cfg.init)
