@@ -427,29 +427,44 @@ def run_b200(args):
 
     # ---- roofline of the dominant kernel (the scan) ----
     peak = np.zeros(2, np.float64)
-    _native.check(_native.load_library().qadc_b200_int_peak(
-        peak.ctypes.data_as(_native._f64p)), "int_peak")
+    lib = _native.load_library()
+    _native.check(lib.qadc_b200_int_peak(peak.ctypes.data_as(_native._f64p)), "int_peak")
     scan_s = (sum(scan_us) / len(scan_us)) * 1e-6
-    lookups = (codes_scanned / args.steps) * pq.m  # per launch, this rank
-    achieved = lookups / scan_s / 1e9
+    pairs = codes_scanned / args.steps  # (query, code) pairs per launch, this rank
+    lookups = pairs * pq.m
     pk = measured_peaks()
     # codes of every DISTINCT list touched once per batch
     hbm_bytes = index.ncodes * pq.m / 2
-    roof = {
-        "bound": "int",
-        "achieved": round(achieved, 2),
-        "peak": round(peak[0] / 1e9, 2),
-        "unit": "G lookup-adds/s vs measured G int lane-instr/s (PRMT+IMAD dual-pipe microbench)",
-        "frac": round(achieved / (peak[0] / 1e9), 4),
+    int_view = {"achieved_G_lookups": round(lookups / scan_s / 1e9, 2),
+                "peak_G_lane_instr": round(peak[0] / 1e9, 2),
+                "frac": round(lookups / scan_s / peak[0], 4),
+                "alu_pipe_peak_G": round(peak[1] / 1e9, 2)}
+    if res.stats.get("scan_tc"):
+        # int8 tcgen05 one-hot GEMM: 16 m MACs (2 ops each) per (query, code)
+        # pair; achieved = useful ops / launch time vs the measured int8 rate
+        mma = np.zeros(1, np.float64)
+        _native.check(lib.qadc_b200_mma_peak(mma.ctypes.data_as(_native._f64p)), "mma_peak")
+        ops = pairs * 16 * pq.m * 2
+        roof = {"bound": "tensor", "achieved": round(ops / scan_s / 1e12, 2),
+                "peak": round(mma[0] / 1e12, 2),
+                "unit": "TOP/s int8 (one-hot MMA ops of the scanned pairs) vs measured "
+                        "tcgen05.mma.kind::i8 peak (qadc_b200_mma_peak)",
+                "frac": round(ops / scan_s / mma[0], 4),
+                "int_issue_view": int_view}
+    else:
+        roof = {"bound": "int", "achieved": int_view["achieved_G_lookups"],
+                "peak": int_view["peak_G_lane_instr"],
+                "unit": "G lookup-adds/s vs measured G int lane-instr/s (PRMT+IMAD dual-pipe microbench)",
+                "frac": int_view["frac"], "alu_pipe_peak_G": int_view["alu_pipe_peak_G"]}
+    roof.update({
         "traffic": ncu_traffic(),
         "scan_kernel_ms": round(scan_s * 1e3, 3),
-        "alu_pipe_peak_G": round(peak[1] / 1e9, 2),
         "hbm": {"bytes_alg_per_launch": int(hbm_bytes),
                 "achieved_gbs": round(hbm_bytes / scan_s / 1e9, 1),
                 "peak_gbs": pk.get("hbm_gbs"),
                 "frac": round(hbm_bytes / scan_s / 1e9 / pk.get("hbm_gbs", 6650.0), 4)},
         "scan_share_of_step": round(scan_s * 1e3 / ms_dev, 3),
-    }
+    })
 
     out = None
     if rank == 0:

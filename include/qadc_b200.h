@@ -144,7 +144,8 @@ QADC_API int64_t qadc_b200_index_bytes(const qadc_b200_index *idx);
  * adc.py:114-187 search(method="qadc") for nq queries at once:
  * probe (IVF) -> residual, rotation, float LUT -> qmax from the first
  * probed cell's first `init` codes -> per-cell qmin/delta and uint8 LUT ->
- * interleaved PRMT scan with streaming thresholds -> exact top-R by
+ * scan with streaming thresholds (int8 tcgen05 one-hot GEMM for m = 16, 32;
+ * interleaved PRMT lookups otherwise) -> exact top-R by
  * (distance, id). Outputs (nq, R) ids / fp32 midpoint distances sorted
  * ascending, padded with -1 / +inf, and out_n (nq) = result count.
  * With QADC_B200_LUT_IN, lut_in (nq, ma, m, 16) fp32 and cells_in (nq, ma)
@@ -152,7 +153,8 @@ QADC_API int64_t qadc_b200_index_bytes(const qadc_b200_index *idx);
  * stream is a cudaStream_t (NULL = legacy default stream).
  * stats (optional, 8 int64): [0] codes scanned, [1] scan candidates,
  * [2] overflow reruns, [3] scan kernel launches, [4] total kernel launches,
- * [5] scan kernel microseconds (event timed), rest reserved.
+ * [5] scan kernel microseconds (event timed), [6] 1 if the scan ran on the
+ * tensor cores, [7] reserved.
  */
 QADC_API int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries,
                            int nq, int R, int ma, int init, unsigned flags,
@@ -196,6 +198,11 @@ QADC_API int qadc_b200_encode(const float *X, int64_t n, int d, int m,
  * = sustained PRMT+IMAD lane-instructions/s (both integer-capable pipes),
  * out[1] = PRMT-only (ALU pipe) lane-instructions/s, on this device. */
 QADC_API int qadc_b200_int_peak(double *out);
+
+/* int8 tensor-core microbenchmark (roofline denominator of the tensor-core
+ * scan): out[0] = dense tcgen05.mma.kind::i8 ops/s (2 per MAC; M=128,
+ * N=256, K=32 instructions, one CTA per SM) on this device. */
+QADC_API int qadc_b200_mma_peak(double *out);
 
 /* kmeans.py:52-78 assign_batch: nearest of K centroids (K, d) per row of
  * X (n, d), einsum-order distances, ties to the lowest index. */

@@ -81,6 +81,8 @@ def _bind(lib):
                                                       _i64p]
     lib.qadc_b200_int_peak.restype = c_int
     lib.qadc_b200_int_peak.argtypes = [_f64p]
+    lib.qadc_b200_mma_peak.restype = c_int
+    lib.qadc_b200_mma_peak.argtypes = [_f64p]
     return lib
 
 

@@ -154,7 +154,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   const int m = idx->m;
   const int nslots = idx->K ? ma : 1;
   const int64_t npairs = (int64_t)nq * nslots;
-  const int qt_tile = scan_qt_per_cta(m);
+  const int qt_tile = scan_tile_queries(m);
   const int nl = idx->nlists;
 
   DevBuf<int64_t> cells_b;
@@ -804,7 +804,7 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
     stats[3] = ss.scan_launches;
     stats[4] = ss.launches;
     stats[5] = (int64_t)llround(ss.scan_us);
-    stats[6] = 0;
+    stats[6] = scan_use_tc(idx->m) ? 1 : 0;  // scan kernel: 1 = int8 tensor-core, 0 = PRMT
     stats[7] = 0;
   }
   return kOk;

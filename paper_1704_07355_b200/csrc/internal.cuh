@@ -143,6 +143,9 @@ struct ScanArgs {
 constexpr int kHistBins = 1024;                 // 32 coarse x 32 fine
 constexpr int kHistWords = kHistBins + 32;      // fine bins, then coarse sums
 int scan_qt_per_cta(int m);
+// Tensor-core scan in use for this m; queries per work item of the scan.
+bool scan_use_tc(int m);
+int scan_tile_queries(int m);
 // Resident scan CTAs on the device (occupancy x SMs) for this shape.
 int scan_resident_ctas(int m, int cap_l, int nsm, int linear);
 int scan_env_int(const char *name, int dflt);

@@ -93,47 +93,70 @@ __global__ void __launch_bounds__(kGemmQ * 32) k_probe_select(
   const float onep = __fadd_ru(1.f, gam), onem = __fsub_rd(1.f, gam);
   int nb = 0, bn = 0;
   uint64_t T = ~0ull;
-  for (int i0 = 0; i0 < K; i0 += 32) {
-    const int k = i0 + lane;
-    uint64_t key = ~0ull;
-    if (k < K) {
-      const float n2 = __fadd_ru(a2, cn2[k]);
-      const float A = __fmaf_rn(-2.f, Sq[k], __fadd_rn(a2, cn2[k]));
-      const float mg = __fmul_ru(eps, n2);
-      const float U = fmaxf(__fmul_ru(__fadd_ru(A, mg), onep), 0.f);
-      key = ((uint64_t)__float_as_uint(U) << 32) | (uint32_t)k;
+  // 8 rows of 32 cells per step: eight independent loads in flight per lane
+  // (the S rows stream from HBM; one dependent load per step would leave the
+  // kernel latency bound)
+  for (int i0 = 0; i0 < K; i0 += 256) {
+    float sv[8], cv[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int k = i0 + 32 * u + lane;
+      sv[u] = k < K ? __ldcs(Sq + k) : 0.f;
+      cv[u] = k < K ? cn2[k] : 0.f;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, key < T);
-    if (bal) {
-      if (bn + __popc(bal) > kSelBuf) warp_merge(v, nb, bn, ma, T);
-      const bool take = key < T;
-      const unsigned bal2 = __ballot_sync(0xffffffffu, take);
-      if (take) v[nb + bn + __popc(bal2 & ((1u << lane) - 1))] = key;
-      bn += __popc(bal2);
-      __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int k = i0 + 32 * u + lane;
+      uint64_t key = ~0ull;
+      if (k < K) {
+        const float n2 = __fadd_ru(a2, cv[u]);
+        const float A = __fmaf_rn(-2.f, sv[u], __fadd_rn(a2, cv[u]));
+        const float mg = __fmul_ru(eps, n2);
+        const float U = fmaxf(__fmul_ru(__fadd_ru(A, mg), onep), 0.f);
+        key = ((uint64_t)__float_as_uint(U) << 32) | (uint32_t)k;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, key < T);
+      if (bal) {
+        if (bn + __popc(bal) > kSelBuf) warp_merge(v, nb, bn, ma, T);
+        const bool take = key < T;
+        const unsigned bal2 = __ballot_sync(0xffffffffu, take);
+        if (take) v[nb + bn + __popc(bal2 & ((1u << lane) - 1))] = key;
+        bn += __popc(bal2);
+        __syncwarp();
+      }
     }
   }
   warp_merge(v, nb, bn, ma, T);
   const float Ustar = __uint_as_float((uint32_t)(v[min(ma, K) - 1] >> 32));
   int nc = 0;
   bool overflow = false;
-  for (int i0 = 0; i0 < K; i0 += 32) {
-    const int k = i0 + lane;
-    bool take = false;
-    if (k < K) {
-      const float n2 = __fadd_ru(a2, cn2[k]);
-      const float A = __fmaf_rn(-2.f, Sq[k], __fadd_rn(a2, cn2[k]));
-      const float mg = __fmul_ru(eps, n2);
-      const float L = fmaxf(__fmul_rd(__fsub_rd(A, mg), onem), 0.f);
-      take = L <= Ustar;
+  for (int i0 = 0; i0 < K && !overflow; i0 += 256) {
+    float sv[8], cv[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int k = i0 + 32 * u + lane;
+      sv[u] = k < K ? __ldcs(Sq + k) : 0.f;
+      cv[u] = k < K ? cn2[k] : 0.f;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, take);
-    if (nc + __popc(bal) > kGemmCand) {
-      overflow = true;
-      break;
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int k = i0 + 32 * u + lane;
+      bool take = false;
+      if (k < K) {
+        const float n2 = __fadd_ru(a2, cv[u]);
+        const float A = __fmaf_rn(-2.f, sv[u], __fadd_rn(a2, cv[u]));
+        const float mg = __fmul_ru(eps, n2);
+        const float L = fmaxf(__fmul_rd(__fsub_rd(A, mg), onem), 0.f);
+        take = L <= Ustar;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, take);
+      if (nc + __popc(bal) > kGemmCand) {
+        overflow = true;
+        break;
+      }
+      if (take) cq[nc + __popc(bal & ((1u << lane) - 1))] = (uint64_t)k;
+      nc += __popc(bal);
     }
-    if (take) cq[nc + __popc(bal & ((1u << lane) - 1))] = (uint64_t)k;
-    nc += __popc(bal);
   }
   __syncwarp();
   if (!overflow) {

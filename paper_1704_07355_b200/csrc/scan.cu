@@ -750,6 +750,381 @@ void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
   else launch_t<MC, QT, false>(a, nsm, st);
 }
 
+// ---- tensor-core scan (int8 tcgen05.mma) ----
+//
+// The lane sum of a code for a query is a dot product with a one-hot code:
+//   sum_j T_q[j][c_j] = onehot(c) . T_q,   onehot(c)[16 j + c_j] = 1,
+// exact in int32 (entries <= 127, m <= 32), and min(255, .) of it is the
+// reference's saturating byte sum (all entries are >= 0). A tile of 128 codes
+// is expanded by its threads into the A operand (128 x 16m bytes, K-major,
+// SMEM); the uint8 tables of the item's NQ queries are the resident B
+// operand (NQ x 16m, K-major, SMEM); one elected thread issues m/2
+// tcgen05.mma.kind::i8 (K = 32 each) into a TMEM accumulator (128 lanes x NQ
+// int32 columns) and commits to an mbarrier; every thread then reads its
+// code's NQ sums with tcgen05.ld and tests them against the queries'
+// thresholds. Survivors go straight to the per-query global candidate lists
+// (midpoint <= the global bound M), counted in the per-query midpoint
+// histogram whose R-th bucket tightens M (hist_bound) — the same selection
+// contract as k_scan. SMEM layout: canonical K-major, no swizzle: row r,
+// 16-byte column j at (r / 8) * 8K + 128 j + 16 (r % 8) (LBO = 128 B,
+// SBO = 8K B).
+constexpr int kTcCodes = 128;  // codes per tile (MMA M)
+constexpr int kTcNQ = 128;     // queries per item (max MMA N)
+constexpr int kStage = 32;     // staged survivors per query per CTA
+
+__device__ __forceinline__ uint64_t tc_smem_desc(uint32_t saddr, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tTC_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra TC_DONE;\n\tbra TC_WAIT;\n\tTC_DONE:\n\t}" ::"r"(mbar),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TcSmem {
+  uint64_t mbar[2];
+  uint32_t tmem;
+  int item;
+  int query[kTcNQ];
+  float qmin[kTcNQ];
+  float delta[kTcNQ];
+  float hinv[kTcNQ];
+  __align__(16) int thr[kTcNQ];
+  unsigned mc[kTcNQ];   // cached global bound M (bits)
+  int pend[kTcNQ];      // appended since this CTA last read the histogram bound
+  int scnt[kTcNQ];      // staged survivors
+  uint32_t stage[kTcNQ][kStage];  // (lane sum << 24) | code index within the item
+};
+// one instance per CTA of k_scan_tc (file-scope: direct shared addressing
+// from every helper)
+__shared__ TcSmem g_tc;
+
+// Global append of one candidate.
+__device__ __forceinline__ void tc_put(const ScanArgs &a, int q, float mid, int64_t code_pos,
+                                       unsigned slot) {
+  const int query = g_tc.query[q];
+  if (slot < (unsigned)a.cap_g) {
+    const size_t o = (size_t)query * a.cap_g + slot;
+    a.cand_mid[o] = mid;
+    a.cand_id[o] = a.ids[code_pos];
+  }
+  const float hinv = g_tc.hinv[q];
+  if (hinv > 0.f) {
+    unsigned *h = a.hist + (size_t)query * kHistWords;
+    const int b = min((int)__fmul_rn(mid, hinv), kHistBins - 1);
+    atomicAdd(&h[b], 1u);
+    atomicAdd(&h[kHistBins + (b >> 5)], 1u);
+  }
+}
+
+// Survivor of the epilogue: staged in shared memory (no global round trip
+// on the tile's critical path); a full stage falls back to a direct append.
+__device__ __noinline__ void tc_hit(const ScanArgs &a, int q, int v, int64_t chunk0, int ci) {
+  const float mid = midpoint(g_tc.qmin[q], g_tc.delta[q], v);
+  if (!(mid <= __uint_as_float(g_tc.mc[q]))) return;
+  const int k = atomicAdd(&g_tc.scnt[q], 1);
+  if (k < kStage) {
+    g_tc.stage[q][k] = ((uint32_t)v << 24) | (uint32_t)ci;
+    return;
+  }
+  const unsigned slot = atomicAdd(&a.cand_n[g_tc.query[q]], 1u);
+  tc_put(a, q, mid, chunk0 * kChunkCodes + ci, slot);
+  atomicAdd(&g_tc.pend[q], 1);
+}
+
+// Warp: move query slot q's staged survivors to its global candidate list
+// (one slot claim per flush).
+__device__ __forceinline__ void tc_flush(const ScanArgs &a, int q, int64_t chunk0) {
+  const int lane = threadIdx.x & 31;
+  const int n = min(g_tc.scnt[q], kStage);
+  unsigned base = 0;
+  if (lane == 0) base = atomicAdd(&a.cand_n[g_tc.query[q]], (unsigned)n);
+  base = __shfl_sync(kFull, base, 0);
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t e = g_tc.stage[q][i];
+    const float mid = midpoint(g_tc.qmin[q], g_tc.delta[q], (int)(e >> 24));
+    tc_put(a, q, mid, chunk0 * kChunkCodes + (e & 0xffffffu), base + i);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    g_tc.scnt[q] = 0;
+    g_tc.pend[q] += n;
+  }
+  __syncwarp();
+}
+
+// Expand sub-quantizers [j0, j0 + MH) of the code in A row `row` (code c
+// of its chunk) into A.
+template <int MC, int MH>
+__device__ __forceinline__ void tc_expand(uint8_t *sA, int row, int j0, const uint32_t (&cw)[MH],
+                                          int c) {
+  constexpr int SBO = 8 * 16 * MC;
+  uint8_t *arow = sA + (row >> 3) * SBO + (row & 7) * 16 + j0 * 128;
+  const int sh = 4 * (c & 7);
+#pragma unroll
+  for (int j = 0; j < MH; j++) {
+    const uint32_t cj = (cw[j] >> sh) & 15u;
+    const uint32_t bit = 1u << ((cj & 3u) << 3);
+    const uint32_t wsel = cj >> 2;
+    uint4 oh;
+    oh.x = wsel == 0 ? bit : 0u;
+    oh.y = wsel == 1 ? bit : 0u;
+    oh.z = wsel == 2 ? bit : 0u;
+    oh.w = wsel == 3 ? bit : 0u;
+    *(uint4 *)(arow + j * 128) = oh;
+  }
+}
+
+template <int MC, int MH>
+__device__ __forceinline__ void tc_load(const ScanArgs &a, int64_t g, int c, int j0,
+                                        uint32_t (&cw)[MH], uint32_t &vb) {
+  const uint32_t *p = a.codes + ((size_t)g * MC + j0) * 32 + (c >> 3);
+#pragma unroll
+  for (int j = 0; j < MH; j++) cw[j] = __ldg(p + j * 32);
+  vb = __ldg(a.valid + g * 32 + (c >> 3));
+}
+
+// 8 warps: warps w and w + 4 share TMEM lane quarter w % 4 (codes
+// 32 (w % 4) .. + 31 of the tile); warp half h = w / 4 expands sub-quantizers
+// [h m/2, (h + 1) m/2) and reads query columns 32 k with k % 2 == h.
+// Software pipeline per item: while the tensor cores run tile t + 1 (A and D
+// double-buffered), the threads read tile t's sums (epilogue) and expand
+// tile t + 2.
+template <int MC>
+__global__ void __launch_bounds__(256, 1) k_scan_tc(const __grid_constant__ ScanArgs a) {
+  constexpr int K = 16 * MC, SBO = 8 * K, MH = MC / 2;
+  constexpr uint32_t kCols = 2 * kTcNQ;
+  extern __shared__ __align__(16) unsigned char dsm[];  // no-swizzle operands: 16 B alignment
+  TcSmem &s = g_tc;
+  uint8_t *sB = dsm;                       // [kTcNQ][K]
+  uint8_t *sA0 = dsm + kTcNQ * K;          // [2][128][K]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int row = tid & 127, half = tid >> 7, j0 = half * MH;
+  const uint32_t sB_a = (uint32_t)__cvta_generic_to_shared(sB);
+  const uint32_t sA_a = (uint32_t)__cvta_generic_to_shared(sA0);
+  const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(&s.mbar[0]);
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s.tmem)),
+                 "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar0 + 8));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    s.item = atomicAdd(a.item_counter, 1);
+  }
+  if (tid < kTcNQ) s.scnt[tid] = 0;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = s.tmem;
+  const uint32_t t_row = tmem + ((uint32_t)((w & 3) * 32) << 16);
+  const int n_items = *a.n_items;
+  uint32_t ph0 = 0, ph1 = 0;
+  for (;;) {
+    const int item = s.item;
+    if (item >= n_items) break;
+    const WorkItem it = a.items[item];
+    const int nq = it.pair_count;
+    // ---- stage the item's tables (B operand) and per-query state ----
+    for (int e = tid; e < kTcNQ * MC; e += 256) {
+      const int q = e / MC, j = e - q * MC;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (q < nq) v = ((const uint4 *)a.qt)[(size_t)a.pair_t[it.pair_begin + q] * MC + j];
+      *(uint4 *)(sB + (q >> 3) * SBO + j * 128 + (q & 7) * 16) = v;
+    }
+    if (tid < kTcNQ) {
+      const int q = tid;
+      int thr = -1;
+      unsigned mb = 0;
+      if (q < nq) {
+        const int pi = it.pair_begin + q;
+        const int query = a.pair_q[pi], t = a.pair_t[pi];
+        s.query[q] = query;
+        s.qmin[q] = a.qmin_f[t];
+        s.delta[q] = a.delta_f[t];
+        const float hw = a.hist_w[query];
+        s.hinv[q] = hw > 0.f ? __frcp_rn(hw) : 0.f;
+        mb = *(volatile unsigned *)&a.M_bits[query];
+        thr = q_threshold(__uint_as_float(mb), s.qmin[q], s.delta[q]);
+      } else {
+        s.query[q] = 0;
+        s.qmin[q] = 0.f;
+        s.delta[q] = 0.f;
+        s.hinv[q] = 0.f;
+      }
+      s.thr[q] = thr;
+      s.mc[q] = mb;
+      s.pend[q] = 0;
+    }
+    const int n_mma = max(16, (nq + 15) & ~15);  // MMA N: the item's queries, rounded to 16
+    const uint32_t idesc = (2u << 4) | ((uint32_t)(n_mma >> 3) << 17) | ((uint32_t)(kTcCodes >> 4) << 24);
+    const int64_t c0g = it.chunk_begin;
+    const int64_t ntiles = 2 * (it.chunk_end - it.chunk_begin);
+    uint32_t cw[MH], vb_next = 0, vb = 0;
+    // prologue: expand tile 0 into A[0], load tile 1's words
+    tc_load<MC, MH>(a, c0g, row, j0, cw, vb_next);
+    tc_expand<MC, MH>(sA0, row, j0, cw, row);
+    vb = vb_next;
+    if (ntiles > 1) tc_load<MC, MH>(a, c0g, kTcCodes + row, j0, cw, vb_next);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (tid == 0) s.item = atomicAdd(a.item_counter, 1);  // claimed ahead
+    auto issue = [&](int64_t t) {
+      const int buf = (int)(t & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int ks = 0; ks < K / 32; ks++) {
+        const uint64_t da = tc_smem_desc(sA_a + buf * 128 * K + ks * 256, SBO);
+        const uint64_t db = tc_smem_desc(sB_a + ks * 256, SBO);
+        const uint32_t acc = ks > 0 ? 1u : 0u;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + buf * kTcNQ),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+              mbar0 + 8 * buf)
+          : "memory");
+    };
+    if (tid == 0) issue(0);
+    for (int64_t t = 0; t < ntiles; t++) {
+      const uint32_t vbt = vb;  // valid byte of tile t's octet
+      // ---- expand tile t + 1 into A[(t + 1) & 1] and start its MMA ----
+      if (t + 1 < ntiles) {
+        tc_expand<MC, MH>(sA0 + (size_t)((t + 1) & 1) * 128 * K, row, j0, cw,
+                          (int)((t + 1) & 1) * kTcCodes + row);
+        vb = vb_next;
+        if (t + 2 < ntiles)
+          tc_load<MC, MH>(a, c0g + ((t + 2) >> 1), (int)((t + 2) & 1) * kTcCodes + row, j0, cw,
+                          vb_next);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      if (t + 1 < ntiles && tid == 0) issue(t + 1);
+      // ---- flushes and bounds for the survivors staged so far (one lane per
+      // query decides, the warp serves the flagged queries) ----
+      if (w < 4) {
+        const int q = tid;
+        const bool fl = q < nq && s.scnt[q] >= kStage / 2;
+        const bool bd = q < nq && s.pend[q] >= a.bound_every;
+        unsigned mf = __ballot_sync(kFull, fl), mbd = __ballot_sync(kFull, bd);
+        while (mf) {
+          const int qq = w * 32 + __ffs(mf) - 1;
+          mf &= mf - 1;
+          tc_flush(a, qq, c0g);
+          if (g_tc.pend[qq] >= a.bound_every) mbd |= 1u << (qq & 31);
+        }
+        while (mbd) {
+          const int qq = w * 32 + __ffs(mbd) - 1;
+          mbd &= mbd - 1;
+          const unsigned mb = hist_bound(a, s.query[qq]);
+          if (lane == 0) {
+            s.pend[qq] = 0;
+            if (mb < s.mc[qq]) {
+              atomicMin(&a.M_bits[s.query[qq]], mb);
+              s.mc[qq] = mb;
+              const int th = q_threshold(__uint_as_float(mb), s.qmin[qq], s.delta[qq]);
+              if (th < s.thr[qq]) s.thr[qq] = th;
+            }
+          }
+          __syncwarp();
+        }
+      }
+      unsigned mpre = 0;
+      if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];  // lands during the wait
+      __syncthreads();  // flushes reset s.scnt: no tc_hit of this tile may interleave
+      // ---- epilogue of tile t ----
+      const int buf = (int)(t & 1);
+      tc_wait(mbar0 + 8 * buf, buf ? ph1 : ph0);
+      if (buf) ph1 ^= 1; else ph0 ^= 1;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int c = buf * kTcCodes + row;
+      const bool valid = (vbt >> (c & 7)) & 1u;
+      const int ci = (int)(t >> 1) * kChunkCodes + c;
+      for (int q0 = half * 32; q0 < nq; q0 += 64) {
+        uint32_t v[32];
+        tc_ld32(t_row + buf * kTcNQ + q0, v);
+        int mn = 1;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const int4 t4 = *(const int4 *)&s.thr[q0 + i];
+          mn = min(mn, min(min((int)v[i] - t4.x, (int)v[i + 1] - t4.y),
+                           min((int)v[i + 2] - t4.z, (int)v[i + 3] - t4.w)));
+        }
+        if (valid && mn <= 0) {  // rare once the bounds converge; static indices keep v[] in registers
+#pragma unroll
+          for (int i = 0; i < 32; i++)
+            if ((int)v[i] <= s.thr[q0 + i]) tc_hit(a, q0 + i, (int)v[i], c0g, ci);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      if (tid < nq && mpre < s.mc[tid]) {
+        s.mc[tid] = mpre;
+        const int th = q_threshold(__uint_as_float(mpre), s.qmin[tid], s.delta[tid]);
+        if (th < s.thr[tid]) s.thr[tid] = th;
+      }
+    }
+    __syncthreads();
+    if (w < 4) {
+      unsigned mf = __ballot_sync(kFull, tid < nq && s.scnt[tid] > 0);
+      while (mf) {
+        const int qq = w * 32 + __ffs(mf) - 1;
+        mf &= mf - 1;
+        tc_flush(a, qq, c0g);
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (w == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+}
+
+template <int MC>
+size_t tc_smem_bytes() { return (size_t)(kTcNQ + 2 * kTcCodes) * 16 * MC; }
+
+template <int MC>
+int tc_resident(int nsm) {
+  const size_t smem = tc_smem_bytes<MC>();
+  cudaFuncSetAttribute(k_scan_tc<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_scan_tc<MC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_tc<MC>, 256, smem);
+  // TMEM: every resident CTA holds 2 kTcNQ columns of the SM's 512
+  per_sm = std::min(std::max(per_sm, 1), 512 / (2 * kTcNQ));
+  return nsm * per_sm;
+}
+
+template <int MC>
+void launch_tc(const ScanArgs &a, int nsm, cudaStream_t st) {
+  const int grid = tc_resident<MC>(nsm);
+  k_scan_tc<MC><<<grid, 256, tc_smem_bytes<MC>(), st>>>(a);
+}
+
 // ---- work list construction ----
 
 __global__ void k_count_pairs(const int64_t *__restrict__ cells, int npairs, int nslots,
@@ -973,7 +1348,21 @@ int scan_qt_per_cta(int m) {
   return m <= 64 ? 8 : 4;
 }
 
+// Tensor-core scan for m in {16, 32} (QADC_B200_TC=0 selects the PRMT
+// kernel).
+bool scan_use_tc(int m) {
+  static const int env = scan_env_int("QADC_B200_TC", 1);
+  return env != 0 && (m == 16 || m == 32);
+}
+
+int scan_tile_queries(int m) { return scan_use_tc(m) ? kTcNQ : scan_qt_per_cta(m); }
+
 void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st) {
+  if (scan_use_tc(a.m)) {
+    if (a.m == 32) launch_tc<32>(a, nsm, st);
+    else launch_tc<16>(a, nsm, st);
+    return;
+  }
   const int qt = scan_qt_per_cta(a.m);
   if (qt == 16) {
     if (a.m == 32) launch_t<32, 16>(a, nsm, st);
@@ -990,6 +1379,7 @@ void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st) {
 }
 
 int scan_resident_ctas(int m, int cap_l, int nsm, int linear) {
+  if (scan_use_tc(m)) return m == 32 ? tc_resident<32>(nsm) : tc_resident<16>(nsm);
   const int qt = scan_qt_per_cta(m);
   const bool lin = linear != 0;
   if (qt == 16) {

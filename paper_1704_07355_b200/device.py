@@ -138,7 +138,7 @@ class DeviceIndex:
                 _native.dptr(cells_d), _native.dptr(ids), _native.dptr(dist), _native.dptr(cnt),
                 st.cuda_stream, stats.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
         _native.check(rc, "search_batch")
-        keys = ("codes", "candidates", "reruns", "scan_launches", "launches", "scan_us")
+        keys = ("codes", "candidates", "reruns", "scan_launches", "launches", "scan_us", "scan_tc")
         return BatchResult(ids, dist, cnt, {k: int(v) for k, v in zip(keys, stats)})
 
     @property

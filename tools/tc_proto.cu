@@ -72,11 +72,14 @@ __global__ void __launch_bounds__(128) k_tc(const uint4 *__restrict__ rows, int6
   uint32_t phase = 0;
   unsigned long long acc = 0;
   const int64_t ntiles = (n + kM - 1) / kM;
+  uint4 nxt = make_uint4(0, 0, 0, 0);
+  if (blockIdx.x * kM + tid < n) nxt = rows[blockIdx.x * kM + tid];
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t code = t * kM + tid;
     // one-hot expansion of this thread's code into A row `tid`
-    uint4 rw = make_uint4(0, 0, 0, 0);
-    if (code < n) rw = rows[code * (M_SUB / 32 > 0 ? M_SUB / 32 : 1)];
+    const uint4 rw = nxt;
+    const int64_t cn = (t + gridDim.x) * kM + tid;
+    if (cn < n) nxt = rows[cn];
     const uint32_t wd[4] = {rw.x, rw.y, rw.z, rw.w};
     uint8_t *arow = sA + (tid >> 3) * SBO + (tid & 7) * 16;
 #pragma unroll
@@ -149,10 +152,22 @@ __global__ void __launch_bounds__(128) k_tc(const uint4 *__restrict__ rows, int6
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
 }
 
+template <int M_SUB, int NQ>
+int run(bool check, int64_t n);
+
 int main(int argc, char **argv) {
   const bool check = argc > 1 && argv[1][0] == 'c';
   const int64_t n = check ? 5000 : (argc > 2 ? atoll(argv[2]) : 10000000);
-  constexpr int M_SUB = 32, NQ = 64;
+  constexpr int M_SUB = 32;
+  const int nqa = argc > 3 ? atoi(argv[3]) : 64;
+  if (nqa == 128) return run<M_SUB, 128>(check, n);
+  if (nqa == 256) return run<M_SUB, 256>(check, n);
+  if (nqa == 32) return run<M_SUB, 32>(check, n);
+  return run<M_SUB, 64>(check, n);
+}
+
+template <int M_SUB, int NQ>
+int run(bool check, int64_t n) {
   const int K = 16 * M_SUB;
   std::vector<uint8_t> rows(n * (M_SUB / 2)), tab(NQ * K);
   srand(1);
@@ -197,6 +212,7 @@ int main(int argc, char **argv) {
   }
   auto kern = k_tc<M_SUB, NQ, false>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
   printf("smem %zu B, %d CTAs/SM\n", smem, per_sm);
