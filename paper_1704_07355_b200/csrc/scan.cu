@@ -770,7 +770,7 @@ void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
 // SBO = 8K B).
 constexpr int kTcCodes = 128;  // codes per tile (MMA M)
 constexpr int kTcNQ = 128;     // queries per item (max MMA N)
-constexpr int kStage = 32;     // staged survivors per query per CTA
+constexpr int kRing = 1024;    // survivor ring between the compute warps and the flusher warp
 
 __device__ __forceinline__ uint64_t tc_smem_desc(uint32_t saddr, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
@@ -799,76 +799,132 @@ __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+struct TcEntry {
+  float mid;
+  int query;     // -1: slot free
+  int64_t pos;   // code position (chunk * 256 + code)
+};
+
 struct TcSmem {
   uint64_t mbar[2];
   uint32_t tmem;
   int item;
+  int done;
+  unsigned head;  // ring slots reserved (monotone)
+  unsigned tail;  // ring slots consumed by the flusher (monotone)
   int query[kTcNQ];
   float qmin[kTcNQ];
   float delta[kTcNQ];
-  float hinv[kTcNQ];
   __align__(16) int thr[kTcNQ];
-  unsigned mc[kTcNQ];   // cached global bound M (bits)
-  int pend[kTcNQ];      // appended since this CTA last read the histogram bound
-  int scnt[kTcNQ];      // staged survivors
-  uint32_t stage[kTcNQ][kStage];  // (lane sum << 24) | code index within the item
+  unsigned mc[kTcNQ];  // cached global bound M (bits)
+  TcEntry ring[kRing];
 };
 // one instance per CTA of k_scan_tc (file-scope: direct shared addressing
 // from every helper)
 __shared__ TcSmem g_tc;
 
-// Global append of one candidate.
-__device__ __forceinline__ void tc_put(const ScanArgs &a, int q, float mid, int64_t code_pos,
+// Global append of one candidate (its slot already claimed).
+__device__ __forceinline__ void tc_put(const ScanArgs &a, int query, float mid, int64_t pos,
                                        unsigned slot) {
-  const int query = g_tc.query[q];
   if (slot < (unsigned)a.cap_g) {
     const size_t o = (size_t)query * a.cap_g + slot;
     a.cand_mid[o] = mid;
-    a.cand_id[o] = a.ids[code_pos];
+    a.cand_id[o] = a.ids[pos];
   }
-  const float hinv = g_tc.hinv[q];
-  if (hinv > 0.f) {
+  const float hw = a.hist_w[query];
+  if (hw > 0.f) {
     unsigned *h = a.hist + (size_t)query * kHistWords;
-    const int b = min((int)__fmul_rn(mid, hinv), kHistBins - 1);
+    const int b = min((int)__fmul_rn(mid, __frcp_rn(hw)), kHistBins - 1);
     atomicAdd(&h[b], 1u);
     atomicAdd(&h[kHistBins + (b >> 5)], 1u);
   }
 }
 
-// Survivor of the epilogue: staged in shared memory (no global round trip
-// on the tile's critical path); a full stage falls back to a direct append.
-__device__ __noinline__ void tc_hit(const ScanArgs &a, int q, int v, int64_t chunk0, int ci) {
+// Survivor of the epilogue: pushed to the shared-memory ring drained by the
+// flusher warp (no global round trip on the tile's critical path). Each
+// thread checks the ring's room before reserving and has at most one
+// reservation in flight, so 256 slots of slack make the reservation safe; a
+// full ring falls back to a direct append.
+__device__ __noinline__ void tc_hit(const ScanArgs &a, int q, int v, int64_t pos) {
   const float mid = midpoint(g_tc.qmin[q], g_tc.delta[q], v);
   if (!(mid <= __uint_as_float(g_tc.mc[q]))) return;
-  const int k = atomicAdd(&g_tc.scnt[q], 1);
-  if (k < kStage) {
-    g_tc.stage[q][k] = ((uint32_t)v << 24) | (uint32_t)ci;
+  const int query = g_tc.query[q];
+  const unsigned h = *(volatile unsigned *)&g_tc.head, t = *(volatile unsigned *)&g_tc.tail;
+  if (h - t < (unsigned)(kRing - 256)) {
+    const unsigned k = atomicAdd(&g_tc.head, 1u);
+    TcEntry &e = g_tc.ring[k % kRing];
+    e.mid = mid;
+    e.pos = pos;
+    __threadfence_block();
+    *(volatile int *)&e.query = query;
     return;
   }
-  const unsigned slot = atomicAdd(&a.cand_n[g_tc.query[q]], 1u);
-  tc_put(a, q, mid, chunk0 * kChunkCodes + ci, slot);
-  atomicAdd(&g_tc.pend[q], 1);
+  tc_put(a, query, mid, pos, atomicAdd(&a.cand_n[query], 1u));
 }
 
-// Warp: move query slot q's staged survivors to its global candidate list
-// (one slot claim per flush).
-__device__ __forceinline__ void tc_flush(const ScanArgs &a, int q, int64_t chunk0) {
+// Flusher warp: drains the ring into the global candidate lists (4 entries
+// per lane per round, their slot claims in flight together) and tightens the
+// global bound M of a query from the histogram every bound_every appends.
+__device__ __forceinline__ void tc_flusher(const ScanArgs &a) {
   const int lane = threadIdx.x & 31;
-  const int n = min(g_tc.scnt[q], kStage);
-  unsigned base = 0;
-  if (lane == 0) base = atomicAdd(&a.cand_n[g_tc.query[q]], (unsigned)n);
-  base = __shfl_sync(kFull, base, 0);
-  for (int i = lane; i < n; i += 32) {
-    const uint32_t e = g_tc.stage[q][i];
-    const float mid = midpoint(g_tc.qmin[q], g_tc.delta[q], (int)(e >> 24));
-    tc_put(a, q, mid, chunk0 * kChunkCodes + (e & 0xffffffu), base + i);
+  unsigned tail = 0;
+  for (;;) {
+    const unsigned head = *(volatile unsigned *)&g_tc.head;
+    if (head == tail) {
+      if (*(volatile int *)&g_tc.done && *(volatile unsigned *)&g_tc.head == tail) break;
+      __nanosleep(200);
+      continue;
+    }
+    const unsigned n = min(head - tail, 128u);
+    TcEntry e[4];
+    unsigned slot[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      e[r].query = -1;
+      const unsigned i = (unsigned)(r * 32 + lane);
+      if (i < n) {
+        volatile TcEntry *ve = &g_tc.ring[(tail + i) % kRing];
+        int qy;
+        while ((qy = ve->query) < 0) {
+        }
+        __threadfence_block();
+        e[r].query = qy;
+        e[r].mid = ve->mid;
+        e[r].pos = ve->pos;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+      if (e[r].query >= 0) slot[r] = atomicAdd(&a.cand_n[e[r].query], 1u);
+    unsigned bound_lanes = 0;
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      const bool has = e[r].query >= 0;
+      if (has) {
+        tc_put(a, e[r].query, e[r].mid, e[r].pos, slot[r]);
+        g_tc.ring[(tail + r * 32 + lane) % kRing].query = -1;
+      }
+      const bool bnd = has && (slot[r] + 1) % (unsigned)a.bound_every == 0;
+      bound_lanes |= __ballot_sync(kFull, bnd) ? (1u << r) : 0u;
+    }
+    __syncwarp();
+    __threadfence_block();  // freed slots (query = -1) visible before the new tail
+    tail += n;
+    if (lane == 0) *(volatile unsigned *)&g_tc.tail = tail;
+    // bound refresh for the queries that crossed a multiple of bound_every
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      if (!(bound_lanes >> r & 1u)) continue;
+      unsigned mq = __ballot_sync(kFull, e[r].query >= 0 && (slot[r] + 1) % (unsigned)a.bound_every == 0);
+      while (mq) {
+        const int src = __ffs(mq) - 1;
+        mq &= mq - 1;
+        const int query = __shfl_sync(kFull, e[r].query, src);
+        const unsigned mb = hist_bound(a, query);
+        if (lane == 0) atomicMin(&a.M_bits[query], mb);
+      }
+    }
   }
-  __syncwarp();
-  if (lane == 0) {
-    g_tc.scnt[q] = 0;
-    g_tc.pend[q] += n;
-  }
-  __syncwarp();
 }
 
 // Expand sub-quantizers [j0, j0 + MH) of the code in A row `row` (code c
@@ -902,22 +958,24 @@ __device__ __forceinline__ void tc_load(const ScanArgs &a, int64_t g, int c, int
   vb = __ldg(a.valid + g * 32 + (c >> 3));
 }
 
-// 8 warps: warps w and w + 4 share TMEM lane quarter w % 4 (codes
-// 32 (w % 4) .. + 31 of the tile); warp half h = w / 4 expands sub-quantizers
-// [h m/2, (h + 1) m/2) and reads query columns 32 k with k % 2 == h.
-// Software pipeline per item: while the tensor cores run tile t + 1 (A and D
-// double-buffered), the threads read tile t's sums (epilogue) and expand
-// tile t + 2.
+__device__ __forceinline__ void tc_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// 9 warps. Warps 0-7 compute: warps w and w + 4 share TMEM lane quarter
+// w % 4 (codes 32 (w % 4) .. + 31 of the tile); warp half h = w / 4 expands
+// sub-quantizers [h m/2, (h + 1) m/2) and reads query columns 32 k with
+// k % 2 == h. Software pipeline per item: while the tensor cores run tile
+// t + 1 (A and D double-buffered), the compute warps read tile t's sums and
+// expand tile t + 2. Warp 8 drains the survivor ring (tc_flusher).
 template <int MC>
-__global__ void __launch_bounds__(256, 1) k_scan_tc(const __grid_constant__ ScanArgs a) {
+__global__ void __launch_bounds__(288, 1) k_scan_tc(const __grid_constant__ ScanArgs a) {
   constexpr int K = 16 * MC, SBO = 8 * K, MH = MC / 2;
   constexpr uint32_t kCols = 2 * kTcNQ;
   extern __shared__ __align__(16) unsigned char dsm[];  // no-swizzle operands: 16 B alignment
   TcSmem &s = g_tc;
   uint8_t *sB = dsm;                       // [kTcNQ][K]
   uint8_t *sA0 = dsm + kTcNQ * K;          // [2][128][K]
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int row = tid & 127, half = tid >> 7, j0 = half * MH;
+  const int tid = threadIdx.x, w = tid >> 5;
+  const int row = tid & 127, half = (tid >> 7) & 1, j0 = half * MH;
   const uint32_t sB_a = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_a = (uint32_t)__cvta_generic_to_shared(sA0);
   const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(&s.mbar[0]);
@@ -932,11 +990,17 @@ __global__ void __launch_bounds__(256, 1) k_scan_tc(const __grid_constant__ Scan
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar0 + 8));
     asm volatile("fence.mbarrier_init.release.cluster;");
     s.item = atomicAdd(a.item_counter, 1);
+    s.done = 0;
+    s.head = 0;
+    s.tail = 0;
   }
-  if (tid < kTcNQ) s.scnt[tid] = 0;
+  for (int i = tid; i < kRing; i += blockDim.x) s.ring[i].query = -1;
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
+  if (w == 8) {
+    tc_flusher(a);
+  } else {
   const uint32_t tmem = s.tmem;
   const uint32_t t_row = tmem + ((uint32_t)((w & 3) * 32) << 16);
   const int n_items = *a.n_items;
@@ -963,19 +1027,15 @@ __global__ void __launch_bounds__(256, 1) k_scan_tc(const __grid_constant__ Scan
         s.query[q] = query;
         s.qmin[q] = a.qmin_f[t];
         s.delta[q] = a.delta_f[t];
-        const float hw = a.hist_w[query];
-        s.hinv[q] = hw > 0.f ? __frcp_rn(hw) : 0.f;
         mb = *(volatile unsigned *)&a.M_bits[query];
         thr = q_threshold(__uint_as_float(mb), s.qmin[q], s.delta[q]);
       } else {
         s.query[q] = 0;
         s.qmin[q] = 0.f;
         s.delta[q] = 0.f;
-        s.hinv[q] = 0.f;
       }
       s.thr[q] = thr;
       s.mc[q] = mb;
-      s.pend[q] = 0;
     }
     const int n_mma = max(16, (nq + 15) & ~15);  // MMA N: the item's queries, rounded to 16
     const uint32_t idesc = (2u << 4) | ((uint32_t)(n_mma >> 3) << 17) | ((uint32_t)(kTcCodes >> 4) << 24);
@@ -989,7 +1049,7 @@ __global__ void __launch_bounds__(256, 1) k_scan_tc(const __grid_constant__ Scan
     if (ntiles > 1) tc_load<MC, MH>(a, c0g, kTcCodes + row, j0, cw, vb_next);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    tc_bar();
     if (tid == 0) s.item = atomicAdd(a.item_counter, 1);  // claimed ahead
     auto issue = [&](int64_t t) {
       const int buf = (int)(t & 1);
@@ -1012,6 +1072,8 @@ __global__ void __launch_bounds__(256, 1) k_scan_tc(const __grid_constant__ Scan
     if (tid == 0) issue(0);
     for (int64_t t = 0; t < ntiles; t++) {
       const uint32_t vbt = vb;  // valid byte of tile t's octet
+      unsigned mpre = 0;
+      if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];  // lands during the wait
       // ---- expand tile t + 1 into A[(t + 1) & 1] and start its MMA ----
       if (t + 1 < ntiles) {
         tc_expand<MC, MH>(sA0 + (size_t)((t + 1) & 1) * 128 * K, row, j0, cw,
@@ -1023,40 +1085,8 @@ __global__ void __launch_bounds__(256, 1) k_scan_tc(const __grid_constant__ Scan
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();
+      tc_bar();
       if (t + 1 < ntiles && tid == 0) issue(t + 1);
-      // ---- flushes and bounds for the survivors staged so far (one lane per
-      // query decides, the warp serves the flagged queries) ----
-      if (w < 4) {
-        const int q = tid;
-        const bool fl = q < nq && s.scnt[q] >= kStage / 2;
-        const bool bd = q < nq && s.pend[q] >= a.bound_every;
-        unsigned mf = __ballot_sync(kFull, fl), mbd = __ballot_sync(kFull, bd);
-        while (mf) {
-          const int qq = w * 32 + __ffs(mf) - 1;
-          mf &= mf - 1;
-          tc_flush(a, qq, c0g);
-          if (g_tc.pend[qq] >= a.bound_every) mbd |= 1u << (qq & 31);
-        }
-        while (mbd) {
-          const int qq = w * 32 + __ffs(mbd) - 1;
-          mbd &= mbd - 1;
-          const unsigned mb = hist_bound(a, s.query[qq]);
-          if (lane == 0) {
-            s.pend[qq] = 0;
-            if (mb < s.mc[qq]) {
-              atomicMin(&a.M_bits[s.query[qq]], mb);
-              s.mc[qq] = mb;
-              const int th = q_threshold(__uint_as_float(mb), s.qmin[qq], s.delta[qq]);
-              if (th < s.thr[qq]) s.thr[qq] = th;
-            }
-          }
-          __syncwarp();
-        }
-      }
-      unsigned mpre = 0;
-      if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];  // lands during the wait
-      __syncthreads();  // flushes reset s.scnt: no tc_hit of this tile may interleave
       // ---- epilogue of tile t ----
       const int buf = (int)(t & 1);
       tc_wait(mbar0 + 8 * buf, buf ? ph1 : ph0);
@@ -1064,7 +1094,7 @@ __global__ void __launch_bounds__(256, 1) k_scan_tc(const __grid_constant__ Scan
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int c = buf * kTcCodes + row;
       const bool valid = (vbt >> (c & 7)) & 1u;
-      const int ci = (int)(t >> 1) * kChunkCodes + c;
+      const int64_t pos = (c0g + (t >> 1)) * kChunkCodes + c;
       for (int q0 = half * 32; q0 < nq; q0 += 64) {
         uint32_t v[32];
         tc_ld32(t_row + buf * kTcNQ + q0, v);
@@ -1078,30 +1108,24 @@ __global__ void __launch_bounds__(256, 1) k_scan_tc(const __grid_constant__ Scan
         if (valid && mn <= 0) {  // rare once the bounds converge; static indices keep v[] in registers
 #pragma unroll
           for (int i = 0; i < 32; i++)
-            if ((int)v[i] <= s.thr[q0 + i]) tc_hit(a, q0 + i, (int)v[i], c0g, ci);
+            if ((int)v[i] <= s.thr[q0 + i]) tc_hit(a, q0 + i, (int)v[i], pos);
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
-      if (tid < nq && mpre < s.mc[tid]) {
+      if (tid < nq && mpre < s.mc[tid]) {  // bounds tightened by the flusher or other CTAs
         s.mc[tid] = mpre;
         const int th = q_threshold(__uint_as_float(mpre), s.qmin[tid], s.delta[tid]);
         if (th < s.thr[tid]) s.thr[tid] = th;
       }
     }
-    __syncthreads();
-    if (w < 4) {
-      unsigned mf = __ballot_sync(kFull, tid < nq && s.scnt[tid] > 0);
-      while (mf) {
-        const int qq = w * 32 + __ffs(mf) - 1;
-        mf &= mf - 1;
-        tc_flush(a, qq, c0g);
-      }
-    }
-    __syncthreads();
+    tc_bar();
   }
+  if (tid == 0) *(volatile int *)&s.done = 1;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (w == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s.tmem), "n"(kCols));
 }
 
 template <int MC>
@@ -1113,7 +1137,7 @@ int tc_resident(int nsm) {
   cudaFuncSetAttribute(k_scan_tc<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_scan_tc<MC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_tc<MC>, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_tc<MC>, 288, smem);
   // TMEM: every resident CTA holds 2 kTcNQ columns of the SM's 512
   per_sm = std::min(std::max(per_sm, 1), 512 / (2 * kTcNQ));
   return nsm * per_sm;
@@ -1122,7 +1146,7 @@ int tc_resident(int nsm) {
 template <int MC>
 void launch_tc(const ScanArgs &a, int nsm, cudaStream_t st) {
   const int grid = tc_resident<MC>(nsm);
-  k_scan_tc<MC><<<grid, 256, tc_smem_bytes<MC>(), st>>>(a);
+  k_scan_tc<MC><<<grid, 288, tc_smem_bytes<MC>(), st>>>(a);
 }
 
 // ---- work list construction ----
