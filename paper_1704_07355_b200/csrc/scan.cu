@@ -958,16 +958,30 @@ __device__ __forceinline__ void tc_load(const ScanArgs &a, int64_t g, int c, int
   vb = __ldg(a.valid + g * 32 + (c >> 3));
 }
 
-__device__ __forceinline__ void tc_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void tc_bar_all() { asm volatile("bar.sync 1, 288;" ::: "memory"); }
+__device__ __forceinline__ void tc_arrive(int t) {
+  if (t & 1) asm volatile("bar.arrive 3, 288;" ::: "memory");
+  else asm volatile("bar.arrive 2, 288;" ::: "memory");
+}
+__device__ __forceinline__ void tc_sync(int t) {
+  if (t & 1) asm volatile("bar.sync 3, 288;" ::: "memory");
+  else asm volatile("bar.sync 2, 288;" ::: "memory");
+}
 
-// 9 warps. Warps 0-7 compute: warps w and w + 4 share TMEM lane quarter
-// w % 4 (codes 32 (w % 4) .. + 31 of the tile); warp half h = w / 4 expands
-// sub-quantizers [h m/2, (h + 1) m/2) and reads query columns 32 k with
-// k % 2 == h. Software pipeline per item: while the tensor cores run tile
-// t + 1 (A and D double-buffered), the compute warps read tile t's sums and
-// expand tile t + 2. Warp 8 drains the survivor ring (tc_flusher).
+// 10 warps, specialised:
+//  * warps 0-7 (compute): warps w and w + 4 share TMEM lane quarter w % 4
+//    (codes 32 (w % 4) .. + 31 of the tile); warp half h = w / 4 expands
+//    sub-quantizers [h m/2, (h + 1) m/2) and reads query columns 32 k with
+//    k % 2 == h. Per tile: expand tile t + 1 into A[(t + 1) & 1], arrive on
+//    the tile's named barrier (2 / 3 alternating), wait for MMA(t) and read
+//    its sums. They never wait for each other inside an item;
+//  * warp 9 (MMA): per tile, bar.sync on the tile's named barrier (all
+//    compute threads expanded it and finished reading the D buffer it
+//    overwrites), then one elected lane issues the m/2 MMAs and commits to
+//    the buffer's mbarrier;
+//  * warp 8 (flusher): drains the survivor ring (tc_flusher).
 template <int MC>
-__global__ void __launch_bounds__(288, 1) k_scan_tc(const __grid_constant__ ScanArgs a) {
+__global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ ScanArgs a) {
   constexpr int K = 16 * MC, SBO = 8 * K, MH = MC / 2;
   constexpr uint32_t kCols = 2 * kTcNQ;
   extern __shared__ __align__(16) unsigned char dsm[];  // no-swizzle operands: 16 B alignment
@@ -1001,6 +1015,7 @@ __global__ void __launch_bounds__(288, 1) k_scan_tc(const __grid_constant__ Scan
   if (w == 8) {
     tc_flusher(a);
   } else {
+  const bool mma_warp = w == 9;
   const uint32_t tmem = s.tmem;
   const uint32_t t_row = tmem + ((uint32_t)((w & 3) * 32) << 16);
   const int n_items = *a.n_items;
@@ -1010,115 +1025,126 @@ __global__ void __launch_bounds__(288, 1) k_scan_tc(const __grid_constant__ Scan
     if (item >= n_items) break;
     const WorkItem it = a.items[item];
     const int nq = it.pair_count;
-    // ---- stage the item's tables (B operand) and per-query state ----
-    for (int e = tid; e < kTcNQ * MC; e += 256) {
-      const int q = e / MC, j = e - q * MC;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (q < nq) v = ((const uint4 *)a.qt)[(size_t)a.pair_t[it.pair_begin + q] * MC + j];
-      *(uint4 *)(sB + (q >> 3) * SBO + j * 128 + (q & 7) * 16) = v;
-    }
-    if (tid < kTcNQ) {
-      const int q = tid;
-      int thr = -1;
-      unsigned mb = 0;
-      if (q < nq) {
-        const int pi = it.pair_begin + q;
-        const int query = a.pair_q[pi], t = a.pair_t[pi];
-        s.query[q] = query;
-        s.qmin[q] = a.qmin_f[t];
-        s.delta[q] = a.delta_f[t];
-        mb = *(volatile unsigned *)&a.M_bits[query];
-        thr = q_threshold(__uint_as_float(mb), s.qmin[q], s.delta[q]);
-      } else {
-        s.query[q] = 0;
-        s.qmin[q] = 0.f;
-        s.delta[q] = 0.f;
-      }
-      s.thr[q] = thr;
-      s.mc[q] = mb;
-    }
-    const int n_mma = max(16, (nq + 15) & ~15);  // MMA N: the item's queries, rounded to 16
-    const uint32_t idesc = (2u << 4) | ((uint32_t)(n_mma >> 3) << 17) | ((uint32_t)(kTcCodes >> 4) << 24);
     const int64_t c0g = it.chunk_begin;
     const int64_t ntiles = 2 * (it.chunk_end - it.chunk_begin);
-    uint32_t cw[MH], vb_next = 0, vb = 0;
-    // prologue: expand tile 0 into A[0], load tile 1's words
-    tc_load<MC, MH>(a, c0g, row, j0, cw, vb_next);
-    tc_expand<MC, MH>(sA0, row, j0, cw, row);
-    vb = vb_next;
-    if (ntiles > 1) tc_load<MC, MH>(a, c0g, kTcCodes + row, j0, cw, vb_next);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    tc_bar();
-    if (tid == 0) s.item = atomicAdd(a.item_counter, 1);  // claimed ahead
-    auto issue = [&](int64_t t) {
-      const int buf = (int)(t & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-      for (int ks = 0; ks < K / 32; ks++) {
-        const uint64_t da = tc_smem_desc(sA_a + buf * 128 * K + ks * 256, SBO);
-        const uint64_t db = tc_smem_desc(sB_a + ks * 256, SBO);
-        const uint32_t acc = ks > 0 ? 1u : 0u;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + buf * kTcNQ),
-            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+    if (!mma_warp) {
+      // ---- stage the item's tables (B operand) and per-query state ----
+      for (int e = tid; e < kTcNQ * MC; e += 256) {
+        const int q = e / MC, j = e - q * MC;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (q < nq) v = ((const uint4 *)a.qt)[(size_t)a.pair_t[it.pair_begin + q] * MC + j];
+        *(uint4 *)(sB + (q >> 3) * SBO + j * 128 + (q & 7) * 16) = v;
       }
-      asm volatile(
-          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-              mbar0 + 8 * buf)
-          : "memory");
-    };
-    if (tid == 0) issue(0);
-    for (int64_t t = 0; t < ntiles; t++) {
-      const uint32_t vbt = vb;  // valid byte of tile t's octet
-      unsigned mpre = 0;
-      if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];  // lands during the wait
-      // ---- expand tile t + 1 into A[(t + 1) & 1] and start its MMA ----
-      if (t + 1 < ntiles) {
-        tc_expand<MC, MH>(sA0 + (size_t)((t + 1) & 1) * 128 * K, row, j0, cw,
-                          (int)((t + 1) & 1) * kTcCodes + row);
-        vb = vb_next;
-        if (t + 2 < ntiles)
-          tc_load<MC, MH>(a, c0g + ((t + 2) >> 1), (int)((t + 2) & 1) * kTcCodes + row, j0, cw,
-                          vb_next);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      tc_bar();
-      if (t + 1 < ntiles && tid == 0) issue(t + 1);
-      // ---- epilogue of tile t ----
-      const int buf = (int)(t & 1);
-      tc_wait(mbar0 + 8 * buf, buf ? ph1 : ph0);
-      if (buf) ph1 ^= 1; else ph0 ^= 1;
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const int c = buf * kTcCodes + row;
-      const bool valid = (vbt >> (c & 7)) & 1u;
-      const int64_t pos = (c0g + (t >> 1)) * kChunkCodes + c;
-      for (int q0 = half * 32; q0 < nq; q0 += 64) {
-        uint32_t v[32];
-        tc_ld32(t_row + buf * kTcNQ + q0, v);
-        int mn = 1;
-#pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const int4 t4 = *(const int4 *)&s.thr[q0 + i];
-          mn = min(mn, min(min((int)v[i] - t4.x, (int)v[i + 1] - t4.y),
-                           min((int)v[i + 2] - t4.z, (int)v[i + 3] - t4.w)));
+      if (tid < kTcNQ) {
+        const int q = tid;
+        int thr = -1;
+        unsigned mb = 0;
+        if (q < nq) {
+          const int pi = it.pair_begin + q;
+          const int query = a.pair_q[pi], t = a.pair_t[pi];
+          s.query[q] = query;
+          s.qmin[q] = a.qmin_f[t];
+          s.delta[q] = a.delta_f[t];
+          mb = *(volatile unsigned *)&a.M_bits[query];
+          thr = q_threshold(__uint_as_float(mb), s.qmin[q], s.delta[q]);
+        } else {
+          s.query[q] = 0;
+          s.qmin[q] = 0.f;
+          s.delta[q] = 0.f;
         }
-        if (valid && mn <= 0) {  // rare once the bounds converge; static indices keep v[] in registers
-#pragma unroll
-          for (int i = 0; i < 32; i++)
-            if ((int)v[i] <= s.thr[q0 + i]) tc_hit(a, q0 + i, (int)v[i], pos);
-        }
+        s.thr[q] = thr;
+        s.mc[q] = mb;
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    tc_bar_all();  // B and the query state are staged
+    if (tid == 0) s.item = atomicAdd(a.item_counter, 1);  // claimed ahead (read after the item's end barrier)
+    if (mma_warp) {
+      const int n_mma = max(16, (nq + 15) & ~15);  // MMA N: the item's queries, rounded to 16
+      const uint32_t idesc =
+          (2u << 4) | ((uint32_t)(n_mma >> 3) << 17) | ((uint32_t)(kTcCodes >> 4) << 24);
+      for (int64_t t = 0; t < ntiles; t++) {
+        tc_sync((int)t);
+        const int buf = (int)(t & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if ((tid & 31) == 0) {
+#pragma unroll
+          for (int ks = 0; ks < K / 32; ks++) {
+            const uint64_t da = tc_smem_desc(sA_a + buf * 128 * K + ks * 256, SBO);
+            const uint64_t db = tc_smem_desc(sB_a + ks * 256, SBO);
+            const uint32_t acc = ks > 0 ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + buf * kTcNQ),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                  mbar0 + 8 * buf)
+              : "memory");
+        }
+        __syncwarp();
+      }
+    } else {
+      uint32_t cw[MH], vb_next = 0, vb = 0;
+      // prologue: expand tile 0 into A[0], load tile 1's words
+      tc_load<MC, MH>(a, c0g, row, j0, cw, vb_next);
+      tc_expand<MC, MH>(sA0, row, j0, cw, row);
+      vb = vb_next;
+      if (ntiles > 1) tc_load<MC, MH>(a, c0g, kTcCodes + row, j0, cw, vb_next);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
-      if (tid < nq && mpre < s.mc[tid]) {  // bounds tightened by the flusher or other CTAs
-        s.mc[tid] = mpre;
-        const int th = q_threshold(__uint_as_float(mpre), s.qmin[tid], s.delta[tid]);
-        if (th < s.thr[tid]) s.thr[tid] = th;
+      tc_arrive(0);
+      for (int64_t t = 0; t < ntiles; t++) {
+        const uint32_t vbt = vb;  // valid byte of tile t's octet
+        unsigned mpre = 0;
+        if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];  // lands during the wait
+        // ---- expand tile t + 1 into A[(t + 1) & 1] (MMA(t - 1), its last
+        // reader, completed before this warp read tile t - 1) ----
+        if (t + 1 < ntiles) {
+          tc_expand<MC, MH>(sA0 + (size_t)((t + 1) & 1) * 128 * K, row, j0, cw,
+                            (int)((t + 1) & 1) * kTcCodes + row);
+          vb = vb_next;
+          if (t + 2 < ntiles)
+            tc_load<MC, MH>(a, c0g + ((t + 2) >> 1), (int)((t + 2) & 1) * kTcCodes + row, j0, cw,
+                            vb_next);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          tc_arrive((int)(t + 1));
+        }
+        // ---- epilogue of tile t ----
+        const int buf = (int)(t & 1);
+        tc_wait(mbar0 + 8 * buf, buf ? ph1 : ph0);
+        if (buf) ph1 ^= 1; else ph0 ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int c = buf * kTcCodes + row;
+        const bool valid = (vbt >> (c & 7)) & 1u;
+        const int64_t pos = (c0g + (t >> 1)) * kChunkCodes + c;
+        for (int q0 = half * 32; q0 < nq; q0 += 64) {
+          uint32_t v[32];
+          tc_ld32(t_row + buf * kTcNQ + q0, v);
+          int mn = 1;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const int4 t4 = *(const int4 *)&s.thr[q0 + i];
+            mn = min(mn, min(min((int)v[i] - t4.x, (int)v[i + 1] - t4.y),
+                             min((int)v[i + 2] - t4.z, (int)v[i + 3] - t4.w)));
+          }
+          if (valid && mn <= 0) {  // rare once the bounds converge; static indices keep v[] in registers
+#pragma unroll
+            for (int i = 0; i < 32; i++)
+              if ((int)v[i] <= s.thr[q0 + i]) tc_hit(a, q0 + i, (int)v[i], pos);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        if (tid < nq && mpre < s.mc[tid]) {  // bounds tightened by the flusher or other CTAs
+          s.mc[tid] = mpre;
+          const int th = q_threshold(__uint_as_float(mpre), s.qmin[tid], s.delta[tid]);
+          if (th < s.thr[tid]) s.thr[tid] = th;
+        }
       }
     }
-    tc_bar();
+    tc_bar_all();  // end of item: every tile read, s.item holds the next item
   }
   if (tid == 0) *(volatile int *)&s.done = 1;
   }
@@ -1137,7 +1163,7 @@ int tc_resident(int nsm) {
   cudaFuncSetAttribute(k_scan_tc<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_scan_tc<MC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_tc<MC>, 288, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_tc<MC>, 320, smem);
   // TMEM: every resident CTA holds 2 kTcNQ columns of the SM's 512
   per_sm = std::min(std::max(per_sm, 1), 512 / (2 * kTcNQ));
   return nsm * per_sm;
@@ -1146,7 +1172,7 @@ int tc_resident(int nsm) {
 template <int MC>
 void launch_tc(const ScanArgs &a, int nsm, cudaStream_t st) {
   const int grid = tc_resident<MC>(nsm);
-  k_scan_tc<MC><<<grid, 288, tc_smem_bytes<MC>(), st>>>(a);
+  k_scan_tc<MC><<<grid, 320, tc_smem_bytes<MC>(), st>>>(a);
 }
 
 // ---- work list construction ----
