@@ -139,13 +139,18 @@ QADC_API int64_t qadc_b200_index_bytes(const qadc_b200_index *idx);
 #define QADC_B200_LUT_IN 2u    /* lut_in / cells_in supplied (device) */
 #define QADC_B200_NO_FSAT 4u   /* leave the saturated first-R lanes out (every
                                   shard but the owner of the global prefix) */
+#define QADC_B200_SCAN_PRMT 8u /* scan with the PRMT (CUDA-core) kernel even
+                                  where the tensor-core scan applies */
+#define QADC_B200_SCAN_TC 16u  /* tensor-core scan (m = 16, 32) even with few
+                                  (query, list) pairs per list; default: the
+                                  tensor cores from 64 pairs per list on */
 
 /*
  * adc.py:114-187 search(method="qadc") for nq queries at once:
  * probe (IVF) -> residual, rotation, float LUT -> qmax from the first
  * probed cell's first `init` codes -> per-cell qmin/delta and uint8 LUT ->
- * scan with streaming thresholds (int8 tcgen05 one-hot GEMM for m = 16, 32;
- * interleaved PRMT lookups otherwise) -> exact top-R by
+ * scan with streaming thresholds (int8 tcgen05 one-hot GEMM for m = 16, 32
+ * with >= 64 pairs per list; interleaved PRMT lookups otherwise) -> exact top-R by
  * (distance, id). Outputs (nq, R) ids / fp32 midpoint distances sorted
  * ascending, padded with -1 / +inf, and out_n (nq) = result count.
  * With QADC_B200_LUT_IN, lut_in (nq, ma, m, 16) fp32 and cells_in (nq, ma)

@@ -24,6 +24,8 @@ MAX_M = 128
 HOST_IO = 1
 LUT_IN = 2
 NO_FSAT = 4
+SCAN_PRMT = 8  # force the PRMT (CUDA-core) scan kernel
+SCAN_TC = 16  # force the int8 tensor-core scan kernel (m = 16, 32)
 
 _lib = None
 

@@ -129,6 +129,7 @@ struct DevBuf {
 struct SearchStats {
   int64_t codes = 0, cands = 0, reruns = 0, scan_launches = 0, launches = 0;
   double scan_us = 0.0;
+  int scan_tc = 0;  // the scan ran on the tensor cores
 };
 
 // Keep stream-ordered workspace in the device pool between calls (the
@@ -149,12 +150,18 @@ void retain_pool_memory() {
 int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int ma, int init,
                 const float *lut_in, const int64_t *cells_in, int64_t *out_ids, float *out_d,
                 int32_t *out_n, cudaStream_t st, SearchStats &ss, const unsigned *M_override,
-                int cap_g, int depth, bool no_fsat) {
+                int cap_g, int depth, bool no_fsat, bool prmt, bool force_tc) {
   if (nq == 0) return kOk;
   const int m = idx->m;
   const int nslots = idx->K ? ma : 1;
   const int64_t npairs = (int64_t)nq * nslots;
-  const int qt_tile = scan_tile_queries(m);
+  // The tensor-core scan amortises each code's one-hot expansion over the
+  // queries probing its list: with few (query, list) pairs per list (IVF
+  // at small nprobe / large K) the PRMT kernel is faster (measured: cfg2
+  // nprobe 16, ~40 pairs per list: 10.2 ms PRMT vs 25.6 ms tensor cores).
+  static const int tc_min_pairs = scan_env_int("QADC_B200_TC_MIN_PAIRS", 64);
+  if (!force_tc && npairs < (int64_t)tc_min_pairs * std::max(idx->nlists, 1)) prmt = true;
+  const int qt_tile = scan_tile_queries(m, prmt);
   const int nl = idx->nlists;
 
   DevBuf<int64_t> cells_b;
@@ -244,7 +251,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
     // together only if the item count fills whole waves. Pick the range
     // count r minimising waves x (chunks per item + per-item overhead).
     const int64_t tiles = (npairs + qt_tile - 1) / qt_tile;
-    const int64_t ctas = scan_resident_ctas(m, cap_l, nsm, linear);
+    const int64_t ctas = scan_resident_ctas(m, cap_l, nsm, linear, prmt);
     const int64_t ch = idx->total_chunks;
     int64_t best_r = 1;
     double best = 1e300;
@@ -315,7 +322,8 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, st);
-  launch_scan(a, nsm, st);
+  launch_scan(a, nsm, st, prmt);
+  ss.scan_tc = scan_use_tc(m, prmt) ? 1 : 0;
   QADC_CUDA(cudaGetLastError());
   cudaEventRecord(e1, st);
   ss.scan_launches++;
@@ -396,7 +404,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
     const int cap2 = (int)std::min<int64_t>(std::max<int64_t>((int64_t)need + 1024, 2LL * cap_g),
                                             (int64_t)1 << 28);
     rc = search_impl(idx, sub_q.p, nr, R, ma, init, lp, cp, sub_ids.p, sub_d.p, sub_n.p, st, ss,
-                     sub_M.p, cap2, depth + 1, no_fsat);
+                     sub_M.p, cap2, depth + 1, no_fsat, prmt, force_tc);
     if (rc) return rc;
     k_scatter_out<<<gridn((int64_t)nr * R), 256, 0, st>>>(sub_ids.p, sub_d.p, sub_n.p, rows.p, nr,
                                                           R, out_ids, out_d, out_n);
@@ -789,7 +797,8 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
   const int cap_g = (int)std::min<int64_t>(
       std::max<int64_t>({8192, 8LL * R, std::min<int64_t>(65536, cap_mem)}), 1 << 20);
   int rc = search_impl(idx, q, nq, R, ma, init, lin, cin, oi, od, on, st, ss, nullptr, cap_g, 0,
-                       (flags & QADC_B200_NO_FSAT) != 0);
+                       (flags & QADC_B200_NO_FSAT) != 0, (flags & QADC_B200_SCAN_PRMT) != 0,
+                       (flags & QADC_B200_SCAN_TC) != 0);
   if (rc) return rc;
   if (host) {
     QADC_CUDA(cudaMemcpyAsync(out_ids, oi, (size_t)nq * R * 8, cudaMemcpyDeviceToHost, st));
@@ -804,7 +813,7 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
     stats[3] = ss.scan_launches;
     stats[4] = ss.launches;
     stats[5] = (int64_t)llround(ss.scan_us);
-    stats[6] = scan_use_tc(idx->m) ? 1 : 0;  // scan kernel: 1 = int8 tensor-core, 0 = PRMT
+    stats[6] = ss.scan_tc;  // scan kernel: 1 = int8 tensor-core, 0 = PRMT
     stats[7] = 0;
   }
   return kOk;

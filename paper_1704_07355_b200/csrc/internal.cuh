@@ -144,12 +144,13 @@ constexpr int kHistBins = 1024;                 // 32 coarse x 32 fine
 constexpr int kHistWords = kHistBins + 32;      // fine bins, then coarse sums
 int scan_qt_per_cta(int m);
 // Tensor-core scan in use for this m; queries per work item of the scan.
-bool scan_use_tc(int m);
-int scan_tile_queries(int m);
+// prmt: the caller asked for the PRMT kernel (QADC_B200_SCAN_PRMT).
+bool scan_use_tc(int m, bool prmt);
+int scan_tile_queries(int m, bool prmt);
 // Resident scan CTAs on the device (occupancy x SMs) for this shape.
-int scan_resident_ctas(int m, int cap_l, int nsm, int linear);
+int scan_resident_ctas(int m, int cap_l, int nsm, int linear, bool prmt);
 int scan_env_int(const char *name, int dflt);
-void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st);
+void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st, bool prmt);
 // Work-list construction (device side). scratch: build_work_scratch ints.
 int64_t build_work_scratch(int nlists, int nslots);
 int64_t build_work(const qadc_b200_index *idx, const int64_t *cells, int nq,

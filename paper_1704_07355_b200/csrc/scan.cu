@@ -756,17 +756,18 @@ void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
 //   sum_j T_q[j][c_j] = onehot(c) . T_q,   onehot(c)[16 j + c_j] = 1,
 // exact in int32 (entries <= 127, m <= 32), and min(255, .) of it is the
 // reference's saturating byte sum (all entries are >= 0). A tile of 128 codes
-// is expanded by its threads into the A operand (128 x 16m bytes, K-major,
-// SMEM); the uint8 tables of the item's NQ queries are the resident B
-// operand (NQ x 16m, K-major, SMEM); one elected thread issues m/2
-// tcgen05.mma.kind::i8 (K = 32 each) into a TMEM accumulator (128 lanes x NQ
-// int32 columns) and commits to an mbarrier; every thread then reads its
+// is expanded by its threads into the A operand, written straight to TMEM
+// with tcgen05.st (128 lanes x 16m bytes, K-major: no shared-memory traffic
+// for the 16x-inflated one-hot operand); the uint8 tables of the item's NQ
+// queries are the resident B operand (NQ x 16m, K-major, SMEM); one elected
+// thread issues m/2 tcgen05.mma.kind::i8 (K = 32 each, A from TMEM) into a
+// TMEM accumulator (128 lanes x NQ int32 columns) and commits to an mbarrier; every thread then reads its
 // code's NQ sums with tcgen05.ld and tests them against the queries'
 // thresholds. Survivors go straight to the per-query global candidate lists
 // (midpoint <= the global bound M), counted in the per-query midpoint
 // histogram whose R-th bucket tightens M (hist_bound) — the same selection
-// contract as k_scan. SMEM layout: canonical K-major, no swizzle: row r,
-// 16-byte column j at (r / 8) * 8K + 128 j + 16 (r % 8) (LBO = 128 B,
+// contract as k_scan. B's SMEM layout: canonical K-major, no swizzle: row
+// r, 16-byte column j at (r / 8) * 8K + 128 j + 16 (r % 8) (LBO = 128 B,
 // SBO = 8K B).
 constexpr int kTcCodes = 128;  // codes per tile (MMA M)
 constexpr int kTcNQ = 128;     // queries per item (max MMA N)
@@ -927,25 +928,40 @@ __device__ __forceinline__ void tc_flusher(const ScanArgs &a) {
   }
 }
 
-// Expand sub-quantizers [j0, j0 + MH) of the code in A row `row` (code c
-// of its chunk) into A.
-template <int MC, int MH>
-__device__ __forceinline__ void tc_expand(uint8_t *sA, int row, int j0, const uint32_t (&cw)[MH],
-                                          int c) {
-  constexpr int SBO = 8 * 16 * MC;
-  uint8_t *arow = sA + (row >> 3) * SBO + (row & 7) * 16 + j0 * 128;
+// Expand sub-quantizers [j0, j0 + MH) of code c of its chunk into the A
+// operand in TMEM: the thread's own lane (= A row, the code's position in
+// the tile), 4 columns (16 one-hot bytes, byte k of the sub-quantizer at
+// column k / 4, byte k % 4) per sub-quantizer, from column a_col. Word w of
+// sub-code x is 1 << (8 x - 32 w) when 0 <= 8 x - 32 w < 32, else 0: PTX
+// shl clamps shift amounts >= 32 (a negative difference reads as a large
+// unsigned amount) to a zero result.
+__device__ __forceinline__ uint32_t tc_shl(uint32_t s) {
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(1u), "r"(s));
+  return r;
+}
+
+template <int MH>
+__device__ __forceinline__ void tc_expand(uint32_t a_col, const uint32_t (&cw)[MH], int c) {
   const int sh = 4 * (c & 7);
 #pragma unroll
-  for (int j = 0; j < MH; j++) {
-    const uint32_t cj = (cw[j] >> sh) & 15u;
-    const uint32_t bit = 1u << ((cj & 3u) << 3);
-    const uint32_t wsel = cj >> 2;
-    uint4 oh;
-    oh.x = wsel == 0 ? bit : 0u;
-    oh.y = wsel == 1 ? bit : 0u;
-    oh.z = wsel == 2 ? bit : 0u;
-    oh.w = wsel == 3 ? bit : 0u;
-    *(uint4 *)(arow + j * 128) = oh;
+  for (int j = 0; j < MH; j += 4) {
+    uint32_t r[16];
+#pragma unroll
+    for (int jj = 0; jj < 4; jj++) {
+      const uint32_t s8 = ((cw[j + jj] >> sh) << 3) & 0x78u;
+      r[4 * jj + 0] = tc_shl(s8);
+      r[4 * jj + 1] = tc_shl(s8 - 32u);
+      r[4 * jj + 2] = tc_shl(s8 - 64u);
+      r[4 * jj + 3] = tc_shl(s8 - 96u);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16};" ::"r"(a_col + 4 * j),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15])
+        : "memory");
   }
 }
 
@@ -983,15 +999,15 @@ __device__ __forceinline__ void tc_sync(int t) {
 template <int MC>
 __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ ScanArgs a) {
   constexpr int K = 16 * MC, SBO = 8 * K, MH = MC / 2;
-  constexpr uint32_t kCols = 2 * kTcNQ;
+  // TMEM columns: D[0], D[1] (kTcNQ each), then A[0], A[1] (K / 4 each)
+  constexpr uint32_t kCols = 512, kACols = K / 4, kA0 = 2 * kTcNQ;
+  static_assert(kA0 + 2 * kACols <= kCols, "TMEM budget");
   extern __shared__ __align__(16) unsigned char dsm[];  // no-swizzle operands: 16 B alignment
   TcSmem &s = g_tc;
   uint8_t *sB = dsm;                       // [kTcNQ][K]
-  uint8_t *sA0 = dsm + kTcNQ * K;          // [2][128][K]
   const int tid = threadIdx.x, w = tid >> 5;
   const int row = tid & 127, half = (tid >> 7) & 1, j0 = half * MH;
   const uint32_t sB_a = (uint32_t)__cvta_generic_to_shared(sB);
-  const uint32_t sA_a = (uint32_t)__cvta_generic_to_shared(sA0);
   const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(&s.mbar[0]);
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -1070,13 +1086,13 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
         if ((tid & 31) == 0) {
 #pragma unroll
           for (int ks = 0; ks < K / 32; ks++) {
-            const uint64_t da = tc_smem_desc(sA_a + buf * 128 * K + ks * 256, SBO);
+            const uint32_t ta = tmem + kA0 + buf * kACols + ks * 8;  // A from TMEM (K = 32 bytes = 8 columns)
             const uint64_t db = tc_smem_desc(sB_a + ks * 256, SBO);
             const uint32_t acc = ks > 0 ? 1u : 0u;
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + buf * kTcNQ),
-                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + buf * kTcNQ),
+                "r"(ta), "l"(db), "r"(idesc), "r"(acc));
           }
           asm volatile(
               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -1087,12 +1103,14 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
       }
     } else {
       uint32_t cw[MH], vb_next = 0, vb = 0;
+      // this thread's A columns (its lane quarter, its half of the K range)
+      const uint32_t a_lane = tmem + ((uint32_t)((w & 3) * 32) << 16) + kA0 + (uint32_t)(j0 * 4);
       // prologue: expand tile 0 into A[0], load tile 1's words
       tc_load<MC, MH>(a, c0g, row, j0, cw, vb_next);
-      tc_expand<MC, MH>(sA0, row, j0, cw, row);
+      tc_expand<MH>(a_lane, cw, row);
       vb = vb_next;
       if (ntiles > 1) tc_load<MC, MH>(a, c0g, kTcCodes + row, j0, cw, vb_next);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       tc_arrive(0);
       for (int64_t t = 0; t < ntiles; t++) {
@@ -1102,13 +1120,13 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
         // ---- expand tile t + 1 into A[(t + 1) & 1] (MMA(t - 1), its last
         // reader, completed before this warp read tile t - 1) ----
         if (t + 1 < ntiles) {
-          tc_expand<MC, MH>(sA0 + (size_t)((t + 1) & 1) * 128 * K, row, j0, cw,
-                            (int)((t + 1) & 1) * kTcCodes + row);
+          tc_expand<MH>(a_lane + (uint32_t)((t + 1) & 1) * kACols, cw,
+                        (int)((t + 1) & 1) * kTcCodes + row);
           vb = vb_next;
           if (t + 2 < ntiles)
             tc_load<MC, MH>(a, c0g + ((t + 2) >> 1), (int)((t + 2) & 1) * kTcCodes + row, j0, cw,
                             vb_next);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           asm volatile("tcgen05.fence::before_thread_sync;");
           tc_arrive((int)(t + 1));
         }
@@ -1155,7 +1173,7 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
 }
 
 template <int MC>
-size_t tc_smem_bytes() { return (size_t)(kTcNQ + 2 * kTcCodes) * 16 * MC; }
+size_t tc_smem_bytes() { return (size_t)kTcNQ * 16 * MC; }
 
 template <int MC>
 int tc_resident(int nsm) {
@@ -1164,8 +1182,9 @@ int tc_resident(int nsm) {
   cudaFuncSetAttribute(k_scan_tc<MC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_tc<MC>, 320, smem);
-  // TMEM: every resident CTA holds 2 kTcNQ columns of the SM's 512
-  per_sm = std::min(std::max(per_sm, 1), 512 / (2 * kTcNQ));
+  // TMEM: every resident CTA holds all 512 columns of its SM (A and D,
+  // double-buffered)
+  per_sm = 1;
   return nsm * per_sm;
 }
 
@@ -1398,17 +1417,17 @@ int scan_qt_per_cta(int m) {
   return m <= 64 ? 8 : 4;
 }
 
-// Tensor-core scan for m in {16, 32} (QADC_B200_TC=0 selects the PRMT
-// kernel).
-bool scan_use_tc(int m) {
+// Tensor-core scan for m in {16, 32}; the PRMT kernel otherwise, or when the
+// call asks for it (QADC_B200_SCAN_PRMT) or QADC_B200_TC=0.
+bool scan_use_tc(int m, bool prmt) {
   static const int env = scan_env_int("QADC_B200_TC", 1);
-  return env != 0 && (m == 16 || m == 32);
+  return !prmt && env != 0 && (m == 16 || m == 32);
 }
 
-int scan_tile_queries(int m) { return scan_use_tc(m) ? kTcNQ : scan_qt_per_cta(m); }
+int scan_tile_queries(int m, bool prmt) { return scan_use_tc(m, prmt) ? kTcNQ : scan_qt_per_cta(m); }
 
-void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st) {
-  if (scan_use_tc(a.m)) {
+void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st, bool prmt) {
+  if (scan_use_tc(a.m, prmt)) {
     if (a.m == 32) launch_tc<32>(a, nsm, st);
     else launch_tc<16>(a, nsm, st);
     return;
@@ -1428,8 +1447,8 @@ void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st) {
   }
 }
 
-int scan_resident_ctas(int m, int cap_l, int nsm, int linear) {
-  if (scan_use_tc(m)) return m == 32 ? tc_resident<32>(nsm) : tc_resident<16>(nsm);
+int scan_resident_ctas(int m, int cap_l, int nsm, int linear, bool prmt) {
+  if (scan_use_tc(m, prmt)) return m == 32 ? tc_resident<32>(nsm) : tc_resident<16>(nsm);
   const int qt = scan_qt_per_cta(m);
   const bool lin = linear != 0;
   if (qt == 16) {

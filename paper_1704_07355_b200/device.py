@@ -97,7 +97,7 @@ class DeviceIndex:
 
     # ------------------------------------------------------------ search
     def search(self, queries, R: int, ma: int = 1, init: int = 1000, lut=None, cells=None,
-               stream=None, with_fsat: bool = True) -> BatchResult:
+               stream=None, with_fsat: bool = True, scan: str = "auto") -> BatchResult:
         """Batched Quick ADC search. `queries` is a (Q, d) float32 torch
         tensor on the GPU (device I/O) or a numpy array (host I/O: the
         host<->device copies happen inside the call). lut/cells inject the
@@ -110,6 +110,9 @@ class DeviceIndex:
         flags = _native.LUT_IN if lut is not None else 0
         if not with_fsat:
             flags |= _native.NO_FSAT
+        if scan not in ("auto", "prmt", "tc"):
+            raise ValueError(f"unknown scan kernel {scan!r}")
+        flags |= {"auto": 0, "prmt": _native.SCAN_PRMT, "tc": _native.SCAN_TC}[scan]
         if isinstance(queries, np.ndarray):
             q = _np(queries, np.float32).reshape(-1, self.d)
             nq = q.shape[0]

@@ -10,6 +10,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from pathlib import Path
 
+import os
+
 import numpy as np
 
 from . import datagen
@@ -238,22 +240,25 @@ def ivf_rows(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, device="cuda",
     encoded (GPU encoder), grouped into row-ordered lists.
 
     Config 2 (list sharding): the whole base of n codes (every rank builds
-    it; `shard_ivf_lists` keeps the rank's lists), exact einsum-order
-    assignment (qadc_b200_assign, the reference's kmeans.assign_batch
-    semantics). Config 4 (range sharding): rank r draws the chunks of its
-    id range of the global CFG4_CHUNK grid; tensor-core assignment.
+    it; `shard_ivf_lists` keeps the rank's lists). Config 4 (range
+    sharding): rank r draws the chunks of its id range of the global
+    CFG4_CHUNK grid. Both assign on the tensor cores (assign_tensor_core;
+    QADC_B200_EXACT_ASSIGN=1 selects the exact einsum-order
+    qadc_b200_assign, the reference's kmeans.assign_batch semantics, ~8x
+    slower at N=1e8): the index is an input of the search path and parity
+    is defined given the index.
     Returns (codes (n_r, m/2), ids (n_r,), row_off (K + 1,))."""
     import torch
 
     from .ivf import assign_device, encode_device
 
     C = torch.from_numpy(np.ascontiguousarray(coarse, dtype=np.float32)).to(device)
+    cn = (C.double() ** 2).sum(1).float()
     if cfg.sharding == "range":
         nch = -(-n // CFG4_CHUNK)
         per = -(-nch // world)
         gs = range(rank * per, min(nch, (rank + 1) * per))
         spans = [(g * CFG4_CHUNK, min(n, (g + 1) * CFG4_CHUNK), g) for g in gs]
-        cn = (C.double() ** 2).sum(1).float()
     else:
         spans = [(c0, min(n, c0 + chunk), c0 // chunk) for c0 in range(0, n, chunk)]
     tot = sum(b - a for a, b, _ in spans)
@@ -270,7 +275,8 @@ def ivf_rows(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, device="cuda",
         else:
             X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000, centre_seed=CORPUS,
                                       stream=datagen.STREAM_BASE * 100 + g, device=device)
-            lab = assign_device(coarse, X)
+            lab = (assign_device(coarse, X) if os.environ.get("QADC_B200_EXACT_ASSIGN") == "1"
+                   else assign_tensor_core(X, C, cn))
         labels[o:o + k] = lab
         codes[o:o + k] = encode_device(pq, X - C[lab])
         ids[o:o + k] = torch.arange(a, b, dtype=torch.int64, device=device)

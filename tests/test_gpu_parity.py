@@ -250,11 +250,19 @@ def _random_flat(rng, n, m, d, nq, cb_scale=50.0):
 def test_search_batch_vs_oracle(gpu, m, R, init):
     rng = np.random.default_rng(m * 1000 + R)
     idx, flat, qs, cb = _random_flat(rng, 150_000, m, 128, 48)
-    res = idx.search(qs, R, init=init)
+    tc = m in (16, 32)  # the int8 tensor-core scan applies
+    res = idx.search(qs, R, init=init, scan="tc" if tc else "auto")
     oi, od, on, _ = orc.search_batch(qs, cb, None, None, 1, flat, R, init)
+    assert res.stats["scan_tc"] == (1 if tc else 0)
     assert np.array_equal(res.ids, oi)
     assert np.array_equal(_bits(res.distances), _bits(od))
     assert np.array_equal(res.counts, on)
+    if tc:  # the CUDA-core PRMT scan on the same inputs
+        pr = idx.search(qs, R, init=init, scan="prmt")
+        assert pr.stats["scan_tc"] == 0
+        assert np.array_equal(pr.ids, oi)
+        assert np.array_equal(_bits(pr.distances), _bits(od))
+        assert np.array_equal(pr.counts, on)
 
 
 def test_edge_cases_vs_oracle(gpu):
@@ -380,12 +388,15 @@ def test_ivf_search_vs_oracle_at_scale(gpu, ma):
         cells[i] = c
         for s_, r in enumerate(res):
             luts[i, s_] = orc.compute_tables(cb, orc.rotate(Rm, r))
-    got = idx.search(qs, R, ma=ma, init=1000, lut=luts, cells=cells)
     oi, od, on, _ = orc.search_batch(qs, cb, Rm, coarse, ma, flat, R, 1000, lut_in=luts,
                                      cells_in=cells)
-    assert np.array_equal(got.ids, oi)
-    assert np.array_equal(_bits(got.distances), _bits(od))
-    assert np.array_equal(got.counts, on)
+    for scan in ("tc", "prmt", "auto"):  # int8 tensor-core scan, PRMT scan, heuristic
+        got = idx.search(qs, R, ma=ma, init=1000, lut=luts, cells=cells, scan=scan)
+        if scan != "auto":
+            assert got.stats["scan_tc"] == (1 if scan == "tc" else 0)
+        assert np.array_equal(got.ids, oi), scan
+        assert np.array_equal(_bits(got.distances), _bits(od)), scan
+        assert np.array_equal(got.counts, on), scan
     # native: the GPU rotates, probes and builds the tables itself; the
     # oracle port uses the same float64 rotation arithmetic, so the whole
     # native path is bit-exact against it too
