@@ -318,6 +318,8 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   static const int bound_every = std::max(1, scan_env_int("QADC_B200_BOUND_EVERY", 32));
   a.bound_every = bound_every;
   a.linear = linear;  // long items (>= 64 chunks per list on average)
+  static const int tc_dbg = scan_env_int("QADC_B200_TC_DEBUG", 0);
+  a.dbg = tc_dbg;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

@@ -138,6 +138,7 @@ struct ScanArgs {
   int R;
   int bound_every;         // appended candidates between global-histogram bound reads
   int linear;              // 1: linear fixed-m loop (long items), 0: interleaved loop
+  int dbg;                 // timing experiments only (QADC_B200_TC_DEBUG; results invalid if != 0)
 };
 
 constexpr int kHistBins = 1024;                 // 32 coarse x 32 fine

@@ -770,7 +770,7 @@ void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
 // r, 16-byte column j at (r / 8) * 8K + 128 j + 16 (r % 8) (LBO = 128 B,
 // SBO = 8K B).
 constexpr int kTcCodes = 128;  // codes per tile (MMA M)
-constexpr int kTcNQ = 128;     // queries per item (max MMA N)
+constexpr int kTcNQ = 256;     // queries per item (max MMA N)
 constexpr int kRing = 1024;    // survivor ring between the compute warps and the flusher warp
 
 __device__ __forceinline__ uint64_t tc_smem_desc(uint32_t saddr, uint32_t sbo) {
@@ -968,45 +968,57 @@ __device__ __forceinline__ void tc_expand(uint32_t a_col, const uint32_t (&cw)[M
 template <int MC, int MH>
 __device__ __forceinline__ void tc_load(const ScanArgs &a, int64_t g, int c, int j0,
                                         uint32_t (&cw)[MH], uint32_t &vb) {
+  if (a.dbg & 4) g = 0;  // timing experiment: every tile reads chunk 0 (L1/L2 resident)
   const uint32_t *p = a.codes + ((size_t)g * MC + j0) * 32 + (c >> 3);
 #pragma unroll
   for (int j = 0; j < MH; j++) cw[j] = __ldg(p + j * 32);
   vb = __ldg(a.valid + g * 32 + (c >> 3));
 }
 
-__device__ __forceinline__ void tc_bar_all() { asm volatile("bar.sync 1, 288;" ::: "memory"); }
+// Named barriers over the compute warps and the MMA warp (NB threads).
+template <int NB>
+__device__ __forceinline__ void tc_bar_all() { asm volatile("bar.sync 1, %0;" ::"n"(NB) : "memory"); }
+template <int NB>
 __device__ __forceinline__ void tc_arrive(int t) {
-  if (t & 1) asm volatile("bar.arrive 3, 288;" ::: "memory");
-  else asm volatile("bar.arrive 2, 288;" ::: "memory");
+  if (t & 1) asm volatile("bar.arrive 3, %0;" ::"n"(NB) : "memory");
+  else asm volatile("bar.arrive 2, %0;" ::"n"(NB) : "memory");
 }
+template <int NB>
 __device__ __forceinline__ void tc_sync(int t) {
-  if (t & 1) asm volatile("bar.sync 3, 288;" ::: "memory");
-  else asm volatile("bar.sync 2, 288;" ::: "memory");
+  if (t & 1) asm volatile("bar.sync 3, %0;" ::"n"(NB) : "memory");
+  else asm volatile("bar.sync 2, %0;" ::"n"(NB) : "memory");
 }
 
-// 10 warps, specialised:
-//  * warps 0-7 (compute): warps w and w + 4 share TMEM lane quarter w % 4
-//    (codes 32 (w % 4) .. + 31 of the tile); warp half h = w / 4 expands
-//    sub-quantizers [h m/2, (h + 1) m/2) and reads query columns 32 k with
-//    k % 2 == h. Per tile: expand tile t + 1 into A[(t + 1) & 1], arrive on
-//    the tile's named barrier (2 / 3 alternating), wait for MMA(t) and read
-//    its sums. They never wait for each other inside an item;
-//  * warp 9 (MMA): per tile, bar.sync on the tile's named barrier (all
-//    compute threads expanded it and finished reading the D buffer it
-//    overwrites), then one elected lane issues the m/2 MMAs and commits to
-//    the buffer's mbarrier;
-//  * warp 8 (flusher): drains the survivor ring (tc_flusher).
-template <int MC>
-__global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ ScanArgs a) {
-  constexpr int K = 16 * MC, SBO = 8 * K, MH = MC / 2;
-  // TMEM columns: D[0], D[1] (kTcNQ each), then A[0], A[1] (K / 4 each)
-  constexpr uint32_t kCols = 512, kACols = K / 4, kA0 = 2 * kTcNQ;
+// 4G + 2 warps, specialised (G = 4 by default):
+//  * warps 0 .. 4G-1 (compute): warps w, w + 4, ... share TMEM lane quarter
+//    w % 4 (codes 32 (w % 4) .. + 31 of the tile); warp part p = w / 4
+//    expands sub-quantizers [p m/G, (p + 1) m/G) and reads query columns
+//    32 k with k % G == p. Per tile: expand tile t + 1 into A[(t + 1) & 1]
+//    while MMA(t) runs, wait for MMA(t), read its sums, then arrive on tile
+//    t + 1's named barrier (2 / 3 alternating). They never wait for each
+//    other inside an item;
+//  * warp 4G + 1 (MMA): per tile, bar.sync on the tile's named barrier (all
+//    compute threads expanded it and finished reading D), then one elected
+//    lane issues the m/2 MMAs (N = the item's queries, up to 256) and
+//    commits to the mbarrier.
+//  D is single-buffered at N = 256: one MMA instruction costs ~77 cycles of
+//  issue for any N <= 128 but 128 cycles of execution at N = 256
+//  (tools/tc_mma_bench: 3.79 vs 4.59 POP/s back to back), so 256 queries per
+//  instruction beat double-buffering two 128-query accumulators;
+//  * warp 4G (flusher): drains the survivor ring (tc_flusher).
+template <int MC, int G>
+__global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_constant__ ScanArgs a) {
+  constexpr int K = 16 * MC, SBO = 8 * K, MH = MC / G;
+  constexpr int NT = 128 * G, NB = NT + 32;  // compute threads; + the MMA warp
+  static_assert(MH % 4 == 0 && kTcNQ % (32 * G) == 0, "tile split");
+  // TMEM columns: D (kTcNQ, single-buffered), then A[0], A[1] (K / 4 each)
+  constexpr uint32_t kCols = 512, kACols = K / 4, kA0 = kTcNQ;
   static_assert(kA0 + 2 * kACols <= kCols, "TMEM budget");
   extern __shared__ __align__(16) unsigned char dsm[];  // no-swizzle operands: 16 B alignment
   TcSmem &s = g_tc;
   uint8_t *sB = dsm;                       // [kTcNQ][K]
   const int tid = threadIdx.x, w = tid >> 5;
-  const int row = tid & 127, half = (tid >> 7) & 1, j0 = half * MH;
+  const int row = tid & 127, part = tid >> 7, j0 = part * MH;
   const uint32_t sB_a = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(&s.mbar[0]);
   if (w == 0) {
@@ -1028,14 +1040,14 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (w == 8) {
+  if (w == 4 * G) {
     tc_flusher(a);
   } else {
-  const bool mma_warp = w == 9;
+  const bool mma_warp = w == 4 * G + 1;
   const uint32_t tmem = s.tmem;
   const uint32_t t_row = tmem + ((uint32_t)((w & 3) * 32) << 16);
   const int n_items = *a.n_items;
-  uint32_t ph0 = 0, ph1 = 0;
+  uint32_t ph0 = 0;
   for (;;) {
     const int item = s.item;
     if (item >= n_items) break;
@@ -1045,7 +1057,7 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
     const int64_t ntiles = 2 * (it.chunk_end - it.chunk_begin);
     if (!mma_warp) {
       // ---- stage the item's tables (B operand) and per-query state ----
-      for (int e = tid; e < kTcNQ * MC; e += 256) {
+      for (int e = tid; e < kTcNQ * MC; e += NT) {
         const int q = e / MC, j = e - q * MC;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (q < nq) v = ((const uint4 *)a.qt)[(size_t)a.pair_t[it.pair_begin + q] * MC + j];
@@ -1073,14 +1085,14 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    tc_bar_all();  // B and the query state are staged
+    tc_bar_all<NB>();  // B and the query state are staged
     if (tid == 0) s.item = atomicAdd(a.item_counter, 1);  // claimed ahead (read after the item's end barrier)
     if (mma_warp) {
       const int n_mma = max(16, (nq + 15) & ~15);  // MMA N: the item's queries, rounded to 16
       const uint32_t idesc =
           (2u << 4) | ((uint32_t)(n_mma >> 3) << 17) | ((uint32_t)(kTcCodes >> 4) << 24);
       for (int64_t t = 0; t < ntiles; t++) {
-        tc_sync((int)t);
+        tc_sync<NB>((int)t);
         const int buf = (int)(t & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if ((tid & 31) == 0) {
@@ -1091,12 +1103,12 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
             const uint32_t acc = ks > 0 ? 1u : 0u;
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + buf * kTcNQ),
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
                 "r"(ta), "l"(db), "r"(idesc), "r"(acc));
           }
           asm volatile(
               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                  mbar0 + 8 * buf)
+                  mbar0)
               : "memory");
         }
         __syncwarp();
@@ -1112,49 +1124,62 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
       if (ntiles > 1) tc_load<MC, MH>(a, c0g, kTcCodes + row, j0, cw, vb_next);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
-      tc_arrive(0);
+      tc_arrive<NB>(0);
       for (int64_t t = 0; t < ntiles; t++) {
         const uint32_t vbt = vb;  // valid byte of tile t's octet
         unsigned mpre = 0;
         if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];  // lands during the wait
-        // ---- expand tile t + 1 into A[(t + 1) & 1] (MMA(t - 1), its last
-        // reader, completed before this warp read tile t - 1) ----
+        // ---- expand tile t + 1 into A[(t + 1) & 1] while MMA(t) runs
+        // (MMA(t - 1), its last reader, completed before this warp read
+        // tile t - 1) ----
         if (t + 1 < ntiles) {
-          tc_expand<MH>(a_lane + (uint32_t)((t + 1) & 1) * kACols, cw,
-                        (int)((t + 1) & 1) * kTcCodes + row);
+          if (!(a.dbg & 2)) tc_expand<MH>(a_lane + (uint32_t)((t + 1) & 1) * kACols, cw,
+                                           (int)((t + 1) & 1) * kTcCodes + row);
           vb = vb_next;
           if (t + 2 < ntiles)
             tc_load<MC, MH>(a, c0g + ((t + 2) >> 1), (int)((t + 2) & 1) * kTcCodes + row, j0, cw,
                             vb_next);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          asm volatile("tcgen05.fence::before_thread_sync;");
-          tc_arrive((int)(t + 1));
         }
-        // ---- epilogue of tile t ----
+        // ---- epilogue of tile t (D is single-buffered: MMA(t + 1) waits
+        // for every compute thread's arrive below) ----
         const int buf = (int)(t & 1);
-        tc_wait(mbar0 + 8 * buf, buf ? ph1 : ph0);
-        if (buf) ph1 ^= 1; else ph0 ^= 1;
+        tc_wait(mbar0, ph0);
+        ph0 ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int c = buf * kTcCodes + row;
         const bool valid = (vbt >> (c & 7)) & 1u;
         const int64_t pos = (c0g + (t >> 1)) * kChunkCodes + c;
-        for (int q0 = half * 32; q0 < nq; q0 += 64) {
+        for (int q0 = part * 32; q0 < nq; q0 += 32 * G) {
           uint32_t v[32];
-          tc_ld32(t_row + buf * kTcNQ + q0, v);
-          int mn = 1;
+          tc_ld32(t_row + q0, v);
+          // per group of 4 queries: min over (sum - threshold); a group
+          // with a non-positive minimum holds a survivor
+          int mg[8];
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const int4 t4 = *(const int4 *)&s.thr[q0 + i];
-            mn = min(mn, min(min((int)v[i] - t4.x, (int)v[i + 1] - t4.y),
-                             min((int)v[i + 2] - t4.z, (int)v[i + 3] - t4.w)));
+          for (int g = 0; g < 8; g++) {
+            const int4 t4 = *(const int4 *)&s.thr[q0 + 4 * g];
+            mg[g] = min(min((int)v[4 * g] - t4.x, (int)v[4 * g + 1] - t4.y),
+                        min((int)v[4 * g + 2] - t4.z, (int)v[4 * g + 3] - t4.w));
           }
-          if (valid && mn <= 0) {  // rare once the bounds converge; static indices keep v[] in registers
+          const int mn = min(min(min(mg[0], mg[1]), min(mg[2], mg[3])),
+                             min(min(mg[4], mg[5]), min(mg[6], mg[7])));
+          if (valid && mn <= 0 && !(a.dbg & 1)) {  // rare once the bounds converge
+            // visit only the groups holding a survivor (static indices keep
+            // v[] in registers)
 #pragma unroll
-            for (int i = 0; i < 32; i++)
-              if ((int)v[i] <= s.thr[q0 + i]) tc_hit(a, q0 + i, (int)v[i], pos);
+            for (int g = 0; g < 8; g++) {
+              if (mg[g] > 0) continue;
+#pragma unroll
+              for (int k = 0; k < 4; k++) {
+                const int i = 4 * g + k;
+                if ((int)v[i] <= s.thr[q0 + i]) tc_hit(a, q0 + i, (int)v[i], pos);
+              }
+            }
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
+        if (t + 1 < ntiles) tc_arrive<NB>((int)(t + 1));  // A(t + 1) written, D read
         if (tid < nq && mpre < s.mc[tid]) {  // bounds tightened by the flusher or other CTAs
           s.mc[tid] = mpre;
           const int th = q_threshold(__uint_as_float(mpre), s.qmin[tid], s.delta[tid]);
@@ -1162,7 +1187,7 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
         }
       }
     }
-    tc_bar_all();  // end of item: every tile read, s.item holds the next item
+    tc_bar_all<NB>();  // end of item: every tile read, s.item holds the next item
   }
   if (tid == 0) *(volatile int *)&s.done = 1;
   }
@@ -1175,23 +1200,33 @@ __global__ void __launch_bounds__(320, 1) k_scan_tc(const __grid_constant__ Scan
 template <int MC>
 size_t tc_smem_bytes() { return (size_t)kTcNQ * 16 * MC; }
 
-template <int MC>
-int tc_resident(int nsm) {
+// Compute warp groups of the tensor-core scan: 4 (16 compute warps, each a
+// quarter of the one-hot expansion and of the query columns: latency hidden
+// by 4 warps per scheduler); QADC_B200_TC_GROUPS=2 selects 8 warps.
+int tc_groups() {
+  static const int g = scan_env_int("QADC_B200_TC_GROUPS", 4) == 2 ? 2 : 4;
+  return g;
+}
+
+template <int MC, int G>
+void launch_tc_g(const ScanArgs &a, int nsm, cudaStream_t st) {
   const size_t smem = tc_smem_bytes<MC>();
-  cudaFuncSetAttribute(k_scan_tc<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k_scan_tc<MC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_tc<MC>, 320, smem);
+  cudaFuncSetAttribute(k_scan_tc<MC, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_scan_tc<MC, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   // TMEM: every resident CTA holds all 512 columns of its SM (A and D,
-  // double-buffered)
-  per_sm = 1;
-  return nsm * per_sm;
+  // double-buffered): one CTA per SM
+  k_scan_tc<MC, G><<<nsm, 128 * G + 64, smem, st>>>(a);
 }
 
 template <int MC>
 void launch_tc(const ScanArgs &a, int nsm, cudaStream_t st) {
-  const int grid = tc_resident<MC>(nsm);
-  k_scan_tc<MC><<<grid, 320, tc_smem_bytes<MC>(), st>>>(a);
+  if (tc_groups() == 2) launch_tc_g<MC, 2>(a, nsm, st);
+  else launch_tc_g<MC, 4>(a, nsm, st);
+}
+
+template <int MC>
+int tc_resident(int nsm) {
+  return nsm;
 }
 
 // ---- work list construction ----
