@@ -771,7 +771,7 @@ void launch_t(const ScanArgs &a, int nsm, cudaStream_t st) {
 // SBO = 8K B).
 constexpr int kTcCodes = 128;  // codes per tile (MMA M)
 constexpr int kTcNQ = 256;     // queries per item (max MMA N)
-constexpr int kRing = 1024;    // survivor ring between the compute warps and the flusher warp
+constexpr int kRing = 2048;    // survivor ring between the compute warps and the flusher warp
 
 __device__ __forceinline__ uint64_t tc_smem_desc(uint32_t saddr, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) |
@@ -787,17 +787,20 @@ __device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase) {
       : "memory");
 }
 
-__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+// 64 accumulator columns of the thread's TMEM lane, low 16 bits of each,
+// two adjacent columns per register (column 2i in the low half of v[i]).
+// Sums are < 2^13, so the 16-bit halves are exact. No wait: the caller
+// issues tcgen05.wait::ld once for all its loads.
+__device__ __forceinline__ void tc_ld64p(uint32_t taddr, uint32_t *v) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+      "%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
         "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
         "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
         "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
 struct TcEntry {
@@ -816,7 +819,9 @@ struct TcSmem {
   int query[kTcNQ];
   float qmin[kTcNQ];
   float delta[kTcNQ];
-  __align__(16) int thr[kTcNQ];
+  // per-query threshold t as t + 0x8000 (t in [-1, 254]); read as packed
+  // pairs by the epilogue's SWAR test
+  __align__(16) uint16_t thr16[kTcNQ];
   unsigned mc[kTcNQ];  // cached global bound M (bits)
   TcEntry ring[kRing];
 };
@@ -844,14 +849,14 @@ __device__ __forceinline__ void tc_put(const ScanArgs &a, int query, float mid, 
 // Survivor of the epilogue: pushed to the shared-memory ring drained by the
 // flusher warp (no global round trip on the tile's critical path). Each
 // thread checks the ring's room before reserving and has at most one
-// reservation in flight, so 256 slots of slack make the reservation safe; a
+// reservation in flight, so 512 slots of slack (one per compute thread) make the reservation safe; a
 // full ring falls back to a direct append.
 __device__ __noinline__ void tc_hit(const ScanArgs &a, int q, int v, int64_t pos) {
   const float mid = midpoint(g_tc.qmin[q], g_tc.delta[q], v);
   if (!(mid <= __uint_as_float(g_tc.mc[q]))) return;
   const int query = g_tc.query[q];
   const unsigned h = *(volatile unsigned *)&g_tc.head, t = *(volatile unsigned *)&g_tc.tail;
-  if (h - t < (unsigned)(kRing - 256)) {
+  if (h - t < (unsigned)(kRing - 512)) {
     const unsigned k = atomicAdd(&g_tc.head, 1u);
     TcEntry &e = g_tc.ring[k % kRing];
     e.mid = mid;
@@ -967,12 +972,11 @@ __device__ __forceinline__ void tc_expand(uint32_t a_col, const uint32_t (&cw)[M
 
 template <int MC, int MH>
 __device__ __forceinline__ void tc_load(const ScanArgs &a, int64_t g, int c, int j0,
-                                        uint32_t (&cw)[MH], uint32_t &vb) {
+                                        uint32_t (&cw)[MH]) {
   if (a.dbg & 4) g = 0;  // timing experiment: every tile reads chunk 0 (L1/L2 resident)
   const uint32_t *p = a.codes + ((size_t)g * MC + j0) * 32 + (c >> 3);
 #pragma unroll
   for (int j = 0; j < MH; j++) cw[j] = __ldg(p + j * 32);
-  vb = __ldg(a.valid + g * 32 + (c >> 3));
 }
 
 // Named barriers over the compute warps and the MMA warp (NB threads).
@@ -1010,6 +1014,8 @@ template <int MC, int G>
 __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_constant__ ScanArgs a) {
   constexpr int K = 16 * MC, SBO = 8 * K, MH = MC / G;
   constexpr int NT = 128 * G, NB = NT + 32;  // compute threads; + the MMA warp
+  constexpr int kCPT = kTcNQ / G;             // accumulator columns per compute thread
+  static_assert(kCPT % 64 == 0, "64-column packed TMEM loads");
   static_assert(MH % 4 == 0 && kTcNQ % (32 * G) == 0, "tile split");
   // TMEM columns: D (kTcNQ, single-buffered), then A[0], A[1] (K / 4 each)
   constexpr uint32_t kCols = 512, kACols = K / 4, kA0 = kTcNQ;
@@ -1018,7 +1024,7 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
   TcSmem &s = g_tc;
   uint8_t *sB = dsm;                       // [kTcNQ][K]
   const int tid = threadIdx.x, w = tid >> 5;
-  const int row = tid & 127, part = tid >> 7, j0 = part * MH;
+  const int row = tid & 127, part = tid >> 7, j0 = part * MH, col0 = part * kCPT;
   const uint32_t sB_a = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(&s.mbar[0]);
   if (w == 0) {
@@ -1048,6 +1054,22 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
   const uint32_t t_row = tmem + ((uint32_t)((w & 3) * 32) << 16);
   const int n_items = *a.n_items;
   uint32_t ph0 = 0;
+  if (!mma_warp) {
+    // zero this thread's accumulator columns once: columns an item's MMA
+    // does not write (>= its N) then always hold real sums (< 2^13) from an
+    // earlier item, which the SWAR test compares against t = -1
+    const uint32_t z[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < kCPT; c += 16)
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+          "%13,%14,%15,%16};" ::"r"(t_row + col0 + c),
+          "r"(z[0]), "r"(z[1]), "r"(z[2]), "r"(z[3]), "r"(z[4]), "r"(z[5]), "r"(z[6]), "r"(z[7]),
+          "r"(z[8]), "r"(z[9]), "r"(z[10]), "r"(z[11]), "r"(z[12]), "r"(z[13]), "r"(z[14]),
+          "r"(z[15])
+          : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
   for (;;) {
     const int item = s.item;
     if (item >= n_items) break;
@@ -1080,7 +1102,7 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
           s.qmin[q] = 0.f;
           s.delta[q] = 0.f;
         }
-        s.thr[q] = thr;
+        s.thr16[q] = (uint16_t)(thr + 0x8000);
         s.mc[q] = mb;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1114,19 +1136,18 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
         __syncwarp();
       }
     } else {
-      uint32_t cw[MH], vb_next = 0, vb = 0;
-      // this thread's A columns (its lane quarter, its half of the K range)
+      uint32_t cw[MH];
+      // this thread's A columns (its lane quarter, its part of the K range)
       const uint32_t a_lane = tmem + ((uint32_t)((w & 3) * 32) << 16) + kA0 + (uint32_t)(j0 * 4);
+      const int n_mma = max(16, (nq + 15) & ~15);
       // prologue: expand tile 0 into A[0], load tile 1's words
-      tc_load<MC, MH>(a, c0g, row, j0, cw, vb_next);
+      tc_load<MC, MH>(a, c0g, row, j0, cw);
       tc_expand<MH>(a_lane, cw, row);
-      vb = vb_next;
-      if (ntiles > 1) tc_load<MC, MH>(a, c0g, kTcCodes + row, j0, cw, vb_next);
+      if (ntiles > 1) tc_load<MC, MH>(a, c0g, kTcCodes + row, j0, cw);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       tc_arrive<NB>(0);
       for (int64_t t = 0; t < ntiles; t++) {
-        const uint32_t vbt = vb;  // valid byte of tile t's octet
         unsigned mpre = 0;
         if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];  // lands during the wait
         // ---- expand tile t + 1 into A[(t + 1) & 1] while MMA(t) runs
@@ -1135,55 +1156,64 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
         if (t + 1 < ntiles) {
           if (!(a.dbg & 2)) tc_expand<MH>(a_lane + (uint32_t)((t + 1) & 1) * kACols, cw,
                                            (int)((t + 1) & 1) * kTcCodes + row);
-          vb = vb_next;
           if (t + 2 < ntiles)
-            tc_load<MC, MH>(a, c0g + ((t + 2) >> 1), (int)((t + 2) & 1) * kTcCodes + row, j0, cw,
-                            vb_next);
+            tc_load<MC, MH>(a, c0g + ((t + 2) >> 1), (int)((t + 2) & 1) * kTcCodes + row, j0, cw);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
-        // ---- epilogue of tile t (D is single-buffered: MMA(t + 1) waits
-        // for every compute thread's arrive below) ----
-        const int buf = (int)(t & 1);
+        // ---- tile t: copy this thread's sums out of TMEM and release D
+        // (MMA(t + 1) waits for every compute thread's arrive), then test
+        // them from registers while MMA(t + 1) runs ----
         tc_wait(mbar0, ph0);
         ph0 ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const int c = buf * kTcCodes + row;
-        const bool valid = (vbt >> (c & 7)) & 1u;
-        const int64_t pos = (c0g + (t >> 1)) * kChunkCodes + c;
-        for (int q0 = part * 32; q0 < nq; q0 += 32 * G) {
-          uint32_t v[32];
-          tc_ld32(t_row + q0, v);
-          // per group of 4 queries: min over (sum - threshold); a group
-          // with a non-positive minimum holds a survivor
-          int mg[8];
+        uint32_t v[kCPT / 2];
 #pragma unroll
-          for (int g = 0; g < 8; g++) {
-            const int4 t4 = *(const int4 *)&s.thr[q0 + 4 * g];
-            mg[g] = min(min((int)v[4 * g] - t4.x, (int)v[4 * g + 1] - t4.y),
-                        min((int)v[4 * g + 2] - t4.z, (int)v[4 * g + 3] - t4.w));
+        for (int l = 0; l < kCPT / 64; l++) {
+          if (col0 + 64 * l < n_mma) tc_ld64p(t_row + col0 + 64 * l, v + 32 * l);
+          else {
+#pragma unroll
+            for (int i = 0; i < 32; i++) v[32 * l + i] = 0;
           }
-          const int mn = min(min(min(mg[0], mg[1]), min(mg[2], mg[3])),
-                             min(min(mg[4], mg[5]), min(mg[6], mg[7])));
-          if (valid && mn <= 0 && !(a.dbg & 1)) {  // rare once the bounds converge
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        if (t + 1 < ntiles) tc_arrive<NB>((int)(t + 1));  // A(t + 1) written, D read
+        // SWAR survivor test on packed pairs: (t + 0x8000) - s keeps bit
+        // 15 of its half iff s <= t (halves never borrow: s < 2^13 and
+        // t + 0x8000 in [0x7fff, 0x80fe])
+        const uint4 *T = (const uint4 *)&s.thr16[col0];
+        uint32_t any = 0;
+#pragma unroll
+        for (int i = 0; i < kCPT / 2; i += 4) {
+          const uint4 tt = T[i / 4];
+          any |= (tt.x - v[i]) | (tt.y - v[i + 1]) | (tt.z - v[i + 2]) | (tt.w - v[i + 3]);
+        }
+        if ((any & 0x80008000u) && !(a.dbg & 1)) {  // rare once the bounds converge
+          const int c = (int)(t & 1) * kTcCodes + row;
+          const int64_t g = c0g + (t >> 1);
+          const uint32_t vb = __ldg(a.valid + g * 32 + (c >> 3));
+          if ((vb >> (c & 7)) & 1u) {
+            const int64_t pos = g * kChunkCodes + c;
             // visit only the groups holding a survivor (static indices keep
             // v[] in registers)
 #pragma unroll
-            for (int g = 0; g < 8; g++) {
-              if (mg[g] > 0) continue;
+            for (int i = 0; i < kCPT / 2; i += 4) {
+              const uint4 tt = T[i / 4];
+              const uint32_t x[4] = {tt.x - v[i], tt.y - v[i + 1], tt.z - v[i + 2], tt.w - v[i + 3]};
+              if (!((x[0] | x[1] | x[2] | x[3]) & 0x80008000u)) continue;
 #pragma unroll
               for (int k = 0; k < 4; k++) {
-                const int i = 4 * g + k;
-                if ((int)v[i] <= s.thr[q0 + i]) tc_hit(a, q0 + i, (int)v[i], pos);
+                const int q = col0 + 2 * (i + k);
+                if (x[k] & 0x8000u) tc_hit(a, q, (int)(v[i + k] & 0xffffu), pos);
+                if (x[k] & 0x80000000u) tc_hit(a, q + 1, (int)(v[i + k] >> 16), pos);
               }
             }
           }
         }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        if (t + 1 < ntiles) tc_arrive<NB>((int)(t + 1));  // A(t + 1) written, D read
         if (tid < nq && mpre < s.mc[tid]) {  // bounds tightened by the flusher or other CTAs
           s.mc[tid] = mpre;
           const int th = q_threshold(__uint_as_float(mpre), s.qmin[tid], s.delta[tid]);
-          if (th < s.thr[tid]) s.thr[tid] = th;
+          if (th + 0x8000 < (int)s.thr16[tid]) s.thr16[tid] = (uint16_t)(th + 0x8000);
         }
       }
     }
