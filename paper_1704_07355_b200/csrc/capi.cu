@@ -325,6 +325,10 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   cudaEventCreate(&e1);
   cudaEventRecord(e0, st);
   launch_scan(a, nsm, st, prmt);
+  if (tc_dbg & 64) {
+    cudaStreamSynchronize(st);
+    tc_stats_dump();
+  }
   ss.scan_tc = scan_use_tc(m, prmt) ? 1 : 0;
   QADC_CUDA(cudaGetLastError());
   cudaEventRecord(e1, st);

@@ -147,6 +147,7 @@ int scan_qt_per_cta(int m);
 // Tensor-core scan in use for this m; queries per work item of the scan.
 // prmt: the caller asked for the PRMT kernel (QADC_B200_SCAN_PRMT).
 bool scan_use_tc(int m, bool prmt);
+void tc_stats_dump();  // debug counters of the tensor-core scan (QADC_B200_TC_DEBUG & 64)
 int scan_tile_queries(int m, bool prmt);
 // Resident scan CTAs on the device (occupancy x SMs) for this shape.
 int scan_resident_ctas(int m, int cap_l, int nsm, int linear, bool prmt);

@@ -823,8 +823,12 @@ struct TcSmem {
   // pairs by the epilogue's SWAR test
   __align__(16) uint16_t thr16[kTcNQ];
   unsigned mc[kTcNQ];  // cached global bound M (bits)
+  __align__(16) uint32_t xfer[16][32];  // per compute warp: one lane's packed sums
   TcEntry ring[kRing];
 };
+// debug counters (QADC_B200_TC_DEBUG bit 64): slow-path entries, hits, ring
+// pushes, direct appends
+__device__ unsigned long long g_tc_stats[4];
 // one instance per CTA of k_scan_tc (file-scope: direct shared addressing
 // from every helper)
 __shared__ TcSmem g_tc;
@@ -846,25 +850,43 @@ __device__ __forceinline__ void tc_put(const ScanArgs &a, int query, float mid, 
   }
 }
 
-// Survivor of the epilogue: pushed to the shared-memory ring drained by the
-// flusher warp (no global round trip on the tile's critical path). Each
-// thread checks the ring's room before reserving and has at most one
-// reservation in flight, so 512 slots of slack (one per compute thread) make the reservation safe; a
-// full ring falls back to a direct append.
-__device__ __noinline__ void tc_hit(const ScanArgs &a, int q, int v, int64_t pos) {
-  const float mid = midpoint(g_tc.qmin[q], g_tc.delta[q], v);
-  if (!(mid <= __uint_as_float(g_tc.mc[q]))) return;
+// Survivors of the epilogue, one candidate per lane (want = the lane has
+// one): pushed to the shared-memory ring drained by the flusher warp (no
+// global round trip on the tile's critical path). Warp-converged: one slot
+// claim per warp. Each warp checks the ring's room before reserving and has
+// at most one reservation (<= 32 slots) in flight, so 16 x 32 = 512 slots of
+// slack make the reservation safe; a full ring falls back to direct appends.
+__device__ __forceinline__ void tc_hit_warp(const ScanArgs &a, bool want, int q, int v,
+                                            int64_t pos) {
+  const int lane = threadIdx.x & 31;
+  float mid = 0.f;
+  if (want) {
+    mid = midpoint(g_tc.qmin[q], g_tc.delta[q], v);
+    if (a.dbg & 64) atomicAdd(&g_tc_stats[1], 1ull);
+    want = mid <= __uint_as_float(g_tc.mc[q]) && !(a.dbg & 32);
+  }
+  const unsigned hm = __ballot_sync(kFull, want);
+  if (!hm) return;
+  const int leader = __ffs(hm) - 1;
+  unsigned base = 0xffffffffu;
+  if (lane == leader) {
+    const unsigned h = *(volatile unsigned *)&g_tc.head, t = *(volatile unsigned *)&g_tc.tail;
+    if (h - t < (unsigned)(kRing - 512)) base = atomicAdd(&g_tc.head, (unsigned)__popc(hm));
+  }
+  base = __shfl_sync(kFull, base, leader);
+  if (!want) return;
   const int query = g_tc.query[q];
-  const unsigned h = *(volatile unsigned *)&g_tc.head, t = *(volatile unsigned *)&g_tc.tail;
-  if (h - t < (unsigned)(kRing - 512)) {
-    const unsigned k = atomicAdd(&g_tc.head, 1u);
+  if (base != 0xffffffffu) {
+    const unsigned k = base + __popc(hm & ((1u << lane) - 1u));
     TcEntry &e = g_tc.ring[k % kRing];
     e.mid = mid;
     e.pos = pos;
-    __threadfence_block();
+    if (!(a.dbg & 16)) __threadfence_block();
     *(volatile int *)&e.query = query;
+    if (a.dbg & 64) atomicAdd(&g_tc_stats[2], 1ull);
     return;
   }
+  if (a.dbg & 64) atomicAdd(&g_tc_stats[3], 1ull);
   tc_put(a, query, mid, pos, atomicAdd(&a.cand_n[query], 1u));
 }
 
@@ -1016,7 +1038,7 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
   constexpr int NT = 128 * G, NB = NT + 32;  // compute threads; + the MMA warp
   constexpr int kCPT = kTcNQ / G;             // accumulator columns per compute thread
   static_assert(kCPT % 64 == 0, "64-column packed TMEM loads");
-  static_assert(MH % 4 == 0 && kTcNQ % (32 * G) == 0, "tile split");
+  static_assert(MH % 4 == 0 && kTcNQ % (32 * G) == 0 && 4 * G <= 16, "tile split");
   // TMEM columns: D (kTcNQ, single-buffered), then A[0], A[1] (K / 4 each)
   constexpr uint32_t kCols = 512, kACols = K / 4, kA0 = kTcNQ;
   static_assert(kA0 + 2 * kACols <= kCols, "TMEM budget");
@@ -1139,7 +1161,6 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
       uint32_t cw[MH];
       // this thread's A columns (its lane quarter, its part of the K range)
       const uint32_t a_lane = tmem + ((uint32_t)((w & 3) * 32) << 16) + kA0 + (uint32_t)(j0 * 4);
-      const int n_mma = max(16, (nq + 15) & ~15);
       // prologue: expand tile 0 into A[0], load tile 1's words
       tc_load<MC, MH>(a, c0g, row, j0, cw);
       tc_expand<MH>(a_lane, cw, row);
@@ -1150,6 +1171,11 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
       for (int64_t t = 0; t < ntiles; t++) {
         unsigned mpre = 0;
         if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];  // lands during the wait
+        // valid byte of this thread's code in tile t (lands during the wait;
+        // read only by the survivor path)
+        const int c_t = (int)(t & 1) * kTcCodes + row;
+        const int64_t g_t = c0g + (t >> 1);
+        const uint32_t vb_t = __ldg(a.valid + g_t * 32 + (c_t >> 3));
         // ---- expand tile t + 1 into A[(t + 1) & 1] while MMA(t) runs
         // (MMA(t - 1), its last reader, completed before this warp read
         // tile t - 1) ----
@@ -1166,15 +1192,11 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
         tc_wait(mbar0, ph0);
         ph0 ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;");
+        // (columns >= the MMA's N hold earlier items' sums: see the zeroing
+        // above)
         uint32_t v[kCPT / 2];
 #pragma unroll
-        for (int l = 0; l < kCPT / 64; l++) {
-          if (col0 + 64 * l < n_mma) tc_ld64p(t_row + col0 + 64 * l, v + 32 * l);
-          else {
-#pragma unroll
-            for (int i = 0; i < 32; i++) v[32 * l + i] = 0;
-          }
-        }
+        for (int l = 0; l < kCPT / 64; l++) tc_ld64p(t_row + col0 + 64 * l, v + 32 * l);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
         if (t + 1 < ntiles) tc_arrive<NB>((int)(t + 1));  // A(t + 1) written, D read
@@ -1184,29 +1206,38 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
         const uint4 *T = (const uint4 *)&s.thr16[col0];
         uint32_t any = 0;
 #pragma unroll
-        for (int i = 0; i < kCPT / 2; i += 4) {
+        for (int i = 0; i < kCPT / 2 && !(a.dbg & 8); i += 4) {
           const uint4 tt = T[i / 4];
           any |= (tt.x - v[i]) | (tt.y - v[i + 1]) | (tt.z - v[i + 2]) | (tt.w - v[i + 3]);
         }
-        if ((any & 0x80008000u) && !(a.dbg & 1)) {  // rare once the bounds converge
-          const int c = (int)(t & 1) * kTcCodes + row;
-          const int64_t g = c0g + (t >> 1);
-          const uint32_t vb = __ldg(a.valid + g * 32 + (c >> 3));
-          if ((vb >> (c & 7)) & 1u) {
-            const int64_t pos = g * kChunkCodes + c;
-            // visit only the groups holding a survivor (static indices keep
-            // v[] in registers)
+        // survivors (rare once the bounds converge): the warp handles its
+        // lanes with survivors one at a time, each of the lane's packed
+        // sum registers passed through shared memory to a lane of its own
+        unsigned todo = __ballot_sync(kFull, (any & 0x80008000u) && ((vb_t >> (c_t & 7)) & 1u) &&
+                                                 !(a.dbg & 1));
+        if (todo) {
+          const int lane = tid & 31;
+          uint32_t *xf = s.xfer[w];
+          const int64_t pos0 = g_t * kChunkCodes + (int64_t)(c_t - lane);
+          while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            if (a.dbg & 64 && lane == src) atomicAdd(&g_tc_stats[0], 1ull);
 #pragma unroll
-            for (int i = 0; i < kCPT / 2; i += 4) {
-              const uint4 tt = T[i / 4];
-              const uint32_t x[4] = {tt.x - v[i], tt.y - v[i + 1], tt.z - v[i + 2], tt.w - v[i + 3]};
-              if (!((x[0] | x[1] | x[2] | x[3]) & 0x80008000u)) continue;
+            for (int r = 0; r < kCPT / 64; r++) {
+              if (lane == src) {
 #pragma unroll
-              for (int k = 0; k < 4; k++) {
-                const int q = col0 + 2 * (i + k);
-                if (x[k] & 0x8000u) tc_hit(a, q, (int)(v[i + k] & 0xffffu), pos);
-                if (x[k] & 0x80000000u) tc_hit(a, q + 1, (int)(v[i + k] >> 16), pos);
+                for (int i = 0; i < 32; i += 4)
+                  *(uint4 *)&xf[i] = make_uint4(v[32 * r + i], v[32 * r + i + 1], v[32 * r + i + 2],
+                                                v[32 * r + i + 3]);
               }
+              __syncwarp();
+              const uint32_t vv = xf[lane];
+              const int q = col0 + 64 * r + 2 * lane;
+              const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
+              __syncwarp();
+              tc_hit_warp(a, (x & 0x8000u) != 0, q, (int)(vv & 0xffffu), pos0 + src);
+              tc_hit_warp(a, (x & 0x80000000u) != 0, q + 1, (int)(vv >> 16), pos0 + src);
             }
           }
         }
@@ -1484,6 +1515,15 @@ int scan_qt_per_cta(int m) {
 
 // Tensor-core scan for m in {16, 32}; the PRMT kernel otherwise, or when the
 // call asks for it (QADC_B200_SCAN_PRMT) or QADC_B200_TC=0.
+void tc_stats_dump() {
+  unsigned long long h[4] = {0, 0, 0, 0};
+  cudaMemcpyFromSymbol(h, g_tc_stats, sizeof(h));
+  fprintf(stderr, "qadc_b200 tc stats: slow-path entries %llu, hits %llu, ring pushes %llu, direct %llu\n",
+          h[0], h[1], h[2], h[3]);
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_tc_stats, z, sizeof(z));
+}
+
 bool scan_use_tc(int m, bool prmt) {
   static const int env = scan_env_int("QADC_B200_TC", 1);
   return !prmt && env != 0 && (m == 16 || m == 32);
