@@ -675,9 +675,9 @@ __global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ cod
     for (int e = threadIdx.x; e < m * 4; e += blockDim.x)
       ((uint32_t *)sqt)[e] = qt[(size_t)pair * m * 4 + e];
     __syncthreads();
-    const int64_t need_end = pref;
+    // (1) stream order, only until R valid lanes are seen
     for (int64_t base = 0; base < n; base += blockDim.x) {
-      if (s_seen >= R && base >= need_end) break;
+      if (s_seen >= R) break;
       const int64_t k = base + threadIdx.x;
       bool valid = false;
       int qv = 255;
@@ -708,11 +708,30 @@ __global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ cod
           fsat_id[(size_t)q * R + p] = id;
         }
       }
-      if (valid && k < pref && qv < 255) atomicAdd(&hist[qv], 1u);
       __syncthreads();
       if (threadIdx.x == 0) s_seen += total;
       __syncthreads();
     }
+    // (2) bound histogram of the prefix: one octet (8 codes) per thread,
+    // each interleaved word read once (coalesced across the CTA)
+    for (int64_t o = threadIdx.x; o * 8 < pref; o += blockDim.x) {
+      const int64_t g = c0 + o / 32;
+      const uint32_t *wp = codes + g * m * 32 + (o % 32);
+      uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int j = 0; j < m; j++) {
+        const uint32_t w = __ldg(wp + j * 32);
+        const unsigned char *row = sqt + j * 16;
+#pragma unroll
+        for (int k = 0; k < 8; k++) acc[k] += row[(w >> (4 * k)) & 15];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const int64_t kk = o * 8 + k;
+        if (kk < pref && acc[k] < 255 && ids[c0 * kChunkCodes + kk] >= 0)
+          atomicAdd(&hist[acc[k]], 1u);
+      }
+    }
+    __syncthreads();
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -856,38 +856,52 @@ __device__ __forceinline__ void tc_put(const ScanArgs &a, int query, float mid, 
 // claim per warp. Each warp checks the ring's room before reserving and has
 // at most one reservation (<= 32 slots) in flight, so 16 x 32 = 512 slots of
 // slack make the reservation safe; a full ring falls back to direct appends.
-__device__ __forceinline__ void tc_hit_warp(const ScanArgs &a, bool want, int q, int v,
-                                            int64_t pos) {
+__device__ __forceinline__ void tc_hit_warp(const ScanArgs &a, bool w0, bool w1, int q,
+                                            uint32_t vv, int64_t pos) {
   const int lane = threadIdx.x & 31;
-  float mid = 0.f;
-  if (want) {
-    mid = midpoint(g_tc.qmin[q], g_tc.delta[q], v);
-    if (a.dbg & 64) atomicAdd(&g_tc_stats[1], 1ull);
-    want = mid <= __uint_as_float(g_tc.mc[q]) && !(a.dbg & 32);
+  float mid0 = 0.f, mid1 = 0.f;
+  if (w0) {
+    mid0 = midpoint(g_tc.qmin[q], g_tc.delta[q], (int)(vv & 0xffffu));
+    w0 = mid0 <= __uint_as_float(g_tc.mc[q]) && !(a.dbg & 32);
   }
-  const unsigned hm = __ballot_sync(kFull, want);
-  if (!hm) return;
-  const int leader = __ffs(hm) - 1;
+  if (w1) {
+    mid1 = midpoint(g_tc.qmin[q + 1], g_tc.delta[q + 1], (int)(vv >> 16));
+    w1 = mid1 <= __uint_as_float(g_tc.mc[q + 1]) && !(a.dbg & 32);
+  }
+  const unsigned b0 = __ballot_sync(kFull, w0), b1 = __ballot_sync(kFull, w1);
+  if (!(b0 | b1)) return;
+  const int leader = __ffs(b0 | b1) - 1;
   unsigned base = 0xffffffffu;
   if (lane == leader) {
     const unsigned h = *(volatile unsigned *)&g_tc.head, t = *(volatile unsigned *)&g_tc.tail;
-    if (h - t < (unsigned)(kRing - 512)) base = atomicAdd(&g_tc.head, (unsigned)__popc(hm));
+    if (h - t < (unsigned)(kRing - 512))
+      base = atomicAdd(&g_tc.head, (unsigned)(__popc(b0) + __popc(b1)));
   }
   base = __shfl_sync(kFull, base, leader);
-  if (!want) return;
-  const int query = g_tc.query[q];
+  if (!(w0 || w1)) return;
+  if (a.dbg & 64) atomicAdd(&g_tc_stats[1], (unsigned long long)(w0 + w1));
   if (base != 0xffffffffu) {
-    const unsigned k = base + __popc(hm & ((1u << lane) - 1u));
-    TcEntry &e = g_tc.ring[k % kRing];
-    e.mid = mid;
-    e.pos = pos;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned k = base + __popc(b0 & lt) + __popc(b1 & lt);
+    TcEntry &e0 = g_tc.ring[k % kRing];
+    TcEntry &e1 = g_tc.ring[(k + (w0 ? 1u : 0u)) % kRing];
+    if (w0) {
+      e0.mid = mid0;
+      e0.pos = pos;
+    }
+    if (w1) {
+      e1.mid = mid1;
+      e1.pos = pos;
+    }
     if (!(a.dbg & 16)) __threadfence_block();
-    *(volatile int *)&e.query = query;
-    if (a.dbg & 64) atomicAdd(&g_tc_stats[2], 1ull);
+    if (w0) *(volatile int *)&e0.query = g_tc.query[q];
+    if (w1) *(volatile int *)&e1.query = g_tc.query[q + 1];
+    if (a.dbg & 64) atomicAdd(&g_tc_stats[2], (unsigned long long)(w0 + w1));
     return;
   }
-  if (a.dbg & 64) atomicAdd(&g_tc_stats[3], 1ull);
-  tc_put(a, query, mid, pos, atomicAdd(&a.cand_n[query], 1u));
+  if (a.dbg & 64) atomicAdd(&g_tc_stats[3], (unsigned long long)(w0 + w1));
+  if (w0) tc_put(a, g_tc.query[q], mid0, pos, atomicAdd(&a.cand_n[g_tc.query[q]], 1u));
+  if (w1) tc_put(a, g_tc.query[q + 1], mid1, pos, atomicAdd(&a.cand_n[g_tc.query[q + 1]], 1u));
 }
 
 // Flusher warp: drains the ring into the global candidate lists (4 entries
@@ -1236,8 +1250,7 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
               const int q = col0 + 64 * r + 2 * lane;
               const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
               __syncwarp();
-              tc_hit_warp(a, (x & 0x8000u) != 0, q, (int)(vv & 0xffffu), pos0 + src);
-              tc_hit_warp(a, (x & 0x80000000u) != 0, q + 1, (int)(vv >> 16), pos0 + src);
+              tc_hit_warp(a, (x & 0x8000u) != 0, (x & 0x80000000u) != 0, q, vv, pos0 + src);
             }
           }
         }
