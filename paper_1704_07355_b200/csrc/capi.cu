@@ -246,12 +246,15 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   const int cap_l = (std::max(R + 128, 256) + 31) / 32 * 32;
   const int linear = scan_env_int("QADC_B200_LINEAR", -1) >= 0 ? scan_env_int("QADC_B200_LINEAR", 0)
                                                                  : (avg_chunks >= 64 ? 1 : 0);
+  // one exhaustive list on the tensor-core scan: CTA pairs (k_scan_tc2)
+  static const int tc2_env = scan_env_int("QADC_B200_TC2", 1);
+  const int pair_cta = (tc2_env && nl == 1 && scan_use_tc(m, prmt) && nsm >= 2) ? 1 : 0;
   if (nl == 1 && idx->total_chunks > 0) {
     // one exhaustive list: equal-size items, so the persistent CTAs finish
     // together only if the item count fills whole waves. Pick the range
     // count r minimising waves x (chunks per item + per-item overhead).
     const int64_t tiles = (npairs + qt_tile - 1) / qt_tile;
-    const int64_t ctas = scan_resident_ctas(m, cap_l, nsm, linear, prmt);
+    const int64_t ctas = pair_cta ? nsm / 2 : scan_resident_ctas(m, cap_l, nsm, linear, prmt);
     const int64_t ch = idx->total_chunks;
     int64_t best_r = 1;
     double best = 1e300;
@@ -320,6 +323,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   a.linear = linear;  // long items (>= 64 chunks per list on average)
   static const int tc_dbg = scan_env_int("QADC_B200_TC_DEBUG", 0);
   a.dbg = tc_dbg;
+  a.pair_cta = pair_cta;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
