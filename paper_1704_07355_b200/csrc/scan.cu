@@ -781,9 +781,9 @@ __device__ __forceinline__ uint64_t tc_smem_desc(uint32_t saddr, uint32_t sbo) {
 __device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\tTC_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@P1 bra TC_DONE;\n\tbra TC_WAIT;\n\tTC_DONE:\n\t}" ::"r"(mbar),
-      "r"(phase)
+      "r"(phase), "n"(1000000)  // suspend-time hint (ns): the warp sleeps instead of spinning
       : "memory");
 }
 
