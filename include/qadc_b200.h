@@ -144,6 +144,9 @@ QADC_API int64_t qadc_b200_index_bytes(const qadc_b200_index *idx);
 #define QADC_B200_SCAN_TC 16u  /* tensor-core scan (m = 16, 32) even with few
                                   (query, list) pairs per list; default: the
                                   tensor cores from 64 pairs per list on */
+#define QADC_B200_SCAN_TC1 32u /* with the tensor-core scan of one exhaustive
+                                  list: one SM per tile instead of CTA pairs
+                                  (cta_group::2, the default) */
 
 /*
  * adc.py:114-187 search(method="qadc") for nq queries at once:

@@ -26,6 +26,7 @@ LUT_IN = 2
 NO_FSAT = 4
 SCAN_PRMT = 8  # force the PRMT (CUDA-core) scan kernel
 SCAN_TC = 16  # force the int8 tensor-core scan kernel (m = 16, 32)
+SCAN_TC1 = 32  # tensor-core scan of an exhaustive list on one SM per tile (not CTA pairs)
 
 _lib = None
 

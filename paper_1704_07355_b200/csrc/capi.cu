@@ -150,7 +150,7 @@ void retain_pool_memory() {
 int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int ma, int init,
                 const float *lut_in, const int64_t *cells_in, int64_t *out_ids, float *out_d,
                 int32_t *out_n, cudaStream_t st, SearchStats &ss, const unsigned *M_override,
-                int cap_g, int depth, bool no_fsat, bool prmt, bool force_tc) {
+                int cap_g, int depth, bool no_fsat, bool prmt, bool force_tc, bool one_sm) {
   if (nq == 0) return kOk;
   const int m = idx->m;
   const int nslots = idx->K ? ma : 1;
@@ -248,7 +248,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
                                                                  : (avg_chunks >= 64 ? 1 : 0);
   // one exhaustive list on the tensor-core scan: CTA pairs (k_scan_tc2)
   static const int tc2_env = scan_env_int("QADC_B200_TC2", 1);
-  const int pair_cta = (tc2_env && nl == 1 && scan_use_tc(m, prmt) && nsm >= 2) ? 1 : 0;
+  const int pair_cta = (tc2_env && !one_sm && nl == 1 && scan_use_tc(m, prmt) && nsm >= 2) ? 1 : 0;
   if (nl == 1 && idx->total_chunks > 0) {
     // one exhaustive list: equal-size items, so the persistent CTAs finish
     // together only if the item count fills whole waves. Pick the range
@@ -414,7 +414,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
     const int cap2 = (int)std::min<int64_t>(std::max<int64_t>((int64_t)need + 1024, 2LL * cap_g),
                                             (int64_t)1 << 28);
     rc = search_impl(idx, sub_q.p, nr, R, ma, init, lp, cp, sub_ids.p, sub_d.p, sub_n.p, st, ss,
-                     sub_M.p, cap2, depth + 1, no_fsat, prmt, force_tc);
+                     sub_M.p, cap2, depth + 1, no_fsat, prmt, force_tc, one_sm);
     if (rc) return rc;
     k_scatter_out<<<gridn((int64_t)nr * R), 256, 0, st>>>(sub_ids.p, sub_d.p, sub_n.p, rows.p, nr,
                                                           R, out_ids, out_d, out_n);
@@ -808,7 +808,7 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
       std::max<int64_t>({8192, 8LL * R, std::min<int64_t>(65536, cap_mem)}), 1 << 20);
   int rc = search_impl(idx, q, nq, R, ma, init, lin, cin, oi, od, on, st, ss, nullptr, cap_g, 0,
                        (flags & QADC_B200_NO_FSAT) != 0, (flags & QADC_B200_SCAN_PRMT) != 0,
-                       (flags & QADC_B200_SCAN_TC) != 0);
+                       (flags & QADC_B200_SCAN_TC) != 0, (flags & QADC_B200_SCAN_TC1) != 0);
   if (rc) return rc;
   if (host) {
     QADC_CUDA(cudaMemcpyAsync(out_ids, oi, (size_t)nq * R * 8, cudaMemcpyDeviceToHost, st));

@@ -28,15 +28,19 @@ __device__ __forceinline__ float midpoint(float qmin, float delta, int q) {
 // Largest t in [-1, 254] with midpoint(t) <= M (midpoint is monotone
 // non-decreasing in t because delta >= 0). -1 means no lane can qualify.
 // Saturated lanes (255) are never scan candidates, so the cap is 254.
+// An estimate from the inverse of the midpoint formula is corrected by exact
+// midpoint evaluations (usually 1-2): the result is the same as a binary
+// search, at a fraction of the dependent instructions (this runs on the scan
+// kernels' per-tile bound refresh).
 __device__ __forceinline__ int q_threshold(float M, float qmin, float delta) {
   if (!(midpoint(qmin, delta, 0) <= M)) return -1;
-  int lo = 0, hi = 254;  // invariant: midpoint(lo) <= M
-  if (midpoint(qmin, delta, hi) <= M) return hi;
-  while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (midpoint(qmin, delta, mid) <= M) lo = mid; else hi = mid;
-  }
-  return lo;
+  if (midpoint(qmin, delta, 254) <= M) return 254;
+  // here delta > 0 and midpoint(0) <= M < midpoint(254)
+  const float est = floorf(__fdiv_rn(M - qmin, delta) - 0.5f);
+  int t = (est >= 0.f && est <= 253.f) ? (int)est : (est > 253.f ? 253 : 0);
+  while (t < 253 && midpoint(qmin, delta, t + 1) <= M) t++;
+  while (t > 0 && !(midpoint(qmin, delta, t) <= M)) t--;
+  return t;
 }
 
 // (distance, id) strict order (scan_kernels.c:24-27).

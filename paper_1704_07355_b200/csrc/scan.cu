@@ -927,8 +927,7 @@ __device__ __forceinline__ void tc_flusher(const ScanArgs &a) {
       if (i < n) {
         volatile TcEntry *ve = &g_tc.ring[(tail + i) % kRing];
         int qy;
-        while ((qy = ve->query) < 0) {
-        }
+        while ((qy = ve->query) < 0) __nanosleep(64);  // writer between its claim and its publish: yield the issue slots
         __threadfence_block();
         e[r].query = qy;
         e[r].mid = ve->mid;
@@ -1511,6 +1510,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
           // the tile's critical path
           const uint32_t vb_t = __ldg(a.valid + g_t * 32 + (crow >> 3));
           todo &= __ballot_sync(kFull, (vb_t >> (crow & 7)) & 1u);
+          if (a.dbg & 256) todo = 0;  // timing experiment: test and validity, no hit handling
         }
         if (todo) {
           uint32_t *xf = s.xfer[w];

@@ -110,9 +110,10 @@ class DeviceIndex:
         flags = _native.LUT_IN if lut is not None else 0
         if not with_fsat:
             flags |= _native.NO_FSAT
-        if scan not in ("auto", "prmt", "tc"):
+        if scan not in ("auto", "prmt", "tc", "tc1"):
             raise ValueError(f"unknown scan kernel {scan!r}")
-        flags |= {"auto": 0, "prmt": _native.SCAN_PRMT, "tc": _native.SCAN_TC}[scan]
+        flags |= {"auto": 0, "prmt": _native.SCAN_PRMT, "tc": _native.SCAN_TC,
+                  "tc1": _native.SCAN_TC | _native.SCAN_TC1}[scan]
         if isinstance(queries, np.ndarray):
             q = _np(queries, np.float32).reshape(-1, self.d)
             nq = q.shape[0]

@@ -257,6 +257,11 @@ def test_search_batch_vs_oracle(gpu, m, R, init):
     assert np.array_equal(res.ids, oi)
     assert np.array_equal(_bits(res.distances), _bits(od))
     assert np.array_equal(res.counts, on)
+    if tc:  # the one-SM tensor-core scan (not CTA pairs) on the same inputs
+        t1 = idx.search(qs, R, init=init, scan="tc1")
+        assert t1.stats["scan_tc"] == 1
+        assert np.array_equal(t1.ids, oi)
+        assert np.array_equal(_bits(t1.distances), _bits(od))
     if tc:  # the CUDA-core PRMT scan on the same inputs
         pr = idx.search(qs, R, init=init, scan="prmt")
         assert pr.stats["scan_tc"] == 0
