@@ -651,15 +651,17 @@ __global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ cod
                                                 unsigned *__restrict__ M_bits, int *__restrict__ fsat_n,
                                                 float *__restrict__ fsat_mid,
                                                 int64_t *__restrict__ fsat_id) {
-  __shared__ unsigned char sqt[kMaxM * 16];
+  __shared__ __align__(16) unsigned char sqt[kMaxM * 16];
   __shared__ int warp_cnt[8];
   __shared__ unsigned hist[256];
+  __shared__ unsigned whist[8][256];  // per-warp prefix histograms (no cross-warp atomic contention)
   __shared__ int s_seen, s_nsat;
   __shared__ unsigned s_maxmid;
   const int q = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x == 0) { s_seen = 0; s_nsat = 0; s_maxmid = 0; }
   for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&whist[0][0])[i] = 0;
   __syncthreads();
   for (int s = 0; s < nslots; s++) {
     const int pair = q * nslots + s;
@@ -714,24 +716,56 @@ __global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ cod
     }
     // (2) bound histogram of the prefix: one octet (8 codes) per thread,
     // each interleaved word read once (coalesced across the CTA)
+    // PRMT lookups (entries <= 127): prmt(t0, t1, sel) gives entries 0-7 and
+    // 0 for selectors >= 8 (sign replicate of a non-negative byte); with
+    // sel ^ 0x8888 and (t2, t3) the other half. Bytes of two sub-quantizers
+    // add without carry (<= 254), then widen into 16-bit lanes. The words of
+    // 8 sub-quantizers are loaded together (independent L2 round trips).
     for (int64_t o = threadIdx.x; o * 8 < pref; o += blockDim.x) {
       const int64_t g = c0 + o / 32;
       const uint32_t *wp = codes + g * m * 32 + (o % 32);
-      uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int j = 0; j < m; j++) {
-        const uint32_t w = __ldg(wp + j * 32);
-        const unsigned char *row = sqt + j * 16;
+      uint32_t a02 = 0, a13 = 0, a46 = 0, a57 = 0;  // 16-bit lanes: codes (0,2), (1,3), (4,6), (5,7)
+      for (int j0 = 0; j0 < m; j0 += 8) {
+        uint32_t wv[8];
 #pragma unroll
-        for (int k = 0; k < 8; k++) acc[k] += row[(w >> (4 * k)) & 15];
+        for (int jj = 0; jj < 8; jj++) wv[jj] = j0 + jj < m ? __ldg(wp + (j0 + jj) * 32) : 0u;
+#pragma unroll
+        for (int jj = 0; jj < 8; jj += 2) {
+          uint32_t lo = 0, hi = 0;  // bytes: codes 0-3 / 4-7, two sub-quantizers
+#pragma unroll
+          for (int u = 0; u < 2; u++) {
+            const int j = j0 + jj + u;
+            if (j < m) {
+              const uint32_t w = wv[jj + u];
+              const uint4 t = *(const uint4 *)(sqt + j * 16);
+              const uint32_t s1 = w >> 16;
+              lo += prmt(t.x, t.y, w) | prmt(t.z, t.w, w ^ 0x8888u);
+              hi += prmt(t.x, t.y, s1) | prmt(t.z, t.w, s1 ^ 0x8888u);
+            }
+          }
+          a02 += lo & 0x00ff00ffu;
+          a13 += (lo >> 8) & 0x00ff00ffu;
+          a46 += hi & 0x00ff00ffu;
+          a57 += (hi >> 8) & 0x00ff00ffu;
+        }
       }
+      const uint32_t acc[8] = {a02 & 0xffffu, a13 & 0xffffu, a02 >> 16, a13 >> 16,
+                               a46 & 0xffffu, a57 & 0xffffu, a46 >> 16, a57 >> 16};
 #pragma unroll
       for (int k = 0; k < 8; k++) {
         const int64_t kk = o * 8 + k;
         if (kk < pref && acc[k] < 255 && ids[c0 * kChunkCodes + kk] >= 0)
-          atomicAdd(&hist[acc[k]], 1u);
+          atomicAdd(&whist[wid][acc[k]], 1u);
       }
     }
     __syncthreads();
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) {
+    unsigned c = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) c += whist[w][t];
+    hist[t] += c;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
