@@ -1476,6 +1476,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
         arrive_ready((gt + 1) & 1);
         if (ntiles > 2) tc_load<MC, MH>(a, c0g + 2, crow, j0, cw);
       }
+      // valid byte of this thread's code, one tile ahead (read by the
+      // survivor path only)
+      uint32_t vb_next = __ldg(a.valid + c0g * 32 + (crow >> 3));
       for (int64_t t = 0; t < ntiles; t++, gt++) {
         const uint32_t b = gt & 1;
         const int64_t g_t = c0g + t;
@@ -1497,6 +1500,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
           arrive_ready(b);
           if (t + 3 < ntiles) tc_load<MC, MH>(a, c0g + t + 3, crow, j0, cw);
         }
+        const uint32_t vb_t = vb_next;
+        if (t + 1 < ntiles) vb_next = __ldg(a.valid + (g_t + 1) * 32 + (crow >> 3));
         const uint4 *T = (const uint4 *)&s.thr16[col0];
         uint32_t any = 0;
 #pragma unroll
@@ -1508,7 +1513,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
         if (todo) {
           // validity (padding codes have id -1) is checked only here, off
           // the tile's critical path
-          const uint32_t vb_t = __ldg(a.valid + g_t * 32 + (crow >> 3));
           todo &= __ballot_sync(kFull, (vb_t >> (crow & 7)) & 1u);
           if (a.dbg & 256) todo = 0;  // timing experiment: test and validity, no hit handling
         }
