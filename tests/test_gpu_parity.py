@@ -283,6 +283,25 @@ def test_edge_cases_vs_oracle(gpu):
             assert np.array_equal(res.counts, on), (n, R)
 
 
+def test_tensor_core_scan_edge_cases_vs_oracle(gpu):
+    """The CTA-pair (cta_group::2) and one-SM tensor-core scans on partial
+    chunks, one query (MMA N = 16: 8 B rows per CTA of the pair), a query
+    count that is not a multiple of 16, and more queries than one MMA's N
+    (two items per code range)."""
+    rng = np.random.default_rng(11)
+    for n in (1, 255, 257, 5000):
+        for nq in (1, 17, 300):
+            idx, flat, qs, cb = _random_flat(rng, n, 32, 128, nq)
+            for R in (1, 100):
+                oi, od, on, _ = orc.search_batch(qs, cb, None, None, 1, flat, R, 1000)
+                for scan in ("tc", "tc1"):
+                    res = idx.search(qs, R, init=1000, scan=scan)
+                    assert res.stats["scan_tc"] == 1
+                    assert np.array_equal(res.ids, oi), (n, nq, R, scan)
+                    assert np.array_equal(_bits(res.distances), _bits(od)), (n, nq, R, scan)
+                    assert np.array_equal(res.counts, on), (n, nq, R, scan)
+
+
 @pytest.mark.parametrize("n", [60_000, 200_000])
 def test_massive_ties_vs_oracle(gpu, n):
     """Three code patterns only (about n, n/7 and n/40 copies): every lane
