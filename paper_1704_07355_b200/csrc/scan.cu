@@ -787,6 +787,18 @@ __device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase) {
       : "memory");
 }
 
+// Non-blocking probe of an mbarrier phase (warp-uniform: lane 0 decides).
+__device__ __forceinline__ bool tc_try_warp(uint32_t mbar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(mbar), "r"(phase)
+      : "memory");
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
 // 64 accumulator columns of the thread's TMEM lane, low 16 bits of each,
 // two adjacent columns per register (column 2i in the low half of v[i]).
 // Sums are < 2^13, so the 16-bit halves are exact. No wait: the caller
@@ -823,7 +835,8 @@ struct TcSmem {
   // pairs by the epilogue's SWAR test
   __align__(16) uint16_t thr16[kTcNQ];
   unsigned mc[kTcNQ];  // cached global bound M (bits)
-  __align__(16) uint32_t xfer[16][32];  // per compute warp: one lane's packed sums
+  __align__(16) uint32_t xfer[16][4][32];  // per compute warp: up to 4 lanes' packed sums
+  int64_t stash_pos[16][4];                 // (k_scan_tc2: survivors stashed until the warp idles)
   TcEntry ring[kRing];
 };
 // debug counters (QADC_B200_TC_DEBUG bit 64): slow-path entries, hits, ring
@@ -1230,7 +1243,7 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
                                                  !(a.dbg & 1));
         if (todo) {
           const int lane = tid & 31;
-          uint32_t *xf = s.xfer[w];
+          uint32_t *xf = s.xfer[w][0];
           const int64_t pos0 = g_t * kChunkCodes + (int64_t)(c_t - lane);
           while (todo) {
             const int src = __ffs(todo) - 1;
@@ -1417,6 +1430,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     const uint32_t a_row0 = sA_a + (uint32_t)((row >> 3) * SBO + 16 * (row & 7) + 128 * j0);
     const int crow = (int)rank * kTcCodes + row;  // code within the chunk
     uint32_t gt = 0;
+    // Survivor stash: a lane with survivors parks its packed sums in shared
+    // memory (up to 4 codes per warp) and the warp handles them while it
+    // would otherwise wait for the next MMA, off the MMA's critical path.
+    int ns = 0;  // warp-uniform
+    auto process_one = [&](int k) {
+      const uint32_t vv = s.xfer[w][k][lane];
+      const int q = col0 + 2 * lane;
+      const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
+      tc_hit_warp(a, (x & 0x8000u) != 0, (x & 0x80000000u) != 0, q, vv, s.stash_pos[w][k]);
+      __syncwarp();
+    };
     auto arrive_ready = [&](uint32_t b) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1432,7 +1456,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       const int64_t c0g = it.chunk_begin;
       const int64_t ntiles = it.chunk_end - it.chunk_begin;
       // every compute thread is past the previous item (its tiles' MMAs all
-      // completed: B and the query state may be overwritten)
+      // completed: B and the query state may be overwritten; its stashed
+      // survivors handled)
+      while (ns > 0) process_one(--ns);
       asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
       // ---- stage this CTA's half of B and the item's query state ----
       for (int e = tid; e < half * MC; e += NT) {
@@ -1484,7 +1510,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
         const int64_t g_t = c0g + t;
         unsigned mpre = 0;
         if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];
-        // ---- tile t: wait for MMA(t), copy the sums out of D[b] ----
+        // ---- tile t: wait for MMA(t) (handling stashed survivors while it
+        // runs), copy the sums out of D[b] ----
+        while (ns > 0 && !tc_try_warp(done_a + 8 * b, (gt >> 1) & 1)) process_one(--ns);
         tc_wait(done_a + 8 * b, (gt >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         uint32_t v[kCPT / 2];
@@ -1516,24 +1544,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
           todo &= __ballot_sync(kFull, (vb_t >> (crow & 7)) & 1u);
           if (a.dbg & 256) todo = 0;  // timing experiment: test and validity, no hit handling
         }
-        if (todo) {
-          uint32_t *xf = s.xfer[w];
-          const int64_t pos0 = g_t * kChunkCodes + (int64_t)(crow - lane);
-          while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            if (lane == src) {
+        while (todo) {
+          if (ns == 4) process_one(--ns);  // stash full: make room
+          const int src = __ffs(todo) - 1;
+          todo &= todo - 1;
+          if (lane == src) {
 #pragma unroll
-              for (int i = 0; i < 32; i += 4)
-                *(uint4 *)&xf[i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            }
-            __syncwarp();
-            const uint32_t vv = xf[lane];
-            const int q = col0 + 2 * lane;
-            const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
-            __syncwarp();
-            tc_hit_warp(a, (x & 0x8000u) != 0, (x & 0x80000000u) != 0, q, vv, pos0 + src);
+            for (int i = 0; i < 32; i += 4)
+              *(uint4 *)&s.xfer[w][ns][i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            s.stash_pos[w][ns] = g_t * kChunkCodes + crow;
           }
+          __syncwarp();
+          ns++;
         }
         if (tid < nq && mpre < s.mc[tid]) {
           s.mc[tid] = mpre;
@@ -1542,6 +1564,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
         }
       }
     }
+    while (ns > 0) process_one(--ns);
     asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
     if (tid == 0) *(volatile int *)&s.done = 1;
   }
