@@ -787,18 +787,6 @@ __device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase) {
       : "memory");
 }
 
-// Non-blocking probe of an mbarrier phase (warp-uniform: lane 0 decides).
-__device__ __forceinline__ bool tc_try_warp(uint32_t mbar, uint32_t phase) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok)
-      : "r"(mbar), "r"(phase)
-      : "memory");
-  return __shfl_sync(0xffffffffu, ok, 0) != 0;
-}
-
 // 64 accumulator columns of the thread's TMEM lane, low 16 bits of each,
 // two adjacent columns per register (column 2i in the low half of v[i]).
 // Sums are < 2^13, so the 16-bit halves are exact. No wait: the caller
@@ -1284,6 +1272,143 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
 }
 
 
+// ---- survivors of the two-SM scan: per-warp rings drained by 4 flushers ----
+// A compute warp hands the packed sums of its codes with survivors to a
+// flusher warp through its own single-producer ring (slots claimed
+// warp-synchronously: no atomics, one fence and one head store per tile).
+// The flusher re-runs the SWAR test per query column, computes midpoints,
+// filters by the cached bound and appends (compacted, up to 32 candidates'
+// slot claims and id reads in flight together). Compute warps, on whose
+// timeliness every MMA depends, never run the per-pair survivor path.
+constexpr int kWRing = 8;       // slots per compute warp
+constexpr int kFlushers = 4;    // flusher warps (flusher f serves compute warps 4 f .. 4 f + 3)
+struct Tc2Ent {
+  uint32_t sums[32];  // packed pairs: columns col0 + 2 i (low half), + 1 (high)
+  int64_t pos;        // code position (chunk * 256 + code)
+  int col0;
+  int pad;
+};
+struct Tc2Cand {
+  int query;
+  float mid;
+  int64_t pos;
+};
+struct Tc2Smem {
+  uint32_t tmem;
+  int done;
+  unsigned whead[16];  // per compute warp: slots published (monotone)
+  unsigned wtail[16];  // per compute warp: slots consumed by its flusher
+  int query[kTcNQ];
+  float qmin[kTcNQ];
+  float delta[kTcNQ];
+  __align__(16) uint16_t thr16[kTcNQ];
+  unsigned mc[kTcNQ];
+  __align__(16) Tc2Ent ent[16][kWRing];
+  Tc2Cand clist[kFlushers][96];
+};
+__shared__ Tc2Smem g_tc2;
+
+// Appends the compacted candidates cl[0, cnt) (one per lane per pass) and
+// refreshes the bound of queries crossing a multiple of bound_every.
+__device__ __forceinline__ void tc2_append(const ScanArgs &a, const Tc2Cand *cl, int cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int base = 0; base < cnt; base += 32) {
+    const int i = base + lane;
+    const bool has = i < cnt;
+    int qy = 0;
+    unsigned slot = 0;
+    if (has) {
+      qy = cl[i].query;
+      const float mid = cl[i].mid;
+      const int64_t id = a.ids[cl[i].pos];  // in flight with the slot claim
+      slot = atomicAdd(&a.cand_n[qy], 1u);
+      if (slot < (unsigned)a.cap_g) {
+        const size_t o = (size_t)qy * a.cap_g + slot;
+        a.cand_mid[o] = mid;
+        a.cand_id[o] = id;
+      }
+      const float hw = a.hist_w[qy];
+      if (hw > 0.f) {
+        unsigned *h = a.hist + (size_t)qy * kHistWords;
+        const int b = min((int)__fmul_rn(mid, __frcp_rn(hw)), kHistBins - 1);
+        atomicAdd(&h[b], 1u);
+        atomicAdd(&h[kHistBins + (b >> 5)], 1u);
+      }
+    }
+    unsigned mq = __ballot_sync(kFull, has && (slot + 1) % (unsigned)a.bound_every == 0);
+    while (mq) {
+      const int src = __ffs(mq) - 1;
+      mq &= mq - 1;
+      const int query = __shfl_sync(kFull, qy, src);
+      const unsigned mb = hist_bound(a, query);
+      if (lane == 0) atomicMin(&a.M_bits[query], mb);
+    }
+  }
+}
+
+__device__ __forceinline__ void tc2_flusher(const ScanArgs &a, int f) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  Tc2Cand *cl = g_tc2.clist[f];
+  unsigned tail[4] = {0, 0, 0, 0};
+  for (;;) {
+    bool busy = false;
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      const int cwi = 4 * f + r;
+      const unsigned head = *(volatile unsigned *)&g_tc2.whead[cwi];
+      if (head == tail[r]) continue;
+      busy = true;
+      __threadfence_block();  // the entries' contents before their head
+      int cnt = 0;
+      for (unsigned k = tail[r]; k != head; k++) {
+        const Tc2Ent &e = g_tc2.ent[cwi][k % kWRing];
+        const uint32_t vv = e.sums[lane];
+        const int64_t pos = e.pos;
+        const int q = e.col0 + 2 * lane;
+        const uint32_t x = *(const uint32_t *)&g_tc2.thr16[q] - vv;
+        bool c[2];
+        float md[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          c[h] = false;
+          md[h] = 0.f;
+          if (x & (0x8000u << (16 * h))) {
+            md[h] = midpoint(g_tc2.qmin[q + h], g_tc2.delta[q + h], (int)((vv >> (16 * h)) & 0xffffu));
+            c[h] = md[h] <= __uint_as_float(g_tc2.mc[q + h]);
+          }
+        }
+        const unsigned b0 = __ballot_sync(kFull, c[0]), b1 = __ballot_sync(kFull, c[1]);
+        if (c[0]) cl[cnt + __popc(b0 & lt)] = {g_tc2.query[q], md[0], pos};
+        if (c[1]) cl[cnt + __popc(b0) + __popc(b1 & lt)] = {g_tc2.query[q + 1], md[1], pos};
+        cnt += __popc(b0) + __popc(b1);
+        if (cnt > 32) {  // room for the next entry's up to 64
+          __syncwarp();
+          tc2_append(a, cl, cnt);
+          __syncwarp();
+          cnt = 0;
+        }
+      }
+      __syncwarp();
+      // the slots are free once read: hand them back before the appends
+      tail[r] = head;
+      if (lane == 0) *(volatile unsigned *)&g_tc2.wtail[cwi] = head;
+      if (cnt) tc2_append(a, cl, cnt);
+      __syncwarp();
+    }
+    if (!busy) {
+      if (*(volatile int *)&g_tc2.done) {
+        bool empty = true;
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+          empty = empty && *(volatile unsigned *)&g_tc2.whead[4 * f + r] == tail[r];
+        if (empty) break;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
 // ---- two-SM variant (cta_group::2): one tile = one 256-code chunk ----
 // A CTA pair (cluster of 2) shares every MMA: M = 256 codes (CTA r expands
 // codes 128 r .. 128 r + 127 of the chunk into its own shared memory), N =
@@ -1320,7 +1445,7 @@ __device__ __forceinline__ void tc2_expand(uint32_t a_row, const uint32_t (&cw)[
 }
 
 template <int MC>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 * 4 + 32 * (kFlushers + 1), 1)
     k_scan_tc2(const __grid_constant__ ScanArgs a) {
   constexpr int G = 4;
   constexpr int K = 16 * MC, SBO = 8 * K, MH = MC / G;
@@ -1330,7 +1455,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
   constexpr uint32_t kCols = 512;
   static_assert(MH >= 1 && kCPT == 64, "tile split");
   extern __shared__ __align__(16) unsigned char dsm[];
-  TcSmem &s = g_tc;
+  Tc2Smem &s = g_tc2;
   uint8_t *sB = dsm;                           // [kTcNQ / 2][K]
   uint8_t *sA = dsm + (size_t)(kTcNQ / 2) * K; // [2][kTcCodes][K]
   __shared__ __align__(8) uint64_t ready[2], done[2];
@@ -1354,10 +1479,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(done_a + 8));
     asm volatile("fence.mbarrier_init.release.cluster;");
     s.done = 0;
-    s.head = 0;
-    s.tail = 0;
   }
-  for (int i = tid; i < kRing; i += blockDim.x) s.ring[i].query = -1;
+  if (tid < 16) {
+    s.whead[tid] = 0;
+    s.wtail[tid] = 0;
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
@@ -1365,9 +1491,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
   const uint32_t tmem = s.tmem;
   const int n_items = *a.n_items;
   const int pair = blockIdx.x >> 1, npair = gridDim.x >> 1;
-  if (w == 4 * G) {
-    tc_flusher(a);
-  } else if (w == 4 * G + 1) {
+  if (w >= 4 * G && w < 4 * G + kFlushers) {
+    tc2_flusher(a, w - 4 * G);
+  } else if (w == 4 * G + kFlushers) {
     // ---- MMA issuer (CTA 0 only) ----
     if (rank == 0) {
       uint32_t gt = 0;
@@ -1430,17 +1556,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
     const uint32_t a_row0 = sA_a + (uint32_t)((row >> 3) * SBO + 16 * (row & 7) + 128 * j0);
     const int crow = (int)rank * kTcCodes + row;  // code within the chunk
     uint32_t gt = 0;
-    // Survivor stash: a lane with survivors parks its packed sums in shared
-    // memory (up to 4 codes per warp) and the warp handles them while it
-    // would otherwise wait for the next MMA, off the MMA's critical path.
-    int ns = 0;  // warp-uniform
-    auto process_one = [&](int k) {
-      const uint32_t vv = s.xfer[w][k][lane];
-      const int q = col0 + 2 * lane;
-      const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
-      tc_hit_warp(a, (x & 0x8000u) != 0, (x & 0x80000000u) != 0, q, vv, s.stash_pos[w][k]);
-      __syncwarp();
-    };
+    unsigned my_head = 0;  // warp-uniform: slots this warp has published
     auto arrive_ready = [&](uint32_t b) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1456,9 +1572,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
       const int64_t c0g = it.chunk_begin;
       const int64_t ntiles = it.chunk_end - it.chunk_begin;
       // every compute thread is past the previous item (its tiles' MMAs all
-      // completed: B and the query state may be overwritten; its stashed
-      // survivors handled)
-      while (ns > 0) process_one(--ns);
+      // completed: B may be overwritten) and, once the flushers have consumed
+      // every entry, so may the query state
+      asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+      if (tid < 16)
+        while (*(volatile unsigned *)&s.wtail[tid] != *(volatile unsigned *)&s.whead[tid]) __nanosleep(128);
       asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
       // ---- stage this CTA's half of B and the item's query state ----
       for (int e = tid; e < half * MC; e += NT) {
@@ -1512,7 +1630,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
         if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];
         // ---- tile t: wait for MMA(t) (handling stashed survivors while it
         // runs), copy the sums out of D[b] ----
-        while (ns > 0 && !tc_try_warp(done_a + 8 * b, (gt >> 1) & 1)) process_one(--ns);
         tc_wait(done_a + 8 * b, (gt >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         uint32_t v[kCPT / 2];
@@ -1544,18 +1661,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
           todo &= __ballot_sync(kFull, (vb_t >> (crow & 7)) & 1u);
           if (a.dbg & 256) todo = 0;  // timing experiment: test and validity, no hit handling
         }
+        // hand the codes with survivors to this warp's flusher, up to a
+        // ring's worth at a time
         while (todo) {
-          if (ns == 4) process_one(--ns);  // stash full: make room
-          const int src = __ffs(todo) - 1;
-          todo &= todo - 1;
-          if (lane == src) {
+          const unsigned room = kWRing - (my_head - *(volatile unsigned *)&s.wtail[w]);
+          const unsigned take = __shfl_sync(kFull, room, 0);
+          if (take == 0) {
+            __nanosleep(32);
+            continue;
+          }
+          const unsigned lt = (1u << lane) - 1u;
+          const unsigned rk = __popc(todo & lt);
+          if (((todo >> lane) & 1u) && rk < take) {
+            Tc2Ent &e = s.ent[w][(my_head + rk) % kWRing];
 #pragma unroll
             for (int i = 0; i < 32; i += 4)
-              *(uint4 *)&s.xfer[w][ns][i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            s.stash_pos[w][ns] = g_t * kChunkCodes + crow;
+              *(uint4 *)&e.sums[i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            e.pos = g_t * kChunkCodes + crow;
+            e.col0 = col0;
+            __threadfence_block();
           }
+          const unsigned n = min((unsigned)__popc(todo), take);
+          // drop the lanes just published from todo
+          unsigned t2 = todo;
+          for (unsigned k = 0; k < n; k++) t2 &= t2 - 1;
+          todo = t2;
           __syncwarp();
-          ns++;
+          my_head += n;
+          if (lane == 0) *(volatile unsigned *)&s.whead[w] = my_head;
         }
         if (tid < nq && mpre < s.mc[tid]) {
           s.mc[tid] = mpre;
@@ -1564,7 +1697,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
         }
       }
     }
-    while (ns > 0) process_one(--ns);
     asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
     if (tid == 0) *(volatile int *)&s.done = 1;
   }
@@ -1584,7 +1716,7 @@ void launch_tc2(const ScanArgs &a, int nsm, cudaStream_t st) {
   const size_t smem = tc2_smem_bytes<MC>();
   cudaFuncSetAttribute(k_scan_tc2<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_scan_tc2<MC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  k_scan_tc2<MC><<<nsm & ~1, 576, smem, st>>>(a);
+  k_scan_tc2<MC><<<nsm & ~1, 128 * 4 + 32 * (kFlushers + 1), smem, st>>>(a);
 }
 
 template <int MC>
