@@ -71,8 +71,16 @@ __device__ __forceinline__ unsigned hist_bound(const ScanArgs &a, int query) {
   const int lane = threadIdx.x & 31;
   const float hw = a.hist_w[query];
   if (!(hw > 0.f)) return 0x7f800000u;
-  const unsigned *h = a.hist + (size_t)query * kHistWords;
-  const unsigned c = *(volatile const unsigned *)&h[kHistBins + lane];
+  // lane l reads fine bins 32 l .. 32 l + 31 (8 independent 16-byte L2
+  // reads: one round trip per refresh; counts read early only make the
+  // bound looser)
+  const uint4 *h = (const uint4 *)(a.hist + (size_t)query * kHistWords) + lane * 8;
+  uint4 r[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) r[i] = __ldcg(h + i);
+  unsigned c = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) c += r[i].x + r[i].y + r[i].z + r[i].w;
   unsigned incl = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -83,16 +91,24 @@ __device__ __forceinline__ unsigned hist_bound(const ScanArgs &a, int query) {
   const unsigned hit = __ballot_sync(kFull, incl >= R);
   if (!hit) return 0x7f800000u;
   const int k = __ffs(hit) - 1;
-  const unsigned base = __shfl_sync(kFull, incl - c, k);
-  const unsigned f = *(volatile const unsigned *)&h[k * 32 + lane];
-  unsigned fi = f;
+  int b = 31;
+  if (lane == k) {  // this lane's bins, from its exclusive prefix
+    unsigned cum = incl - c;
+    bool found = false;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned y = __shfl_up_sync(kFull, fi, o);
-    if (lane >= o) fi += y;
+    for (int i = 0; i < 8; i++) {
+      const unsigned w4[4] = {r[i].x, r[i].y, r[i].z, r[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        cum += w4[j];
+        if (!found && cum >= R) {
+          b = 4 * i + j;
+          found = true;
+        }
+      }
+    }
   }
-  const unsigned hit2 = __ballot_sync(kFull, base + fi >= R);
-  const int b = k * 32 + (hit2 ? __ffs(hit2) - 1 : 31);
+  b = k * 32 + __shfl_sync(kFull, b, k);
   return fbits(__fmul_rn((float)(b + 2), hw));
 }
 
@@ -287,7 +303,6 @@ __device__ __noinline__ void append(const ScanArgs &a, Smem &s, uint32_t *buf, i
         // (b + 2) * w keeps one bucket of slack)
         const int b = min((int)__fmul_rn(midpoint(qmin, delta, (int)v), hinv), kHistBins - 1);
         atomicAdd(&h[b], 1u);
-        atomicAdd(&h[kHistBins + (b >> 5)], 1u);
       }
     }
   }
@@ -847,7 +862,6 @@ __device__ __forceinline__ void tc_put(const ScanArgs &a, int query, float mid, 
     unsigned *h = a.hist + (size_t)query * kHistWords;
     const int b = min((int)__fmul_rn(mid, __frcp_rn(hw)), kHistBins - 1);
     atomicAdd(&h[b], 1u);
-    atomicAdd(&h[kHistBins + (b >> 5)], 1u);
   }
 }
 
@@ -1281,7 +1295,8 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
 // slot claims and id reads in flight together). Compute warps, on whose
 // timeliness every MMA depends, never run the per-pair survivor path.
 constexpr int kWRing = 8;       // slots per compute warp
-constexpr int kFlushers = 4;    // flusher warps (flusher f serves compute warps 4 f .. 4 f + 3)
+constexpr int kFlushers = 4;    // flusher warps (flusher f serves compute warps kPerF f .. kPerF f + kPerF - 1)
+constexpr int kPerF = 16 / kFlushers;
 struct Tc2Ent {
   uint32_t sums[32];  // packed pairs: columns col0 + 2 i (low half), + 1 (high)
   int64_t pos;        // code position (chunk * 256 + code)
@@ -1332,7 +1347,6 @@ __device__ __forceinline__ void tc2_append(const ScanArgs &a, const Tc2Cand *cl,
         unsigned *h = a.hist + (size_t)qy * kHistWords;
         const int b = min((int)__fmul_rn(mid, __frcp_rn(hw)), kHistBins - 1);
         atomicAdd(&h[b], 1u);
-        atomicAdd(&h[kHistBins + (b >> 5)], 1u);
       }
     }
     unsigned mq = __ballot_sync(kFull, has && (slot + 1) % (unsigned)a.bound_every == 0);
@@ -1350,12 +1364,12 @@ __device__ __forceinline__ void tc2_flusher(const ScanArgs &a, int f) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   Tc2Cand *cl = g_tc2.clist[f];
-  unsigned tail[4] = {0, 0, 0, 0};
+  unsigned tail[kPerF] = {};
   for (;;) {
     bool busy = false;
 #pragma unroll
-    for (int r = 0; r < 4; r++) {
-      const int cwi = 4 * f + r;
+    for (int r = 0; r < kPerF; r++) {
+      const int cwi = kPerF * f + r;
       const unsigned head = *(volatile unsigned *)&g_tc2.whead[cwi];
       if (head == tail[r]) continue;
       busy = true;
@@ -1400,8 +1414,8 @@ __device__ __forceinline__ void tc2_flusher(const ScanArgs &a, int f) {
       if (*(volatile int *)&g_tc2.done) {
         bool empty = true;
 #pragma unroll
-        for (int r = 0; r < 4; r++)
-          empty = empty && *(volatile unsigned *)&g_tc2.whead[4 * f + r] == tail[r];
+        for (int r = 0; r < kPerF; r++)
+          empty = empty && *(volatile unsigned *)&g_tc2.whead[kPerF * f + r] == tail[r];
         if (empty) break;
       }
       __nanosleep(64);
