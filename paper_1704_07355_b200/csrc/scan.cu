@@ -1380,6 +1380,8 @@ __device__ __forceinline__ void tc2_flusher(const ScanArgs &a, int f) {
         const uint32_t vv = e.sums[lane];
         const int64_t pos = e.pos;
         const int q = e.col0 + 2 * lane;
+        __syncwarp();  // the slot is free once every lane holds its part
+        if (lane == 0) *(volatile unsigned *)&g_tc2.wtail[cwi] = k + 1;
         const uint32_t x = *(const uint32_t *)&g_tc2.thr16[q] - vv;
         bool c[2];
         float md[2];
@@ -1404,9 +1406,7 @@ __device__ __forceinline__ void tc2_flusher(const ScanArgs &a, int f) {
         }
       }
       __syncwarp();
-      // the slots are free once read: hand them back before the appends
       tail[r] = head;
-      if (lane == 0) *(volatile unsigned *)&g_tc2.wtail[cwi] = head;
       if (cnt) tc2_append(a, cl, cnt);
       __syncwarp();
     }
