@@ -838,8 +838,7 @@ struct TcSmem {
   // pairs by the epilogue's SWAR test
   __align__(16) uint16_t thr16[kTcNQ];
   unsigned mc[kTcNQ];  // cached global bound M (bits)
-  __align__(16) uint32_t xfer[16][4][32];  // per compute warp: up to 4 lanes' packed sums
-  int64_t stash_pos[16][4];                 // (k_scan_tc2: survivors stashed until the warp idles)
+  __align__(16) uint32_t xfer[16][32];  // per compute warp: one lane's packed sums
   TcEntry ring[kRing];
 };
 // debug counters (QADC_B200_TC_DEBUG bit 64): slow-path entries, hits, ring
@@ -1245,7 +1244,7 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
                                                  !(a.dbg & 1));
         if (todo) {
           const int lane = tid & 31;
-          uint32_t *xf = s.xfer[w][0];
+          uint32_t *xf = s.xfer[w];
           const int64_t pos0 = g_t * kChunkCodes + (int64_t)(c_t - lane);
           while (todo) {
             const int src = __ffs(todo) - 1;
