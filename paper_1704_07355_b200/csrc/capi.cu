@@ -248,7 +248,12 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
                                                                  : (avg_chunks >= 64 ? 1 : 0);
   // one exhaustive list on the tensor-core scan: CTA pairs (k_scan_tc2)
   static const int tc2_env = scan_env_int("QADC_B200_TC2", 1);
-  const int pair_cta = (tc2_env && !one_sm && nl == 1 && scan_use_tc(m, prmt) && nsm >= 2) ? 1 : 0;
+  // CTA-pair variant: flusher warps for long scans (>= 8K chunks per
+  // list: the survivor burst of the loose initial bound is amortised),
+  // inline survivor handling otherwise (QADC_B200_TC2=2 / 3 forces inline / rings)
+  static const int tc2_rings_min = scan_env_int("QADC_B200_TC2_RINGS_MIN_CHUNKS", 8192);
+  int pair_cta = (tc2_env && !one_sm && nl == 1 && scan_use_tc(m, prmt) && nsm >= 2) ? 1 : 0;
+  if (pair_cta) pair_cta = tc2_env == 2 ? 2 : tc2_env == 3 ? 1 : (idx->total_chunks >= tc2_rings_min ? 1 : 2);
   if (nl == 1 && idx->total_chunks > 0) {
     // one exhaustive list: equal-size items, so the persistent CTAs finish
     // together only if the item count fills whole waves. Pick the range

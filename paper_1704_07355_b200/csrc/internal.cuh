@@ -138,7 +138,7 @@ struct ScanArgs {
   int R;
   int bound_every;         // appended candidates between global-histogram bound reads
   int linear;              // 1: linear fixed-m loop (long items), 0: interleaved loop
-  int pair_cta;            // tensor-core scan on CTA pairs (k_scan_tc2: static item order)
+  int pair_cta;            // tensor-core scan on CTA pairs (static item order): 1 k_scan_tc2 (flusher rings), 2 k_scan_tc2i (inline survivors)
   int dbg;                 // timing experiments only (QADC_B200_TC_DEBUG; results invalid if != 0)
 };
 

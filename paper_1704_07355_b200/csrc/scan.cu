@@ -802,6 +802,18 @@ __device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase) {
       : "memory");
 }
 
+// Non-blocking probe of an mbarrier phase (warp-uniform: lane 0 decides).
+__device__ __forceinline__ bool tc_try_warp(uint32_t mbar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(mbar), "r"(phase)
+      : "memory");
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
 // 64 accumulator columns of the thread's TMEM lane, low 16 bits of each,
 // two adjacent columns per register (column 2i in the low half of v[i]).
 // Sums are < 2^13, so the 16-bit halves are exact. No wait: the caller
@@ -838,7 +850,8 @@ struct TcSmem {
   // pairs by the epilogue's SWAR test
   __align__(16) uint16_t thr16[kTcNQ];
   unsigned mc[kTcNQ];  // cached global bound M (bits)
-  __align__(16) uint32_t xfer[16][32];  // per compute warp: one lane's packed sums
+  __align__(16) uint32_t xfer[16][4][32];  // per compute warp: up to 4 lanes' packed sums
+  int64_t stash_pos[16][4];                 // (k_scan_tc2i: survivors stashed until the warp idles)
   TcEntry ring[kRing];
 };
 // debug counters (QADC_B200_TC_DEBUG bit 64): slow-path entries, hits, ring
@@ -1244,7 +1257,7 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
                                                  !(a.dbg & 1));
         if (todo) {
           const int lane = tid & 31;
-          uint32_t *xf = s.xfer[w];
+          uint32_t *xf = s.xfer[w][0];
           const int64_t pos0 = g_t * kChunkCodes + (int64_t)(c_t - lane);
           while (todo) {
             const int src = __ffs(todo) - 1;
@@ -1721,12 +1734,280 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 * 4 + 32 * (kFlu
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(s.tmem), "n"(kCols));
 }
 
+// Inline-survivor variant of the CTA-pair scan (k_scan_tc2i): the compute
+// warps handle their own survivors (stashed per warp, handled while waiting
+// for the next MMA; one flusher warp appends). Used for shorter scans,
+// whose survivors arrive mostly in the initial burst that the per-warp
+// rings of k_scan_tc2 cannot absorb.
+template <int MC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(576, 1)
+    k_scan_tc2i(const __grid_constant__ ScanArgs a) {
+  constexpr int G = 4;
+  constexpr int K = 16 * MC, SBO = 8 * K, MH = MC / G;
+  constexpr int NT = 128 * G;           // compute threads
+  constexpr int kCPT = kTcNQ / G;       // accumulator columns per compute thread
+  constexpr int kATile = kTcCodes * K;  // bytes of one A buffer
+  constexpr uint32_t kCols = 512;
+  static_assert(MH >= 1 && kCPT == 64, "tile split");
+  extern __shared__ __align__(16) unsigned char dsm[];
+  TcSmem &s = g_tc;
+  uint8_t *sB = dsm;                           // [kTcNQ / 2][K]
+  uint8_t *sA = dsm + (size_t)(kTcNQ / 2) * K; // [2][kTcCodes][K]
+  __shared__ __align__(8) uint64_t ready[2], done[2];
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const int row = tid & 127, part = tid >> 7, j0 = part * MH, col0 = part * kCPT;
+  const uint32_t sB_a = (uint32_t)__cvta_generic_to_shared(sB);
+  const uint32_t sA_a = (uint32_t)__cvta_generic_to_shared(sA);
+  const uint32_t ready_a = (uint32_t)__cvta_generic_to_shared(&ready[0]);
+  const uint32_t done_a = (uint32_t)__cvta_generic_to_shared(&done[0]);
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s.tmem)),
+                 "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ready_a), "n"(2 * 4 * G));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ready_a + 8), "n"(2 * 4 * G));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(done_a));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(done_a + 8));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    s.done = 0;
+    s.head = 0;
+    s.tail = 0;
+  }
+  for (int i = tid; i < kRing; i += blockDim.x) s.ring[i].query = -1;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = s.tmem;
+  const int n_items = *a.n_items;
+  const int pair = blockIdx.x >> 1, npair = gridDim.x >> 1;
+  if (w == 4 * G) {
+    tc_flusher(a);
+  } else if (w == 4 * G + 1) {
+    // ---- MMA issuer (CTA 0 only) ----
+    if (rank == 0) {
+      uint32_t gt = 0;
+      for (int item = pair; item < n_items; item += npair) {
+        const WorkItem it = a.items[item];
+        const int nq = it.pair_count;
+        const int n_mma = max(16, (nq + 15) & ~15);
+        const uint32_t idesc = (2u << 4) | ((uint32_t)(n_mma >> 3) << 17) |
+                               ((uint32_t)((2 * kTcCodes) >> 4) << 24);
+        const int64_t ntiles = it.chunk_end - it.chunk_begin;
+        for (int64_t t = 0; t < ntiles; t++, gt++) {
+          const uint32_t b = gt & 1;
+          tc_wait(ready_a + 8 * b, (gt >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (lane == 0) {
+#pragma unroll
+            for (int ks = 0; ks < K / 32; ks++) {
+              const uint64_t da = tc_smem_desc(sA_a + b * kATile + ks * 256, SBO);
+              const uint64_t db = tc_smem_desc(sB_a + ks * 256, SBO);
+              const uint32_t acc = ks > 0 ? 1u : 0u;
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+                      tmem + b * (uint32_t)kTcNQ),
+                  "l"(da), "l"(db), "r"(idesc), "r"(acc));
+            }
+            asm volatile(
+                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                " [%0], %1;" ::"r"(done_a + 8 * b),
+                "h"((uint16_t)3)
+                : "memory");
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ---- compute warps ----
+    const uint32_t t_row = tmem + ((uint32_t)((w & 3) * 32) << 16);
+    // zero this thread's accumulator columns (both D buffers) once: see k_scan_tc
+    {
+      const uint32_t z[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int b = 0; b < 2; b++)
+#pragma unroll
+        for (int c = 0; c < kCPT; c += 16)
+          asm volatile(
+              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+              "%12,%13,%14,%15,%16};" ::"r"(t_row + b * kTcNQ + col0 + c),
+              "r"(z[0]), "r"(z[1]), "r"(z[2]), "r"(z[3]), "r"(z[4]), "r"(z[5]), "r"(z[6]),
+              "r"(z[7]), "r"(z[8]), "r"(z[9]), "r"(z[10]), "r"(z[11]), "r"(z[12]), "r"(z[13]),
+              "r"(z[14]), "r"(z[15])
+              : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    // remote (cluster) address of CTA 0's ready barriers
+    uint32_t ready0;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ready0) : "r"(ready_a));
+    // this thread's A row (code 128 rank + row of the chunk) in buffer 0
+    const uint32_t a_row0 = sA_a + (uint32_t)((row >> 3) * SBO + 16 * (row & 7) + 128 * j0);
+    const int crow = (int)rank * kTcCodes + row;  // code within the chunk
+    uint32_t gt = 0;
+    // Survivor stash: a lane with survivors parks its packed sums in shared
+    // memory (up to 4 codes per warp) and the warp handles them while it
+    // would otherwise wait for the next MMA, off the MMA's critical path.
+    int ns = 0;  // warp-uniform
+    auto process_one = [&](int k) {
+      const uint32_t vv = s.xfer[w][k][lane];
+      const int q = col0 + 2 * lane;
+      const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
+      tc_hit_warp(a, (x & 0x8000u) != 0, (x & 0x80000000u) != 0, q, vv, s.stash_pos[w][k]);
+      __syncwarp();
+    };
+    auto arrive_ready = [&](uint32_t b) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(ready0 + 8 * b) : "memory");
+    };
+    for (int item = pair; item < n_items; item += npair) {
+      const WorkItem it = a.items[item];
+      const int nq = it.pair_count;
+      const int n_mma = max(16, (nq + 15) & ~15);
+      const int half = n_mma >> 1;
+      const int64_t c0g = it.chunk_begin;
+      const int64_t ntiles = it.chunk_end - it.chunk_begin;
+      // every compute thread is past the previous item (its tiles' MMAs all
+      // completed: B and the query state may be overwritten; its stashed
+      // survivors handled)
+      while (ns > 0) process_one(--ns);
+      asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+      // ---- stage this CTA's half of B and the item's query state ----
+      for (int e = tid; e < half * MC; e += NT) {
+        const int r = e / MC, j = e - r * MC;
+        const int q = (int)rank * half + r;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (q < nq) v = ((const uint4 *)a.qt)[(size_t)a.pair_t[it.pair_begin + q] * MC + j];
+        *(uint4 *)(sB + (r >> 3) * SBO + j * 128 + (r & 7) * 16) = v;
+      }
+      if (tid < kTcNQ) {
+        const int q = tid;
+        int thr = -1;
+        unsigned mb = 0;
+        if (q < nq) {
+          const int pi = it.pair_begin + q;
+          const int query = a.pair_q[pi], t = a.pair_t[pi];
+          s.query[q] = query;
+          s.qmin[q] = a.qmin_f[t];
+          s.delta[q] = a.delta_f[t];
+          mb = *(volatile unsigned *)&a.M_bits[query];
+          thr = q_threshold(__uint_as_float(mb), s.qmin[q], s.delta[q]);
+        } else {
+          s.query[q] = 0;
+          s.qmin[q] = 0.f;
+          s.delta[q] = 0.f;
+        }
+        s.thr16[q] = (uint16_t)(thr + 0x8000);
+        s.mc[q] = mb;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+      // ---- prologue: expand tiles 0 and 1 (every earlier MMA completed:
+      // both A buffers and both D buffers are free), load tile 2's words ----
+      uint32_t cw[MH];
+      tc_load<MC, MH>(a, c0g, crow, j0, cw);
+      tc2_expand<MH>(a_row0 + (gt & 1) * kATile, cw, crow);
+      arrive_ready(gt & 1);
+      if (ntiles > 1) {
+        tc_load<MC, MH>(a, c0g + 1, crow, j0, cw);
+        tc2_expand<MH>(a_row0 + ((gt + 1) & 1) * kATile, cw, crow);
+        arrive_ready((gt + 1) & 1);
+        if (ntiles > 2) tc_load<MC, MH>(a, c0g + 2, crow, j0, cw);
+      }
+      // valid byte of this thread's code, one tile ahead (read by the
+      // survivor path only)
+      uint32_t vb_next = __ldg(a.valid + c0g * 32 + (crow >> 3));
+      for (int64_t t = 0; t < ntiles; t++, gt++) {
+        const uint32_t b = gt & 1;
+        const int64_t g_t = c0g + t;
+        unsigned mpre = 0;
+        if (tid < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[tid]];
+        // ---- tile t: wait for MMA(t) (handling stashed survivors while it
+        // runs), copy the sums out of D[b] ----
+        while (ns > 0 && !tc_try_warp(done_a + 8 * b, (gt >> 1) & 1)) process_one(--ns);
+        tc_wait(done_a + 8 * b, (gt >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        uint32_t v[kCPT / 2];
+        tc_ld64p(t_row + b * kTcNQ + col0, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // ---- expand tile t + 2 into A[b] (its reader MMA(t) completed) and
+        // release it with D[b]: MMA(t + 2) can follow MMA(t + 1) at once,
+        // and the survivor test and hits of tile t below run while MMA(t + 1)
+        // executes. Global loads are issued after the arrive, so its fence
+        // never waits for them ----
+        if (t + 2 < ntiles) {
+          if (!(a.dbg & 2)) tc2_expand<MH>(a_row0 + b * kATile, cw, crow);
+          arrive_ready(b);
+          if (t + 3 < ntiles) tc_load<MC, MH>(a, c0g + t + 3, crow, j0, cw);
+        }
+        const uint32_t vb_t = vb_next;
+        if (t + 1 < ntiles) vb_next = __ldg(a.valid + (g_t + 1) * 32 + (crow >> 3));
+        const uint4 *T = (const uint4 *)&s.thr16[col0];
+        uint32_t any = 0;
+#pragma unroll
+        for (int i = 0; i < kCPT / 2 && !(a.dbg & 8); i += 4) {
+          const uint4 tt = T[i / 4];
+          any |= (tt.x - v[i]) | (tt.y - v[i + 1]) | (tt.z - v[i + 2]) | (tt.w - v[i + 3]);
+        }
+        unsigned todo = __ballot_sync(kFull, (any & 0x80008000u) && !(a.dbg & 1));
+        if (todo) {
+          // validity (padding codes have id -1) is checked only here, off
+          // the tile's critical path
+          todo &= __ballot_sync(kFull, (vb_t >> (crow & 7)) & 1u);
+          if (a.dbg & 256) todo = 0;  // timing experiment: test and validity, no hit handling
+        }
+        while (todo) {
+          if (ns == 4) process_one(--ns);  // stash full: make room
+          const int src = __ffs(todo) - 1;
+          todo &= todo - 1;
+          if (lane == src) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *(uint4 *)&s.xfer[w][ns][i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            s.stash_pos[w][ns] = g_t * kChunkCodes + crow;
+          }
+          __syncwarp();
+          ns++;
+        }
+        if (tid < nq && mpre < s.mc[tid]) {
+          s.mc[tid] = mpre;
+          const int th = q_threshold(__uint_as_float(mpre), s.qmin[tid], s.delta[tid]);
+          if (th + 0x8000 < (int)s.thr16[tid]) s.thr16[tid] = (uint16_t)(th + 0x8000);
+        }
+      }
+    }
+    while (ns > 0) process_one(--ns);
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    if (tid == 0) *(volatile int *)&s.done = 1;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();  // the pair's MMAs and tcgen05.ld are all complete
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (w == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(s.tmem), "n"(kCols));
+}
+
 template <int MC>
 size_t tc2_smem_bytes() { return (size_t)(kTcNQ / 2) * 16 * MC + 2 * (size_t)kTcCodes * 16 * MC; }
 
 template <int MC>
 void launch_tc2(const ScanArgs &a, int nsm, cudaStream_t st) {
   const size_t smem = tc2_smem_bytes<MC>();
+  if (a.pair_cta == 2) {
+    cudaFuncSetAttribute(k_scan_tc2i<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_tc2i<MC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    k_scan_tc2i<MC><<<nsm & ~1, 576, smem, st>>>(a);
+    return;
+  }
   cudaFuncSetAttribute(k_scan_tc2<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_scan_tc2<MC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   k_scan_tc2<MC><<<nsm & ~1, 128 * 4 + 32 * (kFlushers + 1), smem, st>>>(a);

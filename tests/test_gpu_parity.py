@@ -302,6 +302,19 @@ def test_tensor_core_scan_edge_cases_vs_oracle(gpu):
                     assert np.array_equal(res.counts, on), (n, nq, R, scan)
 
 
+def test_tensor_core_scan_long_list_vs_oracle(gpu):
+    """A list long enough (>= 8192 chunks) for the CTA-pair scan's flusher
+    rings, bit-exact against the oracle (two query items per code range)."""
+    rng = np.random.default_rng(12)
+    idx, flat, qs, cb = _random_flat(rng, 2_200_000, 32, 128, 264)
+    oi, od, on, _ = orc.search_batch(qs, cb, None, None, 1, flat, 100, 1000)
+    res = idx.search(qs, 100, init=1000, scan="tc")
+    assert res.stats["scan_tc"] == 1
+    assert np.array_equal(res.ids, oi)
+    assert np.array_equal(_bits(res.distances), _bits(od))
+    assert np.array_equal(res.counts, on)
+
+
 @pytest.mark.parametrize("n", [60_000, 200_000])
 def test_massive_ties_vs_oracle(gpu, n):
     """Three code patterns only (about n, n/7 and n/40 copies): every lane
