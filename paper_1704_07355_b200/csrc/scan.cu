@@ -112,6 +112,39 @@ __device__ __forceinline__ unsigned hist_bound(const ScanArgs &a, int query) {
   return fbits(__fmul_rn((float)(b + 2), hw));
 }
 
+// Two-level variant for the PRMT scan, whose compute warps refresh the
+// bound inline: 2 x 128 bytes (coarse sums, then one row of fine bins)
+// instead of the whole histogram. Needs the coarse sums kept by that
+// kernel's appends (h[kHistBins + b / 32]).
+__device__ __forceinline__ unsigned hist_bound2(const ScanArgs &a, int query) {
+  const int lane = threadIdx.x & 31;
+  const float hw = a.hist_w[query];
+  if (!(hw > 0.f)) return 0x7f800000u;
+  const unsigned *h = a.hist + (size_t)query * kHistWords;
+  const unsigned c = *(volatile const unsigned *)&h[kHistBins + lane];
+  unsigned incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const unsigned R = (unsigned)a.R;
+  const unsigned hit = __ballot_sync(kFull, incl >= R);
+  if (!hit) return 0x7f800000u;
+  const int k = __ffs(hit) - 1;
+  const unsigned base = __shfl_sync(kFull, incl - c, k);
+  const unsigned f = *(volatile const unsigned *)&h[k * 32 + lane];
+  unsigned fi = f;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, fi, o);
+    if (lane >= o) fi += y;
+  }
+  const unsigned hit2 = __ballot_sync(kFull, base + fi >= R);
+  const int b = k * 32 + (hit2 ? __ffs(hit2) - 1 : 31);
+  return fbits(__fmul_rn((float)(b + 2), hw));
+}
+
 // Global append of every buffered entry of (warp, q) whose midpoint is <=
 // the query's current bound; empties the buffer.
 __device__ __noinline__ void flush_buffer(const ScanArgs &a, Smem &s, uint32_t *buf, int w, int q) {
@@ -303,6 +336,7 @@ __device__ __noinline__ void append(const ScanArgs &a, Smem &s, uint32_t *buf, i
         // (b + 2) * w keeps one bucket of slack)
         const int b = min((int)__fmul_rn(midpoint(qmin, delta, (int)v), hinv), kHistBins - 1);
         atomicAdd(&h[b], 1u);
+        atomicAdd(&h[kHistBins + (b >> 5)], 1u);  // coarse sums for hist_bound2
       }
     }
   }
@@ -316,7 +350,7 @@ __device__ __noinline__ void append(const ScanArgs &a, Smem &s, uint32_t *buf, i
   // (read once per bound_every appended candidates: the histogram read and
   // its two warp scans cost more than the appends themselves)
   if (pend >= a.bound_every) {
-    const unsigned mb = hist_bound(a, query);
+    const unsigned mb = hist_bound2(a, query);
     if (lane == 0 && mb < s.mc[w][q]) {
       atomicMin(&a.M_bits[query], mb);
       s.mc[w][q] = mb;
