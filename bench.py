@@ -316,9 +316,17 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # developer check of the multi-rank logic on a one-GPU box (not a
+    # measurement): QADC_BENCH_BACKEND=gloo QADC_BENCH_ONE_DEVICE=1
+    if os.environ.get("QADC_BENCH_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("QADC_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     _native.require_device()
     from paper_1704_07355_b200.workload import (IVF_CONFIGS, build_ivf_index,
                                                 build_sharded_ivf_index, load_ivf_model)
