@@ -1340,7 +1340,7 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
 // filters by the cached bound and appends (compacted, up to 32 candidates'
 // slot claims and id reads in flight together). Compute warps, on whose
 // timeliness every MMA depends, never run the per-pair survivor path.
-constexpr int kWRing = 8;       // slots per compute warp
+constexpr int kWRing = 10;      // slots per compute warp
 constexpr int kFlushers = 4;    // flusher warps (flusher f serves compute warps kPerF f .. kPerF f + kPerF - 1)
 constexpr int kPerF = 16 / kFlushers;
 struct Tc2Ent {
