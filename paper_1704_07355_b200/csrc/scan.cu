@@ -1369,6 +1369,50 @@ struct Tc2Smem {
 };
 __shared__ Tc2Smem g_tc2;
 
+// Bound of one query per lane (lane-parallel: all crossing queries of an
+// append batch refresh in two L2 round trips): coarse sums, then the fine
+// bins of the coarse bucket holding the R-th candidate.
+__device__ __forceinline__ unsigned hist_bound_lane(const ScanArgs &a, int query) {
+  const float hw = a.hist_w[query];
+  if (!(hw > 0.f)) return 0x7f800000u;
+  const unsigned *h = a.hist + (size_t)query * kHistWords;
+  const unsigned R = (unsigned)a.R;
+  uint4 c4[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) c4[i] = __ldcg((const uint4 *)(h + kHistBins) + i);
+  unsigned cum = 0;
+  int k = -1;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const unsigned w4[4] = {c4[i].x, c4[i].y, c4[i].z, c4[i].w};
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      if (k < 0) {
+        if (cum + w4[j] >= R) k = 4 * i + j;
+        else cum += w4[j];
+      }
+  }
+  if (k < 0) return 0x7f800000u;
+  uint4 f4[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) f4[i] = __ldcg((const uint4 *)(h + 32 * k) + i);
+  int b = 31;
+  bool found = false;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const unsigned w4[4] = {f4[i].x, f4[i].y, f4[i].z, f4[i].w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      cum += w4[j];
+      if (!found && cum >= R) {
+        b = 4 * i + j;
+        found = true;
+      }
+    }
+  }
+  return fbits(__fmul_rn((float)(k * 32 + b + 2), hw));
+}
+
 // Appends the compacted candidates cl[0, cnt) (one per lane per pass) and
 // refreshes the bound of queries crossing a multiple of bound_every.
 __device__ __forceinline__ void tc2_append(const ScanArgs &a, const Tc2Cand *cl, int cnt) {
@@ -1393,16 +1437,11 @@ __device__ __forceinline__ void tc2_append(const ScanArgs &a, const Tc2Cand *cl,
         unsigned *h = a.hist + (size_t)qy * kHistWords;
         const int b = min((int)__fmul_rn(mid, __frcp_rn(hw)), kHistBins - 1);
         atomicAdd(&h[b], 1u);
+        atomicAdd(&h[kHistBins + (b >> 5)], 1u);  // coarse sums (hist_bound_lane)
       }
     }
-    unsigned mq = __ballot_sync(kFull, has && (slot + 1) % (unsigned)a.bound_every == 0);
-    while (mq) {
-      const int src = __ffs(mq) - 1;
-      mq &= mq - 1;
-      const int query = __shfl_sync(kFull, qy, src);
-      const unsigned mb = hist_bound(a, query);
-      if (lane == 0) atomicMin(&a.M_bits[query], mb);
-    }
+    if (has && (slot + 1) % (unsigned)a.bound_every == 0)
+      atomicMin(&a.M_bits[qy], hist_bound_lane(a, qy));
   }
 }
 
