@@ -302,11 +302,12 @@ def test_tensor_core_scan_edge_cases_vs_oracle(gpu):
                     assert np.array_equal(res.counts, on), (n, nq, R, scan)
 
 
-def test_tensor_core_scan_long_list_vs_oracle(gpu):
+@pytest.mark.parametrize("m", [16, 32])
+def test_tensor_core_scan_long_list_vs_oracle(gpu, m):
     """A list long enough (>= 8192 chunks) for the CTA-pair scan's flusher
     rings, bit-exact against the oracle (two query items per code range)."""
-    rng = np.random.default_rng(12)
-    idx, flat, qs, cb = _random_flat(rng, 2_200_000, 32, 128, 264)
+    rng = np.random.default_rng(12 + m)
+    idx, flat, qs, cb = _random_flat(rng, 2_200_000, m, 128, 264)
     oi, od, on, _ = orc.search_batch(qs, cb, None, None, 1, flat, 100, 1000)
     res = idx.search(qs, 100, init=1000, scan="tc")
     assert res.stats["scan_tc"] == 1
