@@ -43,6 +43,17 @@ def test_library_loads_and_exports_every_declared_symbol():
         assert hasattr(lib, name), name
 
 
+def test_search_flags_match_header():
+    """The ctypes flag constants are the header's #defines (the C ABI a
+    maintainer binds)."""
+    hdr = (ROOT / "include" / "qadc_b200.h").read_text()
+    defs = {k: int(v) for k, v in re.findall(r"#define QADC_B200_(\w+) (\d+)u", hdr)}
+    for name in ("HOST_IO", "LUT_IN", "NO_FSAT", "SCAN_PRMT", "SCAN_TC", "SCAN_TC1"):
+        assert defs[name] == getattr(_native, name), name
+    flags = [defs[n] for n in ("HOST_IO", "LUT_IN", "NO_FSAT", "SCAN_PRMT", "SCAN_TC", "SCAN_TC1")]
+    assert len(set(flags)) == len(flags) and all(f & (f - 1) == 0 for f in flags)
+
+
 def test_reference_abi_signatures_match_reference_header():
     """Argument lists of the four replaced functions equal the reference's
     (scan_kernels.h), parameter for parameter."""
