@@ -159,10 +159,13 @@ QADC_API int64_t qadc_b200_index_bytes(const qadc_b200_index *idx);
  * With QADC_B200_LUT_IN, lut_in (nq, ma, m, 16) fp32 and cells_in (nq, ma)
  * replace the probe and table phases ("reference-LUT-injected" mode).
  * stream is a cudaStream_t (NULL = legacy default stream).
- * stats (optional, 8 int64): [0] codes scanned, [1] scan candidates,
+ * stats (optional, 16 int64): [0] codes scanned, [1] scan candidates,
  * [2] overflow reruns, [3] scan kernel launches, [4] total kernel launches,
  * [5] scan kernel microseconds (event timed), [6] 1 if the scan ran on the
- * tensor cores, [7] reserved.
+ * tensor cores, then event-timed microseconds of the other phases of the
+ * first pass (adc.py:140-179's Index / Tables / Scan split): [7] probe,
+ * [8] tables (residual, rotation, LUT, qmax, quantize, prefix facts),
+ * [9] work list, [10] exact top-R select; [11..15] reserved (0).
  */
 QADC_API int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries,
                            int nq, int R, int ma, int init, unsigned flags,
@@ -171,6 +174,18 @@ QADC_API int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries,
                            void *stream, int64_t *stats);
 
 /* ---- device-pointer building blocks (parity tests, diagnostics) ---- */
+
+/* The Index + Tables phases of search_batch (adc.py:140-174) with their
+ * intermediates, for parity accounting of native mode: cells_out (nq, ma)
+ * int64 (IVF; ignored for a flat index), lut_out (nq, ma, m, 16) fp32
+ * (residual, OPQ rotation, compute_tables), qmax_out (nq) fp32 (find_qmax
+ * on the first probed cell), qt_out (nq, ma, m, 16) uint8
+ * (quantize_tables), qmin_out / delta_out (nq, ma) the fp32 casts the scan
+ * uses. Device pointers; ma is 1 for a flat index. */
+QADC_API int qadc_b200_search_tables(qadc_b200_index *idx, const float *queries, int nq,
+                                     int R, int ma, int init, int64_t *cells_out,
+                                     float *lut_out, float *qmax_out, uint8_t *qt_out,
+                                     float *qmin_out, float *delta_out, void *stream);
 
 /* adc.py:61-75 compute_tables for npairs residual queries y (npairs, d):
  * out (npairs, m, 16) fp32, NumPy einsum summation order. */

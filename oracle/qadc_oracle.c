@@ -120,19 +120,29 @@ void orc_probe(const float *cent, int K, int d, const float *q, int ma,
     free(bd);
 }
 
-/* adc.py:108-111 (v @ R^T). OpenBLAS sgemv's summation order is not
- * reproducible, so the restatement fixes one: a sequential
- * fp32 fused-multiply-add chain over k — the GPU kernel's arithmetic
- * (k_residual_lut), so native-OPQ GPU results are bit-exact against this
- * port while both differ from OpenBLAS by rare low-bit flips. */
+/* adc.py:108-111 _rotate: (v @ R.T) with a 1-D v = OpenBLAS sgemv_t
+ * (numpy 2.3 + scipy-openblas 0.3.30 DYNAMIC_ARCH, core "SkylakeX";
+ * the Haswell kernel family). Its summation order, identified bit-for-bit
+ * against numpy on this project's hosts for every d >= 16 with d % 8 == 0
+ * (tests/test_oracle.py pins it): eight fp32 FMA lane accumulators, lane l
+ * taking k = l, l + 8, ... ascending; t_l = acc_l + acc_{l+4} (l < 4);
+ * y = (t0 + t1) + (t2 + t3). Other d keep the same formula (OpenBLAS
+ * takes a different tail path there; no configuration uses them with a
+ * rotation). */
 void orc_rotate(const float *R, int d, const float *v, float *out)
 {
-    int i, k;
+    int i, k, l;
     for (i = 0; i < d; i++) {
-        float acc = 0.0f;
-        for (k = 0; k < d; k++)
-            acc = fmaf(R[(size_t)i * d + k], v[k], acc);
-        out[i] = acc;
+        float a[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t0, t1, t2, t3;
+        for (k = 0; k < d; k++) {
+            l = k & 7;
+            a[l] = fmaf(R[(size_t)i * d + k], v[k], a[l]);
+        }
+        t0 = a[0] + a[4];
+        t1 = a[1] + a[5];
+        t2 = a[2] + a[6];
+        t3 = a[3] + a[7];
+        out[i] = (t0 + t1) + (t2 + t3);
     }
 }
 

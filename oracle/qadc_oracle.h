@@ -34,9 +34,9 @@ void orc_compute_tables(const float *codebooks, int m, int dsub,
 void orc_probe(const float *cent, int K, int d, const float *q, int ma,
                int64_t *cells, float *residuals);
 
-/* adc.py:108-111 _rotate as a sequential fp32 FMA chain (the GPU's
- * arithmetic). NOT bit-exact vs OpenBLAS sgemv; tests that
- * compare against the reference state "native OPQ" tolerance. */
+/* adc.py:108-111 _rotate (v @ R^T) in OpenBLAS sgemv_t's summation order
+ * (SkylakeX/Haswell kernels: 8 FMA lanes, folded (l, l+4), then pairwise),
+ * identified bit-for-bit against numpy on this host (tests/test_oracle.py). */
 void orc_rotate(const float *R, int d, const float *v, float *out);
 
 /* qadc.py:157-194 find_qmax over ONE cell (the search path only ever

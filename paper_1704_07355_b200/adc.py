@@ -124,17 +124,34 @@ def _rotate(pq, v: np.ndarray) -> np.ndarray:
 
 def device_index(index, pq) -> DeviceIndex:
     """The DeviceIndex for (index, pq), built on first use and cached on
-    the index object."""
-    key = (id(pq), id(pq.codebooks), id(getattr(pq, "rotation", None)), len(index.lists))
+    the index object. The key holds the identity of the quantizer arrays
+    and of every list (object, code / block array, count), so replacing or
+    re-encoding a list, or a new quantizer, rebuilds the device copy; the
+    cached entry keeps references to the keyed objects, so their ids cannot
+    be recycled while it lives. `invalidate_device_index` drops it
+    explicitly (in-place edits of a list's arrays are not detectable)."""
+    parts = [pq, pq.codebooks, getattr(pq, "rotation", None), index.coarse]
+    for lst in index.lists:
+        parts += [lst, getattr(lst, "blocks", getattr(lst, "codes", None)), lst.ids]
+    key = tuple(id(p) for p in parts) + tuple(int(lst.count) for lst in index.lists)
     cached = getattr(index, "_b200_device", None)
     if cached is not None and cached[0] == key:
         return cached[1]
     dev = DeviceIndex.from_ivf(index, pq)
     try:
-        index._b200_device = (key, dev)
+        index._b200_device = (key, dev, parts)
     except AttributeError:
         pass
     return dev
+
+
+def invalidate_device_index(index) -> None:
+    """Drop the cached device copy of `index` (after editing its lists in
+    place)."""
+    cached = getattr(index, "_b200_device", None)
+    if cached is not None:
+        cached[1].close()
+        index._b200_device = None
 
 
 def _validate(index, pq, R: int, method: str) -> None:
@@ -196,11 +213,17 @@ def search(index, pq, query, R: int, ma: int = 1, method: str = "adc",
         res = dev.search(q[None], R, ma=ma, init=init)
         t2 = time.perf_counter()
         n = int(res.counts[0])
-        # one fused device call: the whole search is reported as Scan; the
-        # one-time index upload (first call only) as Index
-        idx_ms, scan_ms = (t1 - t0) * 1e3, (t2 - t1) * 1e3
+        # phases from the device events of the call (adc.py:140-179): Index
+        # = probe (+ the one-time index upload on the first call), Tables =
+        # residual, rotation, LUT, qmax, quantize; Scan = the rest of the
+        # call's wall time (work list, scan, exact top-R, host overhead)
+        st = res.stats
+        idx_ms = (t1 - t0) * 1e3 + st["probe_us"] / 1e3
+        tab_ms = st["tables_us"] / 1e3
+        scan_ms = max(0.0, (t2 - t1) * 1e3 - (st["probe_us"] + st["tables_us"]) / 1e3)
         return SearchResult(ids=res.ids[0, :n].copy(), distances=res.distances[0, :n].copy(),
-                            timings=PhaseTimings(idx_ms, 0.0, scan_ms, idx_ms + scan_ms))
+                            timings=PhaseTimings(idx_ms, tab_ms, scan_ms,
+                                                 idx_ms + tab_ms + scan_ms))
     # float-table ADC (method="adc")
     t0 = time.perf_counter()
     if index.coarse is None:

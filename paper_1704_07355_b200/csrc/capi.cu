@@ -130,7 +130,25 @@ struct SearchStats {
   int64_t codes = 0, cands = 0, reruns = 0, scan_launches = 0, launches = 0;
   double scan_us = 0.0;
   int scan_tc = 0;  // the scan ran on the tensor cores
+  // device time per phase of the first pass (adc.py:140-179's Index /
+  // Tables / Scan split; the work list and the exact top-R are the GPU's
+  // own phases), CUDA events on the search stream
+  double probe_us = 0.0, tables_us = 0.0, work_us = 0.0, select_us = 0.0;
 };
+
+// Phase events of search_impl, created once per host thread.
+enum { kEvStart, kEvProbe, kEvTables, kEvScan0, kEvScan1, kEvSelect, kEvCount };
+cudaEvent_t *phase_events() {
+  static thread_local cudaEvent_t ev[kEvCount];
+  static thread_local int dev_made = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev_made != dev) {
+    for (auto &e : ev) cudaEventCreate(&e);
+    dev_made = dev;
+  }
+  return ev;
+}
 
 // Keep stream-ordered workspace in the device pool between calls (the
 // default release threshold of 0 returns it to the OS at every sync, which
@@ -145,6 +163,20 @@ void retain_pool_memory() {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   done_dev = dev;
+}
+
+// ivf.py:166-182 probe of the index's coarse quantizer: cells (nq, ma).
+void index_probe(const qadc_b200_index *idx, const float *queries, int nq, int ma, int64_t *cells,
+                 cudaStream_t st) {
+  static const int probe_kind = scan_env_int("QADC_B200_PROBE", 2);  // 2 gemm, 1 ffma, 0 exact
+  const bool done =
+      (probe_kind >= 2 && idx->pcsplit &&
+       launch_probe_gemm(idx->coarse, idx->pmu, idx->pcsplit, idx->pcn2, idx->K, idx->d, queries,
+                         nq, ma, cells, st)) ||
+      (probe_kind >= 1 && idx->cnorm &&
+       launch_probe_fast(idx->coarseT, idx->coarse, idx->cnorm, idx->K, idx->d, queries, nq, ma,
+                         cells, st));
+  if (!done) launch_probe(idx->coarseT, idx->K, idx->d, queries, nq, ma, cells, st);
 }
 
 int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int ma, int init,
@@ -177,27 +209,21 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   DevBuf<unsigned> cls;
   int rc = 0;
 
+  cudaEvent_t *ev = phase_events();
+  if (depth == 0) cudaEventRecord(ev[kEvStart], st);
   const int64_t *cells = nullptr;
   if (idx->K) {
     if (cells_in) {
       cells = cells_in;
     } else {
       if ((rc = cells_b.alloc(npairs, st))) return cuda_fail(cudaGetLastError(), "alloc cells");
-      static const int probe_kind = scan_env_int("QADC_B200_PROBE", 2);  // 2 gemm, 1 ffma, 0 exact
-      const bool done =
-          (probe_kind >= 2 && idx->pcsplit &&
-           launch_probe_gemm(idx->coarse, idx->pmu, idx->pcsplit, idx->pcn2, idx->K, idx->d,
-                             queries, nq, ma, cells_b.p, st)) ||
-          (probe_kind >= 1 && idx->cnorm &&
-           launch_probe_fast(idx->coarseT, idx->coarse, idx->cnorm, idx->K, idx->d, queries, nq,
-                             ma, cells_b.p, st));
-      if (!done)
-        launch_probe(idx->coarseT, idx->K, idx->d, queries, nq, ma, cells_b.p, st);
+      index_probe(idx, queries, nq, ma, cells_b.p, st);
       QADC_CUDA(cudaGetLastError());
       ss.launches++;
       cells = cells_b.p;
     }
   }
+  if (depth == 0) cudaEventRecord(ev[kEvProbe], st);
   const float *lut = lut_in;
   if (!lut) {
     if (lut_b.alloc(npairs * m * 16, st)) return cuda_fail(cudaGetLastError(), "alloc lut");
@@ -222,7 +248,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   static const int variant_stats = scan_env_int("QADC_B200_VARIANT_STATS", 0);
   static const int no_order = scan_env_int("QADC_B200_NO_ORDER", 0);
 
-  launch_qmax(idx, lut, cells, nq, nslots, R, init, qmax_b.p, st);
+  if ((rc = launch_qmax(idx, lut, cells, nq, nslots, R, init, qmax_b.p, st))) return rc;
   launch_quantize(lut, (int)npairs, m, qmax_b.p, nslots, nullptr, nullptr, qt_b.p, qmin_f.p,
                   delta_f.p, nullptr, nullptr, st, max_depth, pair_depth.p);
   launch_prefix(idx, qt_b.p, qmin_f.p, delta_f.p, cells, nq, nslots, R, init, M_bits.p, fsat_n.p,
@@ -231,6 +257,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   QADC_CUDA(cudaGetLastError());
   ss.launches += 4;
   if (no_fsat) cudaMemsetAsync(fsat_n.p, 0, sizeof(int) * nq, st);
+  if (depth == 0) cudaEventRecord(ev[kEvTables], st);
 
   // ---- work list ----
   const int nsm = device_sms();
@@ -329,9 +356,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   static const int tc_dbg = scan_env_int("QADC_B200_TC_DEBUG", 0);
   a.dbg = tc_dbg;
   a.pair_cta = pair_cta;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  cudaEvent_t e0 = ev[kEvScan0], e1 = ev[kEvScan1];
   cudaEventRecord(e0, st);
   launch_scan(a, nsm, st, prmt);
   if (tc_dbg & 64) {
@@ -347,6 +372,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
                 fsat_id.p, out_ids, out_d, out_n, overflow.p, st);
   ss.launches++;
   QADC_CUDA(cudaGetLastError());
+  cudaEventRecord(ev[kEvSelect], st);
 
   // ---- overflow handling (rare: massive ties or very loose early bounds) ----
   std::vector<int> h_over(nq);
@@ -366,8 +392,17 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   ss.scan_us += ms * 1e3;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  if (depth == 0) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ev[kEvStart], ev[kEvProbe]);
+    ss.probe_us += t * 1e3;
+    cudaEventElapsedTime(&t, ev[kEvProbe], ev[kEvTables]);
+    ss.tables_us += t * 1e3;
+    cudaEventElapsedTime(&t, ev[kEvTables], e0);
+    ss.work_us += t * 1e3;
+    cudaEventElapsedTime(&t, e1, ev[kEvSelect]);
+    ss.select_us += t * 1e3;
+  }
   for (int q = 0; q < nq; q++) ss.cands += std::min<unsigned>(h_cn[q], (unsigned)cap_g);
   std::vector<int> rerun, big;
   unsigned need = 0;
@@ -829,8 +864,39 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
     stats[4] = ss.launches;
     stats[5] = (int64_t)llround(ss.scan_us);
     stats[6] = ss.scan_tc;  // scan kernel: 1 = int8 tensor-core, 0 = PRMT
-    stats[7] = 0;
+    stats[7] = (int64_t)llround(ss.probe_us);
+    stats[8] = (int64_t)llround(ss.tables_us);
+    stats[9] = (int64_t)llround(ss.work_us);
+    stats[10] = (int64_t)llround(ss.select_us);
+    for (int i = 11; i < 16; i++) stats[i] = 0;
   }
+  return kOk;
+}
+
+extern "C" int qadc_b200_search_tables(qadc_b200_index *idx, const float *queries, int nq,
+                                       int R, int ma, int init, int64_t *cells_out,
+                                       float *lut_out, float *qmax_out, uint8_t *qt_out,
+                                       float *qmin_out, float *delta_out, void *stream) {
+  g_err.clear();
+  if (!idx || !queries || !lut_out || !qmax_out || !qt_out || !qmin_out || !delta_out)
+    return arg_error("null argument");
+  if (R < 1 || init < 1 || nq < 0) return arg_error("invalid R / init / nq");
+  if (idx->K && (ma < 1 || ma > idx->K)) return arg_error("ma must be in 1..K");
+  if (idx->K && !cells_out) return arg_error("an IVF index needs cells_out");
+  cudaStream_t st = (cudaStream_t)stream;
+  retain_pool_memory();
+  if (nq == 0) return kOk;
+  const int nslots = idx->K ? ma : 1;
+  const int64_t *cells = nullptr;
+  if (idx->K) {
+    index_probe(idx, queries, nq, ma, cells_out, st);
+    cells = cells_out;
+  }
+  launch_residual_lut(idx, queries, cells, nq, nslots, lut_out, st);
+  if (int rc = launch_qmax(idx, lut_out, cells, nq, nslots, R, init, qmax_out, st)) return rc;
+  launch_quantize(lut_out, nq * nslots, idx->m, qmax_out, nslots, nullptr, nullptr, nullptr,
+                  qmin_out, delta_out, nullptr, qt_out, st);
+  QADC_CUDA(cudaGetLastError());
   return kOk;
 }
 

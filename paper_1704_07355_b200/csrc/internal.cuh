@@ -90,7 +90,7 @@ bool launch_probe_gemm(const float *coarse, const float *mu, const void *csplit,
 void launch_residual_lut(const qadc_b200_index *idx, const float *queries,
                          const int64_t *cells, int nq, int nslots,
                          float *lut, cudaStream_t st);
-void launch_qmax(const qadc_b200_index *idx, const float *lut,
+int launch_qmax(const qadc_b200_index *idx, const float *lut,
                  const int64_t *cells, int nq, int nslots, int R, int init,
                  float *qmax, cudaStream_t st);
 void launch_quantize(const float *lut, int npairs, int m, const float *qmax_per_query,

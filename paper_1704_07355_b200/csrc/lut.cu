@@ -385,28 +385,32 @@ __global__ void __launch_bounds__(256) k_probe_fast(
 
 // ---------------- residual + rotation + LUT (adc.py:108-111, 141-148,
 // ivf.py:181-182) ----------------
-// One CTA per (query, probe slot). residual = q - C[cell] in fp32; OPQ
-// rotation y = R r accumulated in float64 and rounded once (the reference
-// uses OpenBLAS sgemv whose order is unpinned: rotated
-// configs are "native OPQ" parity with counted bucket flips).
+// kLutPairs (query, probe slot) pairs per CTA. residual = q - C[cell] in
+// fp32. OPQ rotation y = R r in the reference's own arithmetic: _rotate
+// computes (v @ R.T) with a 1-D v, i.e. OpenBLAS sgemv_t (numpy's
+// scipy-openblas 0.3.30, DYNAMIC_ARCH core "SkylakeX" / Haswell kernels).
+// Its order, identified bit-for-bit on this project's hosts (d >= 16,
+// d % 8 == 0: 100 % of outputs, tests/test_oracle.py): eight fp32 FMA lane
+// accumulators, lane l taking k = l, l + 8, l + 16, ... in ascending k; then
+// t_l = acc_l + acc_{l+4} (l < 4) and y = (t0 + t1) + (t2 + t3). R^T is
+// read through L1 (64 KB, float4 rows: 4 consecutive outputs per thread).
 constexpr int kLutPairs = 16;  // (query, slot) pairs per CTA
 
-// kLutPairs (query, slot) pairs per CTA. OPQ rotation y = R r: the
-// reference calls OpenBLAS sgemv, whose summation order is not reproducible
-// (SURVEY A.7); here y_i = fma-chain over k = 0..d-1 in fp32 (the oracle
-// port restates exactly this order), R staged once per CTA in shared memory
-// as R^T (conflict-free), each thread producing 4 consecutive outputs of
-// one pair from one broadcast r[k].
+__device__ __forceinline__ float blas8_fold(const float (&a)[8]) {
+  return __fadd_rn(__fadd_rn(__fadd_rn(a[0], a[4]), __fadd_rn(a[1], a[5])),
+                   __fadd_rn(__fadd_rn(a[2], a[6]), __fadd_rn(a[3], a[7])));
+}
+
 __global__ void __launch_bounds__(256) k_residual_lut(
     const float *__restrict__ queries, const float *__restrict__ coarse,
     const float *__restrict__ rotation, const float *__restrict__ rotT,
     const float *__restrict__ codebooks, const int64_t *__restrict__ cells, int d, int m,
-    int nslots, int npairs, float *__restrict__ lut) {
+    int nslots, int npairs, int ppc, float *__restrict__ lut) {
   extern __shared__ __align__(16) float smf[];
-  float *sr = smf;                                              // [kLutPairs][d]
-  float *sy = sr + (size_t)kLutPairs * d;                       // [kLutPairs][d]
-  const int p0 = blockIdx.x * kLutPairs;
-  const int np = min(kLutPairs, npairs - p0);
+  float *sr = smf;                                              // [ppc][d]
+  float *sy = sr + (size_t)ppc * d;                             // [ppc][d]
+  const int p0 = blockIdx.x * ppc;
+  const int np = min(ppc, npairs - p0);
   for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
     const int p = e / d, t = e - p * d;
     const int pair = p0 + p;
@@ -416,40 +420,44 @@ __global__ void __launch_bounds__(256) k_residual_lut(
   __syncthreads();
   const float *y = sr;
   if (rotation) {
-    if ((d & 3) == 0 && np == kLutPairs) {
-      // thread tile: 4 consecutive outputs x 4 pairs (16 accumulators), each
-      // k step = one float4 row segment of R^T (L1-resident, coalesced
-      // across the warp) and four broadcast residual values
+    if ((d & 7) == 0) {
+      // thread task: 4 consecutive outputs of one pair, 8 lane accumulators
+      // each; per k one float4 segment of R^T row k and one broadcast r[k]
       const int quads = d >> 2;
-      for (int task = threadIdx.x; task < (kLutPairs / 4) * quads; task += blockDim.x) {
-        const int pg = task / quads, i0 = (task - pg * quads) * 4;
-        const float *r0 = sr + (size_t)(pg * 4) * d;
-        float a[4][4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) a[u][0] = a[u][1] = a[u][2] = a[u][3] = 0.f;
-#pragma unroll 4
-        for (int k = 0; k < d; k++) {
-          const float4 c = __ldg((const float4 *)(rotT + (size_t)k * d + i0));
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const float rv = r0[(size_t)u * d + k];
-            a[u][0] = __fmaf_rn(c.x, rv, a[u][0]);
-            a[u][1] = __fmaf_rn(c.y, rv, a[u][1]);
-            a[u][2] = __fmaf_rn(c.z, rv, a[u][2]);
-            a[u][3] = __fmaf_rn(c.w, rv, a[u][3]);
-          }
-        }
+      for (int task = threadIdx.x; task < np * quads; task += blockDim.x) {
+        const int p = task / quads, i0 = (task - p * quads) * 4;
+        const float *r = sr + (size_t)p * d;
+        float a[4][8];
 #pragma unroll
         for (int u = 0; u < 4; u++)
-          *(float4 *)(sy + (size_t)(pg * 4 + u) * d + i0) = make_float4(a[u][0], a[u][1], a[u][2], a[u][3]);
+#pragma unroll
+          for (int l = 0; l < 8; l++) a[u][l] = 0.f;
+#pragma unroll 1
+        for (int k0 = 0; k0 < d; k0 += 8) {
+#pragma unroll
+          for (int l = 0; l < 8; l++) {
+            const float4 c = __ldg((const float4 *)(rotT + (size_t)(k0 + l) * d + i0));
+            const float rv = r[k0 + l];
+            a[0][l] = __fmaf_rn(c.x, rv, a[0][l]);
+            a[1][l] = __fmaf_rn(c.y, rv, a[1][l]);
+            a[2][l] = __fmaf_rn(c.z, rv, a[2][l]);
+            a[3][l] = __fmaf_rn(c.w, rv, a[3][l]);
+          }
+        }
+        *(float4 *)(sy + (size_t)p * d + i0) =
+            make_float4(blas8_fold(a[0]), blas8_fold(a[1]), blas8_fold(a[2]), blas8_fold(a[3]));
       }
     } else {
       for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
         const int p = e / d, i = e - p * d;
         const float *r = sr + (size_t)p * d;
-        float acc = 0.f;
-        for (int k = 0; k < d; k++) acc = __fmaf_rn(rotT[(size_t)k * d + i], r[k], acc);
-        sy[e] = acc;
+        float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int k0 = 0; k0 < d; k0 += 8) {
+#pragma unroll
+          for (int l = 0; l < 8; l++)
+            if (k0 + l < d) a[l] = __fmaf_rn(rotT[(size_t)(k0 + l) * d + i], r[k0 + l], a[l]);
+        }
+        sy[e] = blas8_fold(a);
       }
     }
     __syncthreads();
@@ -477,13 +485,14 @@ __global__ void __launch_bounds__(256) k_qmax(const uint32_t *__restrict__ codes
                                               const float *__restrict__ lut,
                                               const int64_t *__restrict__ cells, int m, int nslots,
                                               int R, int init, unsigned *__restrict__ scratch,
+                                              int scratch_per_q, int q0,
                                               float *__restrict__ qmax) {
   extern __shared__ unsigned char smem[];
   float *st = (float *)smem;  // m * 16
   __shared__ unsigned hist[256];
   __shared__ unsigned s_prefix;
   __shared__ int s_k;
-  const int q = blockIdx.x;
+  const int q = q0 + blockIdx.x;
   const int pair = q * nslots;
   const int64_t L = cells ? cells[pair] : 0;
   for (int e = threadIdx.x; e < m * 16; e += blockDim.x) st[e] = lut[(size_t)pair * m * 16 + e];
@@ -502,7 +511,7 @@ __global__ void __launch_bounds__(256) k_qmax(const uint32_t *__restrict__ codes
     }
     return;
   }
-  unsigned *keys = scratch + (size_t)q * init;
+  unsigned *keys = scratch + (size_t)blockIdx.x * scratch_per_q;  // take <= scratch_per_q
   const int64_t c0 = chunk_off[L];
   for (int k = threadIdx.x; k < take; k += blockDim.x) {
     float acc = 0.f;
@@ -836,22 +845,37 @@ void launch_residual_lut(const qadc_b200_index *idx, const float *queries, const
                          int nq, int nslots, float *lut, cudaStream_t st) {
   if (nq <= 0) return;
   const int npairs = nq * nslots, d = idx->d;
-  const size_t smem = (size_t)kLutPairs * d * 8;  // residual + rotated, fp32
+  // residual + rotated vectors of ppc pairs in shared memory (fp32): fewer
+  // pairs per CTA for large d so any d fits the 227 KB limit
+  const int ppc = (int)std::max<int64_t>(1, std::min<int64_t>(kLutPairs, (220LL << 10) / (8LL * d)));
+  const size_t smem = (size_t)ppc * d * 8;
   cudaFuncSetAttribute(k_residual_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_residual_lut<<<(npairs + kLutPairs - 1) / kLutPairs, 256, smem, st>>>(
+  k_residual_lut<<<(npairs + ppc - 1) / ppc, 256, smem, st>>>(
       queries, idx->K ? idx->coarse : nullptr, idx->rotation, idx->rotationT, idx->codebooks,
-      cells, d, idx->m, nslots, npairs, lut);
+      cells, d, idx->m, nslots, npairs, ppc, lut);
 }
 
-void launch_qmax(const qadc_b200_index *idx, const float *lut, const int64_t *cells, int nq,
-                 int nslots, int R, int init, float *qmax, cudaStream_t st) {
-  if (nq <= 0) return;
+int launch_qmax(const qadc_b200_index *idx, const float *lut, const int64_t *cells, int nq,
+                int nslots, int R, int init, float *qmax, cudaStream_t st) {
+  if (nq <= 0) return kOk;
+  // per-query key scratch: min(init, longest list) values; queries run in
+  // chunks so the workspace stays <= 256 MB for any init / batch size
+  int64_t longest = 0;
+  for (int64_t c : idx->h_count) longest = std::max(longest, c);
+  const int per_q = (int)std::max<int64_t>(1, std::min<int64_t>(init, longest));
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nq, (256LL << 20) / 4 / per_q));
   unsigned *scratch = nullptr;
-  cudaMallocAsync(&scratch, (size_t)nq * std::max(init, 1) * 4, st);
-  k_qmax<<<nq, 256, (size_t)idx->m * 64, st>>>(idx->pcodes, idx->pchunk_off, idx->count, lut,
-                                               idx->K ? cells : nullptr, idx->m, nslots, R, init,
-                                               scratch, qmax);
+  cudaError_t e = cudaMallocAsync(&scratch, (size_t)chunk * per_q * 4, st);
+  if (e != cudaSuccess) return cuda_fail(e, "alloc qmax scratch");
+  for (int64_t q0 = 0; q0 < nq; q0 += chunk) {
+    const int n = (int)std::min<int64_t>(chunk, nq - q0);
+    k_qmax<<<n, 256, (size_t)idx->m * 64, st>>>(idx->pcodes, idx->pchunk_off, idx->count, lut,
+                                                 idx->K ? cells : nullptr, idx->m, nslots, R, init,
+                                                 scratch, per_q, (int)q0, qmax);
+  }
   cudaFreeAsync(scratch, st);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? kOk : cuda_fail(e, "k_qmax");
 }
 
 void launch_quantize(const float *lut, int npairs, int m, const float *qmax_per_query, int nslots,

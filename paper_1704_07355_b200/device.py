@@ -106,7 +106,7 @@ class DeviceIndex:
 
         lib = _native.load_library()
         st = stream if stream is not None else torch.cuda.current_stream()
-        stats = np.zeros(8, dtype=np.int64)
+        stats = np.zeros(16, dtype=np.int64)
         flags = _native.LUT_IN if lut is not None else 0
         if not with_fsat:
             flags |= _native.NO_FSAT
@@ -142,8 +142,36 @@ class DeviceIndex:
                 _native.dptr(cells_d), _native.dptr(ids), _native.dptr(dist), _native.dptr(cnt),
                 st.cuda_stream, stats.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
         _native.check(rc, "search_batch")
-        keys = ("codes", "candidates", "reruns", "scan_launches", "launches", "scan_us", "scan_tc")
+        keys = ("codes", "candidates", "reruns", "scan_launches", "launches", "scan_us", "scan_tc",
+                "probe_us", "tables_us", "work_us", "select_us")
         return BatchResult(ids, dist, cnt, {k: int(v) for k, v in zip(keys, stats)})
+
+    def tables(self, queries, R: int, ma: int = 1, init: int = 1000, stream=None) -> dict:
+        """The Index + Tables phases of `search` (adc.py:140-174) with their
+        intermediates, for native-mode parity accounting: cells (Q, ma),
+        fp32 LUTs (Q, ma, m, 16), qmax (Q,), uint8 tables (Q, ma, m, 16),
+        and the fp32 qmin / delta (Q, ma) the scan uses. `queries` is a
+        (Q, d) float32 device tensor."""
+        import torch
+
+        st = stream if stream is not None else torch.cuda.current_stream()
+        q = queries.to(dtype=torch.float32).contiguous()
+        nq, dev = q.shape[0], q.device
+        slots = ma if self.K else 1
+        out = {
+            "cells": torch.zeros((nq, slots), dtype=torch.int64, device=dev),
+            "lut": torch.empty((nq, slots, self.m, 16), dtype=torch.float32, device=dev),
+            "qmax": torch.empty(nq, dtype=torch.float32, device=dev),
+            "qt": torch.empty((nq, slots, self.m, 16), dtype=torch.uint8, device=dev),
+            "qmin": torch.empty((nq, slots), dtype=torch.float32, device=dev),
+            "delta": torch.empty((nq, slots), dtype=torch.float32, device=dev),
+        }
+        _native.check(_native.load_library().qadc_b200_search_tables(
+            self._h, _native.dptr(q), nq, R, ma, init,
+            _native.dptr(out["cells"]) if self.K else None, _native.dptr(out["lut"]),
+            _native.dptr(out["qmax"]), _native.dptr(out["qt"]), _native.dptr(out["qmin"]),
+            _native.dptr(out["delta"]), st.cuda_stream), "search_tables")
+        return out
 
     @property
     def nbytes(self) -> int:

@@ -19,6 +19,34 @@ from .device import DeviceIndex
 
 BENCH_DATA = Path(__file__).resolve().parent.parent / "bench_data"
 
+_TIMING = os.environ.get("QADC_BUILD_TIMING") == "1"
+BUILD_TIMES: dict = {}
+
+
+class _phase:
+    """Accumulates device-synchronised wall time of an index-build phase
+    into BUILD_TIMES when QADC_BUILD_TIMING=1 (developer diagnostics)."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if _TIMING:
+            import time
+
+            import torch
+            torch.cuda.synchronize()
+            self.t = time.perf_counter()
+        return self
+
+    def __exit__(self, *a):
+        if _TIMING:
+            import time
+
+            import torch
+            torch.cuda.synchronize()
+            BUILD_TIMES[self.name] = BUILD_TIMES.get(self.name, 0.0) + time.perf_counter() - self.t
+
 
 @dataclass(frozen=True)
 class FlatConfig:
@@ -146,7 +174,8 @@ CFG4_CHUNK = 1_000_000
 
 def load_ivf_model(cfg: IvfConfig):
     if not cfg.coarse_file:
-        return train_ivf_model_gpu(cfg)
+        with _phase("train_model"):
+            return train_ivf_model_gpu(cfg)
     pq = _PQ(np.load(BENCH_DATA / cfg.codebooks_file), np.load(BENCH_DATA / cfg.rotation_file))
     return pq, np.load(BENCH_DATA / cfg.coarse_file)
 
@@ -268,21 +297,26 @@ def ivf_rows(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, device="cuda",
     o = 0
     for a, b, g in spans:
         k = b - a
-        if cfg.sharding == "range":
-            X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + 4, centre_seed=CORPUS,
-                                      stream=datagen.STREAM_BASE * 100_000 + g, device=device)
-            lab = assign_tensor_core(X, C, cn)
-        else:
-            X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000, centre_seed=CORPUS,
-                                      stream=datagen.STREAM_BASE * 100 + g, device=device)
-            lab = (assign_device(coarse, X) if os.environ.get("QADC_B200_EXACT_ASSIGN") == "1"
-                   else assign_tensor_core(X, C, cn))
+        with _phase("generate"):
+            if cfg.sharding == "range":
+                X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + 4, centre_seed=CORPUS,
+                                          stream=datagen.STREAM_BASE * 100_000 + g, device=device)
+            else:
+                X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000, centre_seed=CORPUS,
+                                          stream=datagen.STREAM_BASE * 100 + g, device=device)
+        with _phase("assign"):
+            if cfg.sharding != "range" and os.environ.get("QADC_B200_EXACT_ASSIGN") == "1":
+                lab = assign_device(coarse, X)
+            else:
+                lab = assign_tensor_core(X, C, cn)
         labels[o:o + k] = lab
-        codes[o:o + k] = encode_device(pq, X - C[lab])
+        with _phase("encode"):
+            codes[o:o + k] = encode_device(pq, X - C[lab])
         ids[o:o + k] = torch.arange(a, b, dtype=torch.int64, device=device)
         o += k
         del X, lab
-    rows, rid, row_off = _sorted_rows(codes, labels, ids, C.shape[0])
+    with _phase("sort"):
+        rows, rid, row_off = _sorted_rows(codes, labels, ids, C.shape[0])
     del codes, labels, ids
     return rows, rid, row_off
 
@@ -302,7 +336,8 @@ def build_ivf_index(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, shard: 
     Returns the DeviceIndex, list sizes, and the row-ordered (codes, ids,
     row_off) it was built from."""
     rows, ids, row_off = ivf_rows(cfg, pq, coarse, n, device=device, chunk=chunk)
-    index = make_ivf_index(pq, coarse, rows, ids, row_off, device)
+    with _phase("index_create"):
+        index = make_ivf_index(pq, coarse, rows, ids, row_off, device)
     sizes = (row_off[1:] - row_off[:-1]).cpu().numpy()
     return index, sizes, rows, ids, row_off
 

@@ -18,6 +18,9 @@ Fixtures (all small):
   probe.npz        ivf.probe (K=300, d=128)
   find_qmax.npz    qadc.find_qmax (single cell, prefix, degenerate)
   search_*.npz     adc.search(method="qadc") end to end on seeded corpora
+  search_cfg2_k4096.npz  configs[2]'s K=4096 + OPQ model at N=1e5 (nprobe 16, 64)
+
+`python tests/golden/make_golden.py cfg2` regenerates only the last one.
 """
 
 from __future__ import annotations
@@ -48,8 +51,12 @@ def load_reference():
     return qadc
 
 
-def main():
+def main(only=None):
     load_reference()
+    sys.path.insert(0, str(REPO))
+    if only == "cfg2":
+        make_search_cfg2(HERE / "search_cfg2_k4096.npz", n=100_000, nq=16, mas=(16, 64))
+        return
     from qadc import adc, ivf, kernels, qadc as rq
     from qadc import pq as rpq
     from qadc.heap import NeighborHeap
@@ -185,6 +192,7 @@ def main():
                 Rs=(100,), init=1000, opq=False, K=0, mas=(1,))
     make_search(HERE / "search_ivf_opq.npz", datagen.SIFT_LIKE, m=32, n=20000, nq=30,
                 Rs=(100,), init=1000, opq=True, K=64, mas=(4, 16))
+    make_search_cfg2(HERE / "search_cfg2_k4096.npz", n=100_000, nq=16, mas=(16, 64))
     print("golden fixtures written to", HERE)
 
 
@@ -256,5 +264,53 @@ def make_search(path, mix, m, n, nq, Rs, init, opq, K, mas):
     np.savez_compressed(path, **out)
 
 
+def make_search_cfg2(path, n, nq, mas, R=100, init=1000):
+    """configs[2]'s model at reduced N: the committed K=4096 coarse
+    quantizer, OPQ rotation and residual codebooks (bench_data/), a seeded
+    mixture base assigned and encoded by the REFERENCE (kmeans.assign_batch,
+    pq.encode_batch, ivf._split_lists), and the reference's adc.search
+    (method="qadc") outputs at nprobe 16 and 64 plus its probe order and
+    (nprobe 16) fp32 tables."""
+    from qadc import adc, ivf, kmeans
+    from qadc import pq as rpq
+
+    from paper_1704_07355_b200 import datagen
+
+    bd = REPO / "bench_data"
+    coarse = np.load(bd / "cfg2_coarse_K4096.npy")
+    rot = np.load(bd / "cfg2_rotation.npy")
+    cbk = np.load(bd / "cfg2_m32_codebooks.npy")
+    K = coarse.shape[0]
+    pq = rpq.ProductQuantizer(m=cbk.shape[0], b=4, codebooks=cbk, rotation=rot)
+    base = datagen.mixture_numpy(datagen.SIFT_LIKE, n, seed=11, stream=datagen.STREAM_BASE)
+    queries = datagen.mixture_numpy(datagen.SIFT_LIKE, nq, seed=11, stream=datagen.STREAM_QUERY)
+    labels, _ = kmeans.assign_batch(coarse, base)
+    packed = rpq.encode_batch(pq, base - coarse[labels])
+    index = ivf.IvfIndex(d=pq.d, m=pq.m, b=pq.b, coarse=kmeans.Codebook(coarse),
+                         lists=ivf._split_lists(packed, labels, K, ivf.LAYOUT_TRANSPOSED),
+                         layout=ivf.LAYOUT_TRANSPOSED)
+    out = {"queries": queries, "labels": labels.astype(np.uint16), "codes": packed,
+           "init": np.int64(init)}
+    for ma in mas:
+        res_i = np.full((nq, R), -1, np.int64)
+        res_d = np.full((nq, R), np.inf, np.float32)
+        cells = np.zeros((nq, ma), np.int64)
+        for qi, q in enumerate(queries):
+            r = adc.search(index, pq, q, R=R, ma=ma, method="qadc", init=init)
+            res_i[qi, : r.ids.shape[0]] = r.ids
+            res_d[qi, : r.ids.shape[0]] = r.distances
+            ps = ivf.probe(index, q, ma)
+            cells[qi] = ps.cells
+            if ma == mas[0]:
+                if qi == 0:
+                    out["luts"] = np.zeros((nq, ma, pq.m, 16), np.float32)
+                for s_, rq_ in enumerate(ps.residual_queries):
+                    out["luts"][qi, s_] = adc.compute_tables(pq, adc._rotate(pq, rq_)).tables
+        out[f"ma{ma}_ids"] = res_i
+        out[f"ma{ma}_d"] = res_d
+        out[f"ma{ma}_cells"] = cells
+    np.savez_compressed(path, **out)
+
+
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1] if len(sys.argv) > 1 else None)

@@ -35,6 +35,8 @@ else:
     ma = 1
 torch.cuda.synchronize()
 print(f"model+index build {time.perf_counter() - t0:.1f} s", flush=True)
+from paper_1704_07355_b200.workload import BUILD_TIMES
+print("build phases (QADC_BUILD_TIMING=1):", {k: round(v, 2) for k, v in BUILD_TIMES.items()}, flush=True)
 qs = torch.from_numpy(queries(cfg, nq or cfg.q)).cuda()
 for _ in range(3):
     index.search(qs, cfg.R, ma=ma, init=cfg.init)
