@@ -1,23 +1,32 @@
 #!/usr/bin/env python
 """Quick ADC search benchmark on B200 (BASELINE.json metric: codes scanned/s
-and QPS, with the scan kernel's roofline fraction).
+and QPS at N=1e9, with the scan kernel's roofline fraction).
 
-Workload (N=1 GPU): BASELINE configs[1] — exhaustive Quick ADC, d=128
-mixture data, m=32 x 4-bit codes, N=10^7 codes, Q=1000 batched queries,
-R=100, init=1000. One step = one search_batch pass of all Q queries over
-the whole index (LUT, qmax, quantize, scan, exact top-R).
+Workload (default, N=1 GPU): BASELINE configs[4] — the metric's own
+configuration, which fits one B200 (16 GB of codes + 8 GB of ids): IVF
+K=65536 + OPQ, m=32 x 4-bit residual codes, N=10^9, Q=10^4 batched queries,
+nprobe=64, R=100, init=1000. One step = one search_batch pass of all Q
+queries (probe, residual + rotation + LUT, qmax, quantize, scan, exact
+top-R). `--config cfg0..cfg3` selects the other BASELINE configs.
 
-Multi-GPU (torchrun, one process per GPU, NCCL): weak scaling — every rank
-holds its own 10^7-code shard of one global list (ids rank*N + i) plus the
-replicated global prefix, scans it, and the per-rank top-R lists are merged
-(all_gather over NCCL, exact (distance, id) merge). value = all codes
-scanned by all ranks / max-over-ranks step time.
+Multi-GPU (torchrun, one process per GPU, NCCL): configs[4] is range-sharded
+(rank r holds its id range of every list, global list prefixes replicated;
+strong scaling over the fixed N=10^9), configs[2] list-sharded, the
+exhaustive configs range-sharded with a fixed N per GPU (weak scaling); the
+per-rank top-R lists are merged exactly (all_gather over NCCL, (distance,
+id) order). value = all codes scanned / max-over-ranks step time.
 
-`--impl reference` times the reference's own CPU implementation of the path
-on the host cores: the reference's compiled qadc_scan_u8 (oracle/_ref, built
-from /root/reference/pkg/src/qadc/src/scan_kernels.c) driven by the C
-restatement of adc.search's orchestration (oracle/), all host threads, on
-a bounded sample of queries over the same full index.
+Beside the device number the line carries: `e2e` (host queries in, host
+results out, through the public API), `roofline` (the scan kernel vs the
+measured integer-issue or int8-MMA peak, plus the HBM view), `cpu_baseline`
+(the reference's compiled qadc_scan_u8 driven by the restated adc.search
+orchestration on the host cores, on a query sample of the same index), and
+`parity` (the GPU's results and tables against the reference's semantics
+on that sample: ids / distance bits, fp32 LUT bits, uint8 flips, qmax).
+
+`--impl reference` times the reference's CPU path alone (rank 0): the same
+workload built with plain torch (no product library in that process), the
+same query sample scheme, all host threads.
 """
 
 from __future__ import annotations
@@ -44,7 +53,8 @@ METRICS = {
     "cfg3": "Quick ADC codes scanned/s (whole job) at configs[3]: exhaustive, d=960, m=32x4-bit, N=1e6, Q=1000, R=100",
     "cfg4": "Quick ADC codes scanned/s (whole job) at configs[4]: IVF K=65536 + OPQ, m=32x4-bit, N=1e9 range-sharded, Q=1e4, nprobe=64, R=100",
 }
-METRIC = METRICS["cfg1"]
+DEFAULT_CONFIG = "cfg4"
+METRIC = METRICS[DEFAULT_CONFIG]
 UNIT = "codes/s"
 
 
@@ -54,14 +64,20 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
+    p.add_argument("--config", default=DEFAULT_CONFIG,
+                   choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
     p.add_argument("--nprobe", type=int, default=None, help="IVF configs: probed cells (ma)")
     p.add_argument("--n", type=int, default=None,
                    help="codes per GPU (exhaustive) / in total (IVF); default: the config's N")
     p.add_argument("--queries", type=int, default=None)
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU work of the bounded reference sample")
+    p.add_argument("--parity-queries", type=int, default=200,
+                   help="IVF configs: queries of the native-mode parity accounting")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--replicate-tables", action="store_true",
+                   help="N>1: every rank prepares the whole batch (default: the Index + Tables "
+                        "phases are split by query and all-gathered, dist.sharded_prepare)")
     p.add_argument("--recall", type=int, default=0,
                    help="report R@1/10/100 on this many queries (exact GPU ground truth)")
     return p.parse_args()
@@ -135,10 +151,11 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "fallback": True}
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the scan kernel from the committed ncu
-    summary (profiles/), or None."""
-    f = ROOT / "profiles" / "scan_ncu_summary.json"
+def ncu_traffic(config):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum)
+    of this config's scan kernel from its own committed `ncu --set full`
+    summary (profiles/scan_ncu_<config>.json), or None."""
+    f = ROOT / "profiles" / f"scan_ncu_{config}.json"
     if f.exists():
         try:
             return json.loads(f.read_text()).get("dram_bytes_per_launch")
@@ -147,116 +164,150 @@ def ncu_traffic():
     return None
 
 
-def cpu_reference_run(cfg, codes_np, n, qs, R, init, seconds, nthreads=None):
-    """The reference's own compiled qadc_scan_u8 (oracle/_ref), driven by the
-    restated adc.search orchestration (oracle/), on a bounded query sample;
-    returns (codes/s, sample description, kind, cores, results)."""
-    from oracle import oracle as orc
-    from paper_1704_07355_b200.qadc import transpose_list
+def host_info():
+    """CPU model, thread count and the numpy / OpenBLAS build the CPU
+    baseline ran with (the reference's arithmetic depends on them)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        import ctypes
+        import glob
+        for f in glob.glob(os.path.join(os.path.dirname(np.__file__), "..", "numpy.libs",
+                                        "libscipy_openblas*.so")):
+            L = ctypes.CDLL(f)
+            fn = getattr(L, "scipy_openblas_get_config64_", None) or getattr(
+                L, "scipy_openblas_get_config", None)
+            if fn is not None:
+                fn.restype = ctypes.c_char_p
+                blas = fn().decode()
+    except Exception:
+        pass
+    return {"cpu_model": model, "threads": os.cpu_count(), "numpy": np.__version__,
+            "openblas": blas}
 
-    tl = transpose_list(codes_np, np.arange(n, dtype=np.int64))
-    flat = (tl.blocks.reshape(-1), np.array([0, tl.blocks.shape[0]], np.int64), tl.ids,
-            np.array([n], np.int64))
+
+def config_of(cfg, ivf_cfg, n, nq, ma, world):
+    """The workload's config dict, identical in both arms."""
+    c = {"workload": cfg.name, "m": cfg.m, "d": cfg.mix.d, "Q": nq, "R": cfg.R,
+         "init": cfg.init, "nprobe": ma}
+    if ivf_cfg is not None:
+        c.update({"K": ivf_cfg.K, "N_total": n,
+                  "sharding": ivf_cfg.sharding + (" (strong)" if world > 1 else "")})
+    else:
+        c.update({"N_per_gpu": n, "N_total": n * world,
+                  "sharding": "range (weak)" if world > 1 else "none"})
+    return c
+
+
+POOL = 512  # IVF configs: queries of the CPU sample (both arms) and its list extraction
+
+
+def _time_cpu(fn, seconds):
+    """Run fn() (one pass over the sample) until `seconds` of wall time
+    accumulated (at least once); returns (last result, wall per pass)."""
+    walls, out = [], None
+    t_end = time.perf_counter() + seconds
+    while True:
+        t0 = time.perf_counter()
+        out = fn()
+        walls.append(time.perf_counter() - t0)
+        if time.perf_counter() >= t_end:
+            break
+    return out, statistics.median(walls), len(walls)
+
+
+def cpu_reference_run(cb, flat, n, qs, R, init, seconds, nthreads=None):
+    """Exhaustive CPU baseline: the reference's compiled qadc_scan_u8
+    (oracle/_ref) driven by the restated adc.search orchestration (oracle/)
+    on all host threads, over the full index, on the largest query prefix
+    that fits `seconds` of CPU work."""
+    from oracle import oracle as orc
+
     use_ref = orc.ref_lib() is not None
-    kind = "reference" if use_ref else "port"
     nthreads = nthreads or os.cpu_count() or 1
-    cb = np.load(Path(__file__).resolve().parent / "bench_data" / cfg.codebooks_file)
-    # calibrate: one query per thread
     probe = qs[: max(1, min(nthreads, qs.shape[0]))]
     t0 = time.perf_counter()
     orc.search_batch(probe, cb, None, None, 1, flat, R, init, use_ref_scan=use_ref,
                      nthreads=nthreads)
-    t1 = time.perf_counter()
-    per_query_wall = (t1 - t0) / probe.shape[0]
-    nq = int(max(probe.shape[0], min(qs.shape[0], seconds / max(per_query_wall, 1e-6))))
+    per_q = (time.perf_counter() - t0) / probe.shape[0]
+    nq = int(max(probe.shape[0], min(qs.shape[0], seconds / max(per_q, 1e-6))))
     sample = qs[:nq]
     t0 = time.perf_counter()
     oi, od, on, _ = orc.search_batch(sample, cb, None, None, 1, flat, R, init,
                                      use_ref_scan=use_ref, nthreads=nthreads)
     wall = time.perf_counter() - t0
-    return (nq * n / wall, f"{nq} of {qs.shape[0]} queries over the full N={n} index",
-            kind, nthreads, (oi, od, on), wall)
+    return {"value": nq * n / wall, "unit": UNIT, "cores": nthreads,
+            "kind": "reference" if use_ref else "port",
+            "sample": f"{nq} of {qs.shape[0]} queries over the full N={n} index",
+            "seconds": round(wall, 2)}, (oi, od, on), nq
 
 
-def flat_lists(codes_np, ids_np, row_off):
-    """Reference-layout (blocks, blk_off, ids, count) of row-ordered lists."""
-    from paper_1704_07355_b200.qadc import transpose_list
-
-    blocks, ids, boff, count = [], [], [0], []
-    for L in range(row_off.shape[0] - 1):
-        a, b = int(row_off[L]), int(row_off[L + 1])
-        tl = transpose_list(codes_np[a:b], ids_np[a:b])
-        blocks.append(tl.blocks.reshape(-1))
-        ids.append(tl.ids)
-        boff.append(boff[-1] + tl.blocks.shape[0])
-        count.append(tl.count)
-    return (np.concatenate(blocks), np.asarray(boff, np.int64), np.concatenate(ids),
-            np.asarray(count, np.int64))
-
-
-def probed_sub_index(pq, coarse, rows, ids, row_off, qs, ma):
-    """Reference-layout lists (oracle input) holding only the lists the
-    given queries probe (every other list empty): the oracle's result and
-    work for these queries are those of the full index. Rows come from the
-    GPU index's row-ordered lists. Returns (flat, codes scanned)."""
-    import torch
-
-    from oracle import oracle as orc
-    from paper_1704_07355_b200.qadc import transpose_list
-
-    cells = np.stack([orc.probe(coarse, q, ma)[0] for q in qs])
-    want = np.zeros(row_off.shape[0] - 1, bool)
-    want[np.unique(cells)] = True
-    off = row_off.cpu().numpy()
-    sizes = np.diff(off)
-    sel = torch.from_numpy(np.nonzero(want)[0])
-    from paper_1704_07355_b200.shard import _ranges
-    idx = _ranges(row_off[:-1][sel.to(row_off.device)], row_off[1:][sel.to(row_off.device)]
-                  - row_off[:-1][sel.to(row_off.device)])
-    r_h, i_h = rows[idx].cpu().numpy(), ids[idx].cpu().numpy()
-    blocks, bids, boff, count = [], [], [0], []
-    o = 0
-    for L in range(want.shape[0]):
-        k = int(sizes[L]) if want[L] else 0
-        if k:
-            tl = transpose_list(r_h[o:o + k], i_h[o:o + k])
-            blocks.append(tl.blocks.reshape(-1))
-            bids.append(tl.ids)
-            boff.append(boff[-1] + tl.blocks.shape[0])
-            o += k
-        else:
-            boff.append(boff[-1])
-        count.append(k)
-    flat = (np.concatenate(blocks) if blocks else np.zeros(0, np.uint8), np.asarray(boff, np.int64),
-            np.concatenate(bids) if bids else np.zeros(0, np.int64), np.asarray(count, np.int64))
-    return flat, int(sizes[cells].sum())
-
-
-def cpu_reference_run_ivf(cfg, pq, coarse, rows, ids, row_off, qs, R, init, ma, seconds,
+def cpu_reference_run_ivf(pq, coarse, flat, sizes, pool, cells, R, init, ma, seconds, nq_total,
                           nthreads=None):
-    """IVF variant of cpu_reference_run: probe, OPQ rotation, tables, qmax
-    and quantization restated (oracle/), block scan = the reference's own
-    compiled qadc_scan_u8 (oracle/_ref), on a bounded query sample over the
-    lists those queries probe."""
+    """IVF CPU baseline: the restated adc.search orchestration (probe,
+    residual, OPQ rotation in OpenBLAS sgemv order, tables, qmax,
+    quantization; oracle/) with the reference's own compiled qadc_scan_u8
+    (oracle/_ref) as the block scan, all host threads, over the POOL
+    queries (their probed lists extracted from the full index), repeated
+    for about `seconds`. codes/s counts (query, probed list) codes."""
     from oracle import oracle as orc
 
     use_ref = orc.ref_lib() is not None
     nthreads = nthreads or os.cpu_count() or 1
-    probe = qs[: max(1, min(2 * nthreads, qs.shape[0]))]
-    flat, _ = probed_sub_index(pq, coarse, rows, ids, row_off, probe, ma)
-    t0 = time.perf_counter()
-    orc.search_batch(probe, pq.codebooks, pq.rotation, coarse, ma, flat, R, init,
-                     use_ref_scan=use_ref, nthreads=nthreads)
-    per_q = (time.perf_counter() - t0) / probe.shape[0]
-    nq = int(max(probe.shape[0], min(qs.shape[0], seconds / max(per_q, 1e-6))))
-    sample = qs[:nq]
-    flat, codes_scanned = probed_sub_index(pq, coarse, rows, ids, row_off, sample, ma)
-    t0 = time.perf_counter()
-    oi, od, on, _ = orc.search_batch(sample, pq.codebooks, pq.rotation, coarse, ma, flat, R, init,
-                                     use_ref_scan=use_ref, nthreads=nthreads)
-    wall = time.perf_counter() - t0
-    return (codes_scanned / wall, f"{nq} of {qs.shape[0]} queries, nprobe={ma}, over the lists "
-            "they probe", "reference" if use_ref else "port", nthreads, (oi, od, on), wall)
+    codes = int(sizes[np.asarray(cells)].sum())
+
+    def one():
+        return orc.search_batch(pool, pq.codebooks, pq.rotation, coarse, ma, flat, R, init,
+                                use_ref_scan=use_ref, nthreads=nthreads)
+    (oi, od, on, _), wall, reps = _time_cpu(one, seconds)
+    return {"value": codes / wall, "unit": UNIT, "cores": nthreads,
+            "kind": "reference" if use_ref else "port",
+            "sample": f"{pool.shape[0]} of {nq_total} queries, nprobe={ma}, over the lists they "
+                      f"probe of the full index ({reps} passes, median)",
+            "seconds": round(wall * reps, 2)}, (oi, od, on)
+
+
+def ivf_parity(index, pq, coarse, flat, pool, R, init, ma, gpu_i, gpu_d, cpu_res, nparity):
+    """Native-mode parity of the GPU against the reference on the pool:
+    (1) results vs the timed CPU reference run; (2) on the first
+    `nparity` queries, the GPU's tables vs the reference's Index + Tables
+    phases re-run with THIS host's numpy rotation (adc.py:108-111; counts
+    of fp32 LUT bit mismatches, uint8 flips, qmax mismatches, max LUT
+    relative error) and the results vs the oracle fed those tables; (3) a
+    reference-LUT-injected GPU run on the same queries (must be exact)."""
+    import torch
+
+    from oracle import oracle as orc
+    from oracle import parity
+
+    oi, od, _ = cpu_res
+    out = {"vs_cpu_reference": parity.compare_results(gpu_i[: oi.shape[0]], gpu_d[: oi.shape[0]],
+                                                      oi, od)}
+    k = min(nparity, pool.shape[0])
+    qk = pool[:k]
+    t = {a: b.cpu().numpy() for a, b in index.tables(torch.from_numpy(qk).cuda(), R, ma=ma,
+                                                     init=init).items()}
+    ref = parity.reference_tables(qk, pq.codebooks, pq.rotation, coarse, ma, flat, R, init)
+    acc = parity.account(t, ref)
+    ri, rd, _, _ = orc.search_batch(qk, pq.codebooks, pq.rotation, coarse, ma, flat, R, init,
+                                    lut_in=ref["lut"], cells_in=ref["cells"],
+                                    nthreads=os.cpu_count())
+    out["native_tables_vs_host_blas"] = {a: b for a, b in acc.items() if not a.startswith("_")}
+    out["native_results_vs_host_blas"] = parity.compare_results(gpu_i[:k], gpu_d[:k], ri, rd,
+                                                                acc["_diverged"])
+    inj = index.search(torch.from_numpy(qk).cuda(), R, ma=ma, init=init,
+                       lut=torch.from_numpy(ref["lut"]).cuda(),
+                       cells=torch.from_numpy(ref["cells"]).cuda())
+    out["lut_injected"] = parity.compare_results(inj.ids.cpu().numpy(),
+                                                 inj.distances.cpu().numpy(), ri, rd)
+    return out
 
 
 def measure_recall(cfg, pq, n, qs, ids, codes=None):
@@ -310,8 +361,11 @@ def run_b200(args):
     import torch.distributed as dist
 
     from paper_1704_07355_b200 import _native
-    from paper_1704_07355_b200.dist import merge_topr
-    from paper_1704_07355_b200.workload import CONFIGS, build_shard_index, load_pq, queries
+    from paper_1704_07355_b200.dist import merge_topr, sharded_prepare
+    from paper_1704_07355_b200.workload import (BUILD_TIMES, CONFIGS, IVF_CONFIGS,
+                                                build_ivf_index, build_shard_index,
+                                                build_sharded_ivf_index, load_ivf_model, load_pq,
+                                                queries)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -328,8 +382,6 @@ def run_b200(args):
         else:
             dist.init_process_group(backend)
     _native.require_device()
-    from paper_1704_07355_b200.workload import (IVF_CONFIGS, build_ivf_index,
-                                                build_sharded_ivf_index, load_ivf_model)
     ivf_cfg = IVF_CONFIGS.get(args.config)
     cfg = ivf_cfg or CONFIGS[args.config]
     n = args.n or cfg.n
@@ -355,8 +407,15 @@ def run_b200(args):
     q_pin = torch.from_numpy(qs).pin_memory()
     torch.cuda.synchronize()
 
+    shard_tables = world > 1 and not args.replicate_tables
+
+    def search(q):
+        if shard_tables:  # query-sharded Index + Tables phases, then the local scan
+            return index.scan(sharded_prepare(index, q, R, ma, init), R, ma=ma, init=init)
+        return index.search(q, R, ma=ma, init=init, with_fsat=(rank == 0))
+
     def step_device():
-        res = index.search(q_dev, R, ma=ma, init=init, with_fsat=(rank == 0))
+        res = search(q_dev)
         gi, gd, _ = merge_topr(res.ids, res.distances, R)
         return (gi, gd), res
 
@@ -378,18 +437,16 @@ def run_b200(args):
     # ---- device-resident timed region ----
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    scan_us, launches, codes_scanned, cands, reruns = [], 0, 0, 0, 0
+    st = {k: 0 for k in ("scan_us", "launches", "codes", "candidates", "reruns", "probe_us",
+                         "tables_us", "work_us", "select_us")}
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             (gi, gd), res = step_device()
-            scan_us.append(res.stats["scan_us"])
-            launches += res.stats["launches"]
-            codes_scanned += res.stats["codes"]
-            cands += res.stats["candidates"]
-            reruns += res.stats["reruns"]
+            for k in st:
+                st[k] += res.stats[k]
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -401,7 +458,7 @@ def run_b200(args):
 
     def step_e2e():
         qd = q_pin.to("cuda", non_blocking=True)
-        res = index.search(qd, R, ma=ma, init=init, with_fsat=(rank == 0))
+        res = search(qd)
         gi, gd, _ = merge_topr(res.ids, res.distances, R)
         out_i_pin.copy_(gi, non_blocking=True)
         out_d_pin.copy_(gd, non_blocking=True)
@@ -422,9 +479,8 @@ def run_b200(args):
     ms_e2e = max_over_ranks(e2.elapsed_time(e3) / args.steps)
 
     # codes scanned per step = sum over (query, probed list) of len(list),
-    # counted by the library on each rank's own codes (stats["codes"]),
-    # summed over ranks
-    per_rank_codes = codes_scanned / args.steps
+    # counted by the library on each rank's own codes, summed over ranks
+    per_rank_codes = st["codes"] / args.steps
     total_codes = per_rank_codes
     if world > 1:
         t = torch.tensor([per_rank_codes], dtype=torch.float64, device="cuda")
@@ -437,8 +493,8 @@ def run_b200(args):
     peak = np.zeros(2, np.float64)
     lib = _native.load_library()
     _native.check(lib.qadc_b200_int_peak(peak.ctypes.data_as(_native._f64p)), "int_peak")
-    scan_s = (sum(scan_us) / len(scan_us)) * 1e-6
-    pairs = codes_scanned / args.steps  # (query, code) pairs per launch, this rank
+    scan_s = st["scan_us"] / args.steps * 1e-6
+    pairs = per_rank_codes  # (query, code) pairs per launch, this rank
     lookups = pairs * pq.m
     pk = measured_peaks()
     # codes of every DISTINCT list touched once per batch
@@ -462,11 +518,14 @@ def run_b200(args):
     else:
         roof = {"bound": "int", "achieved": int_view["achieved_G_lookups"],
                 "peak": int_view["peak_G_lane_instr"],
-                "unit": "G lookup-adds/s vs measured G int lane-instr/s (PRMT+IMAD dual-pipe microbench)",
+                "unit": "G lookup-adds/s (m per scanned (query, code) pair) vs measured G int "
+                        "lane-instr/s (PRMT+IMAD dual-pipe microbench, qadc_b200_int_peak)",
                 "frac": int_view["frac"], "alu_pipe_peak_G": int_view["alu_pipe_peak_G"]}
     roof.update({
-        "traffic": ncu_traffic(),
+        "kernel": "k_scan_tc2" if res.stats.get("scan_tc") else "k_scan (PRMT)",
+        "traffic": ncu_traffic(args.config),
         "scan_kernel_ms": round(scan_s * 1e3, 3),
+        "algorithmic_units_per_launch": {"pairs": int(pairs), "lookups": int(lookups)},
         "hbm": {"bytes_alg_per_launch": int(hbm_bytes),
                 "achieved_gbs": round(hbm_bytes / scan_s / 1e9, 1),
                 "peak_gbs": pk.get("hbm_gbs"),
@@ -476,51 +535,64 @@ def run_b200(args):
 
     out = None
     if rank == 0:
+        ph = {k: round(st[k] / args.steps / 1e3, 3) for k in ("probe_us", "tables_us", "work_us",
+                                                             "scan_us", "select_us")}
         out = {
             "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev,
             "higher_is_better": True, "scaling": "weak" if ivf_cfg is None else "strong",
             "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (BASELINE mixture generator drawn on GPU; " + (
-                "reference-trained PQ)" if ivf_cfg is None or ivf_cfg.coarse_file else
-                "GPU-trained coarse K=%d + residual PQ, seeded; see DESIGN.md)" % ivf_cfg.K),
-            "config": {"workload": cfg.name,
-                       "N_per_gpu": n if ivf_cfg is None else index.ncodes,
-                       "N_total": n * world if ivf_cfg is None else n, "Q": nq,
-                       "R": R, "init": init, "m": pq.m, "d": pq.d, "nprobe": ma,
-                       "sharding": "range (weak)" if ivf_cfg is None else
-                       ivf_cfg.sharding + " (strong)",
-                       "codes_scanned_per_step": int(total_codes),
-                       "index_build_s": round(t_build, 1),
-                       "l2": "inputs larger than L2 (codes %.0f MB > 126 MB)" % (hbm_bytes / 1e6)
-                       if hbm_bytes > 126e6 else
-                       "index %.0f MB fits L2: steady-state (L2-warm) throughput" % (hbm_bytes / 1e6)},
+            "data": "synthetic (BASELINE mixture generator drawn on the GPU, seeded; " + (
+                "PQ codebooks trained by the reference's train_pq)" if ivf_cfg is None else
+                f"coarse K={ivf_cfg.K} by GPU Lloyd (tools/train_coarse.py), seeded orthogonal "
+                "OPQ rotation, residual PQ codebooks by the reference's train_pq; see DESIGN.md)"),
+            "config": config_of(cfg, ivf_cfg, n, nq, ma, world),
+            "tables_phase": ("query-sharded + all_gather" if shard_tables else
+                             ("replicated on every rank" if world > 1 else "local")),
             "qps": nq / (ms_dev * 1e-3),
             "e2e": {"value": e2e_value, "unit": UNIT, "qps": nq / (ms_e2e * 1e-3),
                     "ms_per_step": ms_e2e, "h2d_bytes_per_step": int(nq * pq.d * 4),
                     "d2h_bytes_per_step": int(nq * R * 12)},
             "roofline": roof,
+            "phases_ms": {"probe": ph["probe_us"], "tables": ph["tables_us"],
+                          "work_list": ph["work_us"], "scan": ph["scan_us"],
+                          "select": ph["select_us"]},
             "clocks": clk.summary(),
-            "gpu_launches": int(launches),
-            "candidates_per_query": cands / max(1, args.steps * nq),
-            "reruns": reruns,
+            "gpu_launches": int(st["launches"]),
+            "candidates_per_query": st["candidates"] / max(1, args.steps * nq),
+            "reruns": st["reruns"],
+            "workload_notes": {
+                "codes_scanned_per_step": int(total_codes),
+                "index_build_s": round(t_build, 1),
+                "index_build_phases_s": {k: round(v, 1) for k, v in BUILD_TIMES.items()},
+                "l2": "inputs larger than L2 (codes %.0f MB > 126 MB)" % (hbm_bytes / 1e6)
+                if hbm_bytes > 126e6 else
+                "index %.0f MB fits L2: steady-state (L2-warm) throughput" % (hbm_bytes / 1e6)},
         }
         if world == 1 and not args.no_cpu_baseline:
+            out["cpu_host"] = host_info()
             if ivf_cfg is not None:
-                v, sample, kind, cores, (oi, od, on), wall = cpu_reference_run_ivf(
-                    ivf_cfg, pq, coarse, rows, row_ids, row_off, qs, R, init, ma,
-                    args.cpu_seconds)
+                pool = qs[: min(POOL, nq)]
+                t = index.tables(torch.from_numpy(pool).cuda(), R, ma=ma, init=init)
+                cells = t["cells"].cpu().numpy()
+                flat, sizes = host_lists(rows, row_ids, row_off, cells)
+                cb_res, cpu_res = cpu_reference_run_ivf(pq, coarse, flat, sizes, pool, cells, R,
+                                                        init, ma, args.cpu_seconds, nq)
+                out["cpu_baseline"] = cb_res
+                out["parity"] = ivf_parity(index, pq, coarse, flat, pool, R, init, ma,
+                                           out_i.numpy(), out_d.numpy(), cpu_res,
+                                           args.parity_queries)
             else:
-                v, sample, kind, cores, (oi, od, on), wall = cpu_reference_run(
-                    cfg, codes.cpu().numpy(), n, qs, R, init, args.cpu_seconds)
-            k = oi.shape[0]
-            gi_np, gd_np = out_i.numpy()[:k], out_d.numpy()[:k]
-            exact = int(sum(np.array_equal(gi_np[i], oi[i]) and
-                            np.array_equal(gd_np[i].view(np.uint32), od[i].view(np.uint32))
-                            for i in range(k)))
-            out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-                                   "sample": sample, "seconds": round(wall, 2)}
-            out["parity_vs_cpu_reference"] = {"queries": k, "bit_exact": exact}
+                from paper_1704_07355_b200.qadc import transpose_list
+                tl = transpose_list(codes.cpu().numpy(), np.arange(n, dtype=np.int64))
+                flat = (tl.blocks.reshape(-1), np.array([0, tl.blocks.shape[0]], np.int64),
+                        tl.ids, np.array([n], np.int64))
+                cb_res, (oi, od, on), k = cpu_reference_run(pq.codebooks, flat, n, qs, R, init,
+                                                            args.cpu_seconds)
+                out["cpu_baseline"] = cb_res
+                from oracle import parity
+                out["parity"] = {"vs_cpu_reference": parity.compare_results(
+                    out_i.numpy()[:k], out_d.numpy()[:k], oi, od)}
     if out is not None and args.recall and world == 1:
         out["recall"] = measure_recall(cfg, pq, n, qs[: args.recall], out_i.numpy()[: args.recall],
                                        codes=None if ivf_cfg is not None else codes)
@@ -530,59 +602,102 @@ def run_b200(args):
 
 
 def run_reference(args):
-    """CPU reference arm (see module docstring)."""
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    """CPU reference arm: the reference's compiled qadc_scan_u8 (oracle/_ref)
+    driven by the restated adc.search orchestration (oracle/), all host
+    threads, on a bounded query sample per step. The index is built in
+    plain torch on the GPU (workload.ivf_rows_torch / encode_torch): no
+    product kernel runs, and libqadc_b200.so is never loaded, in this
+    process. Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return None
-    from paper_1704_07355_b200.workload import (CONFIGS, IVF_CONFIGS, build_ivf_index, load_ivf_model,
-                                                load_pq, queries)
+    import torch
+
+    from paper_1704_07355_b200.workload import (CONFIGS, IVF_CONFIGS, encode_torch,
+                                                ivf_rows_torch, load_ivf_model, load_pq, queries)
 
     ivf_cfg = IVF_CONFIGS.get(args.config)
     cfg = ivf_cfg or CONFIGS[args.config]
     n = args.n or cfg.n
     nq = args.queries or cfg.q
     ma = (args.nprobe or ivf_cfg.nprobe) if ivf_cfg is not None else 1
-    # index construction is setup, not the timed path: encode on the GPU if
-    # one is visible (same index the B200 arm scans), else fail loudly
-    import torch
-
-    from paper_1704_07355_b200.workload import shard_codes
     if not torch.cuda.is_available():
-        return {"impl": "reference", "unavailable": "index setup needs the GPU encoder"}
+        return {"impl": "reference", "unavailable": "the index setup draws the base on the GPU"}
+    from oracle import oracle as orc
     qs = queries(cfg, nq)
+    nthreads = os.cpu_count() or 1
+    use_ref = orc.ref_lib() is not None
+    t_build = time.perf_counter()
     if ivf_cfg is not None:
         pq, coarse = load_ivf_model(ivf_cfg)
-        _, _, rows, row_ids, row_off = build_ivf_index(ivf_cfg, pq, coarse, n)
+        pool = qs[: min(POOL, nq)]
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(nthreads) as ex:
+            cells = np.stack(list(ex.map(lambda q: orc.probe(coarse, q, ma)[0], pool)))
+        keep = np.zeros(ivf_cfg.K, bool)
+        keep[np.unique(cells)] = True
+        rows, row_ids, row_off = ivf_rows_torch(ivf_cfg, pq, coarse, n, keep)
+        flat, sizes = host_lists(rows, row_ids, row_off, cells)
+        del rows, row_ids
+        codes = int(sizes[cells].sum())
+        desc = (f"{pool.shape[0]} of {nq} queries, nprobe={ma}, over the lists they probe of "
+                f"the full N={n} index (built in plain torch)")
 
-        def one(seconds):
-            return cpu_reference_run_ivf(ivf_cfg, pq, coarse, rows, row_ids, row_off, qs, cfg.R,
-                                         cfg.init, ma, seconds)
+        def one():
+            t0 = time.perf_counter()
+            orc.search_batch(pool, pq.codebooks, pq.rotation, coarse, ma, flat, cfg.R, cfg.init,
+                             use_ref_scan=use_ref, nthreads=nthreads)
+            return codes / (time.perf_counter() - t0), time.perf_counter() - t0
     else:
         pq = load_pq(cfg)
-        codes_np = shard_codes(cfg, pq, n, 0).cpu().numpy()
+        from paper_1704_07355_b200 import datagen
+        from paper_1704_07355_b200.qadc import transpose_list
+        from paper_1704_07355_b200.workload import CORPUS, SEED
+        parts = []
+        for c0 in range(0, n, 4 * datagen.CHUNK):
+            k = min(4 * datagen.CHUNK, n - c0)
+            X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000, centre_seed=CORPUS,
+                                      stream=datagen.STREAM_BASE * 100 + c0 // (4 * datagen.CHUNK))
+            parts.append(encode_torch(pq, X).cpu().numpy())
+        tl = transpose_list(np.concatenate(parts), np.arange(n, dtype=np.int64))
+        flat = (tl.blocks.reshape(-1), np.array([0, tl.blocks.shape[0]], np.int64), tl.ids,
+                np.array([n], np.int64))
+        probe = qs[: max(1, min(nthreads, nq))]
+        t0 = time.perf_counter()
+        orc.search_batch(probe, pq.codebooks, None, None, 1, flat, cfg.R, cfg.init,
+                         use_ref_scan=use_ref, nthreads=nthreads)
+        per_q = (time.perf_counter() - t0) / probe.shape[0]
+        per_step = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+        k = int(max(probe.shape[0], min(nq, per_step / max(per_q, 1e-6))))
+        sample = qs[:k]
+        desc = f"{k} of {nq} queries over the full N={n} index (encoded in plain torch)"
 
-        def one(seconds):
-            return cpu_reference_run(cfg, codes_np, n, qs, cfg.R, cfg.init, seconds)
+        def one():
+            t0 = time.perf_counter()
+            orc.search_batch(sample, pq.codebooks, None, None, 1, flat, cfg.R, cfg.init,
+                             use_ref_scan=use_ref, nthreads=nthreads)
+            return k * n / (time.perf_counter() - t0), time.perf_counter() - t0
+    t_build = time.perf_counter() - t_build
     vals, walls = [], []
-    desc = kind = cores = None
-    per_step = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
     for i in range(args.warmup + args.steps):
-        v, desc, kind, cores, _, wall = one(per_step)
+        v, w = one()
         if i >= args.warmup:
             vals.append(v)
-            walls.append(wall)
+            walls.append(w)
     value = statistics.median(vals)
     return {
         "impl": "reference", "metric": METRICS[args.config], "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(walls) * 1e3, "higher_is_better": True,
         "scaling": "weak" if ivf_cfg is None else "strong", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (BASELINE mixture generator; same index as the B200 arm)",
-        "config": {"workload": cfg.name, "N_per_gpu": n, "Q": nq, "R": cfg.R, "init": cfg.init,
-                   "nprobe": ma},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": desc},
+        "data": "synthetic (BASELINE mixture generator, same seeds and model files as the B200 "
+                "arm; index built in plain torch)",
+        "config": config_of(cfg, ivf_cfg, n, nq, ma, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads,
+                         "kind": "reference" if use_ref else "port", "sample": desc},
+        "cpu_host": host_info(),
+        "index_setup_s": round(t_build, 1),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

@@ -173,6 +173,41 @@ QADC_API int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries,
                            int64_t *out_ids, float *out_d, int32_t *out_n,
                            void *stream, int64_t *stats);
 
+/*
+ * search_batch in two halves, for callers that move the per-query state
+ * between them (the query-sharded Tables phase of a multi-GPU search:
+ * every rank prepares a slice of the batch, the slices are all-gathered,
+ * then every rank scans its own codes for the whole batch). Device
+ * pointers only; npairs = nq * (ma for IVF, 1 for a flat index).
+ *
+ * prepare = the Index + Tables phases (adc.py:140-174): cells (npairs)
+ * int64 probe order (IVF; ignored for a flat index), qt (npairs * m * 4)
+ * uint32 words of the uint8 tables (entries 4w..4w+3 of sub-quantizer
+ * w / 4), qmin_f / delta_f (npairs) fp32, depth (npairs) uint8 byte-sum
+ * depth, qmax (nq) fp32, M_bits (nq) uint32 initial distance bound
+ * (float bits), fsat_n (nq) int32 / fsat_mid (nq * R) fp32 / fsat_id
+ * (nq * R) int64 the saturated first-R lanes (QADC_B200_NO_FSAT: none).
+ * With QADC_B200_LUT_IN, lut_in / cells_in replace the probe and LUT.
+ *
+ * scan = work list, scan, exact top-R over those arrays (M_bits is
+ * tightened in place); outputs as search_batch. stats as search_batch
+ * (each call fills the phases it ran).
+ */
+QADC_API int qadc_b200_search_prepare(qadc_b200_index *idx, const float *queries, int nq,
+                                      int R, int ma, int init, unsigned flags,
+                                      const float *lut_in, const int64_t *cells_in,
+                                      int64_t *cells, uint32_t *qt, float *qmin_f,
+                                      float *delta_f, uint8_t *depth, float *qmax,
+                                      uint32_t *M_bits, int32_t *fsat_n, float *fsat_mid,
+                                      int64_t *fsat_id, void *stream, int64_t *stats);
+QADC_API int qadc_b200_search_scan(qadc_b200_index *idx, int nq, int R, int ma, int init,
+                                   unsigned flags, const int64_t *cells, const uint32_t *qt,
+                                   const float *qmin_f, const float *delta_f,
+                                   const uint8_t *depth, uint32_t *M_bits,
+                                   const int32_t *fsat_n, const float *fsat_mid,
+                                   const int64_t *fsat_id, int64_t *out_ids, float *out_d,
+                                   int32_t *out_n, void *stream, int64_t *stats);
+
 /* ---- device-pointer building blocks (parity tests, diagnostics) ---- */
 
 /* The Index + Tables phases of search_batch (adc.py:140-174) with their

@@ -64,6 +64,13 @@ def _bind(lib):
     lib.qadc_b200_search_batch.argtypes = [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_uint,
                                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                            c_void_p, _i64p]
+    lib.qadc_b200_search_prepare.restype = c_int
+    lib.qadc_b200_search_prepare.argtypes = [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_uint,
+                                             c_void_p, c_void_p] + [c_void_p] * 10 + [c_void_p,
+                                                                                      _i64p]
+    lib.qadc_b200_search_scan.restype = c_int
+    lib.qadc_b200_search_scan.argtypes = [c_void_p, c_int, c_int, c_int, c_int, c_uint] + [
+        c_void_p] * 12 + [c_void_p, _i64p]
     lib.qadc_b200_search_tables.restype = c_int
     lib.qadc_b200_search_tables.argtypes = [c_void_p, c_void_p, c_int, c_int, c_int, c_int,
                                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

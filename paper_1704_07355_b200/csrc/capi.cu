@@ -54,23 +54,6 @@ __global__ void k_init_bounds(unsigned *M_bits, const unsigned *M_override, floa
   }
 }
 
-__global__ void k_gather_rows_f(const float *__restrict__ src, const int *__restrict__ rows, int n,
-                                int width, float *__restrict__ dst) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * width;
-       t += (int64_t)gridDim.x * blockDim.x)
-    dst[t] = src[(size_t)rows[t / width] * width + t % width];
-}
-__global__ void k_gather_rows_i(const int64_t *__restrict__ src, const int *__restrict__ rows, int n,
-                                int width, int64_t *__restrict__ dst) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * width;
-       t += (int64_t)gridDim.x * blockDim.x)
-    dst[t] = src[(size_t)rows[t / width] * width + t % width];
-}
-__global__ void k_gather_u(const unsigned *__restrict__ src, const int *__restrict__ rows, int n,
-                           unsigned *__restrict__ dst) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-    dst[t] = src[rows[t]];
-}
 __global__ void k_scatter_out(const int64_t *__restrict__ ids, const float *__restrict__ d,
                               const int32_t *__restrict__ n, const int *__restrict__ rows, int cnt,
                               int R, int64_t *__restrict__ out_ids, float *__restrict__ out_d,
@@ -137,7 +120,7 @@ struct SearchStats {
 };
 
 // Phase events of search_impl, created once per host thread.
-enum { kEvStart, kEvProbe, kEvTables, kEvScan0, kEvScan1, kEvSelect, kEvCount };
+enum { kEvStart, kEvProbe, kEvTables, kEvWork0, kEvScan0, kEvScan1, kEvSelect, kEvCount };
 cudaEvent_t *phase_events() {
   static thread_local cudaEvent_t ev[kEvCount];
   static thread_local int dev_made = -1;
@@ -179,14 +162,94 @@ void index_probe(const qadc_b200_index *idx, const float *queries, int nq, int m
   if (!done) launch_probe(idx->coarseT, idx->K, idx->d, queries, nq, ma, cells, st);
 }
 
-int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int ma, int init,
-                const float *lut_in, const int64_t *cells_in, int64_t *out_ids, float *out_d,
-                int32_t *out_n, cudaStream_t st, SearchStats &ss, const unsigned *M_override,
-                int cap_g, int depth, bool no_fsat, bool prmt, bool force_tc, bool one_sm) {
+// Per-query scan inputs produced by the Index + Tables phases
+// (adc.py:140-174 for every query of the batch), device arrays.
+struct Prep {
+  const int64_t *cells = nullptr;   // [npairs] probe order (IVF) or null (flat)
+  const uint32_t *qt = nullptr;     // [npairs][m][4] uint8 tables as words
+  const float *qmin_f = nullptr;    // [npairs] fp32 casts the scan uses
+  const float *delta_f = nullptr;   // [npairs]
+  const uint8_t *depth = nullptr;   // [npairs] byte-sum depth of the pair's tables
+  unsigned *M_bits = nullptr;       // [nq] running distance bound (the scan tightens it)
+  const int *fsat_n = nullptr;      // [nq] saturated first-R lanes (F_sat)
+  const float *fsat_mid = nullptr;  // [nq][R]
+  const int64_t *fsat_id = nullptr; // [nq][R]
+};
+
+template <class T>
+__global__ void k_gather(const T *__restrict__ src, const int *__restrict__ rows, int n, int width,
+                         T *__restrict__ dst) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)n * width;
+       t += (int64_t)gridDim.x * blockDim.x)
+    dst[t] = src[(size_t)rows[t / width] * width + t % width];
+}
+
+// Index + Tables phases: probe (IVF, unless cells_in), residual + rotation +
+// float LUT (unless lut_in), qmax from the first probed cell, per-pair qmin /
+// delta and uint8 tables (+ byte-sum depth), prefix facts (F_sat, initial
+// bound). Outputs are caller-owned device arrays; cells_out may alias
+// nothing (flat) and receives the probe order otherwise.
+int prepare_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int ma, int init,
+                 const float *lut_in, const int64_t *cells_in, bool no_fsat, cudaStream_t st,
+                 SearchStats &ss, int64_t *cells_out, uint32_t *qt, float *qmin_f, float *delta_f,
+                 uint8_t *depth, float *qmax, unsigned *M_bits, int *fsat_n, float *fsat_mid,
+                 int64_t *fsat_id) {
   if (nq == 0) return kOk;
   const int m = idx->m;
   const int nslots = idx->K ? ma : 1;
   const int64_t npairs = (int64_t)nq * nslots;
+  cudaEvent_t *ev = phase_events();
+  cudaEventRecord(ev[kEvStart], st);
+  const int64_t *cells = nullptr;
+  if (idx->K) {
+    if (cells_in) {
+      if (cells_out && cells_out != cells_in)
+        QADC_CUDA(cudaMemcpyAsync(cells_out, cells_in, npairs * 8, cudaMemcpyDeviceToDevice, st));
+      cells = cells_in;
+    } else {
+      index_probe(idx, queries, nq, ma, cells_out, st);
+      QADC_CUDA(cudaGetLastError());
+      ss.launches++;
+      cells = cells_out;
+    }
+  }
+  cudaEventRecord(ev[kEvProbe], st);
+  DevBuf<float> lut_b;
+  const float *lut = lut_in;
+  if (!lut) {
+    if (lut_b.alloc(npairs * m * 16, st)) return cuda_fail(cudaGetLastError(), "alloc lut");
+    launch_residual_lut(idx, queries, cells, nq, nslots, lut_b.p, st);
+    QADC_CUDA(cudaGetLastError());
+    ss.launches++;
+    lut = lut_b.p;
+  }
+  // tuning knob (default = measured best): byte-sum depth cap
+  static const int max_depth = std::min(16, std::max(2, scan_env_int("QADC_B200_MAX_DEPTH", 16)));
+  if (int rc = launch_qmax(idx, lut, cells, nq, nslots, R, init, qmax, st)) return rc;
+  launch_quantize(lut, (int)npairs, m, qmax, nslots, nullptr, nullptr, qt, qmin_f, delta_f,
+                  nullptr, nullptr, st, max_depth, depth);
+  launch_prefix(idx, qt, qmin_f, delta_f, cells, nq, nslots, R, init, M_bits, fsat_n, fsat_mid,
+                fsat_id, st);
+  QADC_CUDA(cudaGetLastError());
+  ss.launches += 3;
+  if (no_fsat) QADC_CUDA(cudaMemsetAsync(fsat_n, 0, sizeof(int) * nq, st));
+  cudaEventRecord(ev[kEvTables], st);
+  return kOk;
+}
+
+// Work list, scan, exact top-R (and the rare overflow passes) over prepared
+// per-query inputs. p.M_bits is tightened in place. level > 0: a rerun pass
+// over a subset with a larger candidate capacity (no phase timing).
+int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int init,
+              int64_t *out_ids, float *out_d, int32_t *out_n, cudaStream_t st, SearchStats &ss,
+              int cap_g, int level, bool prmt, bool force_tc, bool one_sm) {
+  if (nq == 0) return kOk;
+  const int m = idx->m;
+  const int nslots = idx->K ? ma : 1;
+  const int64_t npairs = (int64_t)nq * nslots;
+  const int64_t *cells = idx->K ? p.cells : nullptr;
+  cudaEvent_t *ev = phase_events();
+  if (level == 0) cudaEventRecord(ev[kEvWork0], st);
   // The tensor-core scan amortises each code's one-hot expansion over the
   // queries probing its list: with few (query, list) pairs per list (IVF
   // at small nprobe / large K) the PRMT kernel is faster (measured: cfg2
@@ -196,68 +259,29 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   const int qt_tile = scan_tile_queries(m, prmt);
   const int nl = idx->nlists;
 
-  DevBuf<int64_t> cells_b;
-  DevBuf<float> lut_b, qmax_b, qmin_f, delta_f, fsat_mid, cand_mid, hist_w;
-  DevBuf<uint32_t> qt_b;
-  DevBuf<unsigned> M_bits, cand_n, hist;
-  DevBuf<int> fsat_n, n_items, counter, scratch, overflow;
+  DevBuf<float> cand_mid, hist_w;
+  DevBuf<unsigned> cand_n, hist;
+  DevBuf<int> n_items, counter, scratch, overflow;
   DevBuf<unsigned long long> ncodes;
-  DevBuf<int64_t> fsat_id, cand_id;
+  DevBuf<int64_t> cand_id;
   DevBuf<int32_t> pair_q, pair_t;
   DevBuf<WorkItem> items, items_ord;
-  DevBuf<uint8_t> pair_depth;
   DevBuf<unsigned> cls;
   int rc = 0;
-
-  cudaEvent_t *ev = phase_events();
-  if (depth == 0) cudaEventRecord(ev[kEvStart], st);
-  const int64_t *cells = nullptr;
-  if (idx->K) {
-    if (cells_in) {
-      cells = cells_in;
-    } else {
-      if ((rc = cells_b.alloc(npairs, st))) return cuda_fail(cudaGetLastError(), "alloc cells");
-      index_probe(idx, queries, nq, ma, cells_b.p, st);
-      QADC_CUDA(cudaGetLastError());
-      ss.launches++;
-      cells = cells_b.p;
-    }
-  }
-  if (depth == 0) cudaEventRecord(ev[kEvProbe], st);
-  const float *lut = lut_in;
-  if (!lut) {
-    if (lut_b.alloc(npairs * m * 16, st)) return cuda_fail(cudaGetLastError(), "alloc lut");
-    launch_residual_lut(idx, queries, cells, nq, nslots, lut_b.p, st);
-    QADC_CUDA(cudaGetLastError());
-    ss.launches++;
-    lut = lut_b.p;
-  }
-  if (qmax_b.alloc(nq, st) || qt_b.alloc(npairs * m * 4, st) || qmin_f.alloc(npairs, st) ||
-      delta_f.alloc(npairs, st) || M_bits.alloc(nq, st) || fsat_n.alloc(nq, st) ||
-      fsat_mid.alloc((int64_t)nq * R, st) || fsat_id.alloc((int64_t)nq * R, st) ||
-      hist.alloc((int64_t)nq * kHistWords, st) || hist_w.alloc(nq, st) || cand_n.alloc(nq, st) ||
+  if (hist.alloc((int64_t)nq * kHistWords, st) || hist_w.alloc(nq, st) || cand_n.alloc(nq, st) ||
       cand_mid.alloc((int64_t)nq * cap_g, st) || cand_id.alloc((int64_t)nq * cap_g, st) ||
       pair_q.alloc(npairs, st) || pair_t.alloc(npairs, st) || n_items.alloc(1, st) ||
-      counter.alloc(1, st) || scratch.alloc(build_work_scratch(nl, nslots), st) || overflow.alloc(nq, st) ||
-      ncodes.alloc(1, st) || pair_depth.alloc(npairs, st))
+      counter.alloc(1, st) || scratch.alloc(build_work_scratch(nl, nslots), st) ||
+      overflow.alloc(nq, st) || ncodes.alloc(1, st))
     return cuda_fail(cudaGetLastError(), "alloc workspace");
-  // tuning knobs (defaults are the measured best): byte-sum depth cap and
-  // the half-tile loop for tiles with <= QT/2 queries
-  static const int max_depth = std::min(16, std::max(2, scan_env_int("QADC_B200_MAX_DEPTH", 16)));
+  // tuning knobs (defaults are the measured best): the half-tile loop for
+  // tiles with <= QT/2 queries, item ordering, per-variant item counts
   static const int no_half = scan_env_int("QADC_B200_NO_HALF", 0);
   static const int variant_stats = scan_env_int("QADC_B200_VARIANT_STATS", 0);
   static const int no_order = scan_env_int("QADC_B200_NO_ORDER", 0);
-
-  if ((rc = launch_qmax(idx, lut, cells, nq, nslots, R, init, qmax_b.p, st))) return rc;
-  launch_quantize(lut, (int)npairs, m, qmax_b.p, nslots, nullptr, nullptr, qt_b.p, qmin_f.p,
-                  delta_f.p, nullptr, nullptr, st, max_depth, pair_depth.p);
-  launch_prefix(idx, qt_b.p, qmin_f.p, delta_f.p, cells, nq, nslots, R, init, M_bits.p, fsat_n.p,
-                fsat_mid.p, fsat_id.p, st);
-  k_init_bounds<<<gridn(nq), 256, 0, st>>>(M_bits.p, M_override, hist_w.p, nq);
+  k_init_bounds<<<gridn(nq), 256, 0, st>>>(p.M_bits, nullptr, hist_w.p, nq);
   QADC_CUDA(cudaGetLastError());
-  ss.launches += 4;
-  if (no_fsat) cudaMemsetAsync(fsat_n.p, 0, sizeof(int) * nq, st);
-  if (depth == 0) cudaEventRecord(ev[kEvTables], st);
+  ss.launches++;
 
   // ---- work list ----
   const int nsm = device_sms();
@@ -318,7 +342,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
              scratch.p, max_items, st);
   if (items_ord.alloc(max_items, st) || cls.alloc(order_items_scratch(max_items), st))
     return cuda_fail(cudaGetLastError(), "alloc items");
-  order_items(items.p, n_items.p, max_items, pair_t.p, pair_depth.p, no_half ? 0 : qt_tile / 2,
+  order_items(items.p, n_items.p, max_items, pair_t.p, p.depth, no_half ? 0 : qt_tile / 2,
               nslots, cls.p, items_ord.p, st);
   ss.launches += 8;
 
@@ -337,10 +361,10 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   a.item_counter = counter.p;
   a.pair_q = pair_q.p;
   a.pair_t = pair_t.p;
-  a.qt = qt_b.p;
-  a.qmin_f = qmin_f.p;
-  a.delta_f = delta_f.p;
-  a.M_bits = M_bits.p;
+  a.qt = p.qt;
+  a.qmin_f = p.qmin_f;
+  a.delta_f = p.delta_f;
+  a.M_bits = p.M_bits;
   a.cand_n = cand_n.p;
   a.cand_mid = cand_mid.p;
   a.cand_id = cand_id.p;
@@ -368,8 +392,8 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   cudaEventRecord(e1, st);
   ss.scan_launches++;
   ss.launches++;
-  launch_select(nq, R, M_bits.p, cand_n.p, cand_mid.p, cand_id.p, cap_g, fsat_n.p, fsat_mid.p,
-                fsat_id.p, out_ids, out_d, out_n, overflow.p, st);
+  launch_select(nq, R, p.M_bits, cand_n.p, cand_mid.p, cand_id.p, cap_g, p.fsat_n, p.fsat_mid,
+                p.fsat_id, out_ids, out_d, out_n, overflow.p, st);
   ss.launches++;
   QADC_CUDA(cudaGetLastError());
   cudaEventRecord(ev[kEvSelect], st);
@@ -382,7 +406,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   unsigned long long h_codes = 0;
   QADC_CUDA(cudaMemcpyAsync(&h_codes, ncodes.p, sizeof(h_codes), cudaMemcpyDeviceToHost, st));
   QADC_CUDA(cudaStreamSynchronize(st));
-  if (depth == 0) ss.codes += (int64_t)h_codes;
+  if (level == 0) ss.codes += (int64_t)h_codes;
   if (variant_stats) {
     unsigned v[8];
     cudaMemcpy(v, cls.p, sizeof(v), cudaMemcpyDeviceToHost);
@@ -392,13 +416,9 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   ss.scan_us += ms * 1e3;
-  if (depth == 0) {
+  if (level == 0) {
     float t = 0.f;
-    cudaEventElapsedTime(&t, ev[kEvStart], ev[kEvProbe]);
-    ss.probe_us += t * 1e3;
-    cudaEventElapsedTime(&t, ev[kEvProbe], ev[kEvTables]);
-    ss.tables_us += t * 1e3;
-    cudaEventElapsedTime(&t, ev[kEvTables], e0);
+    cudaEventElapsedTime(&t, ev[kEvWork0], e0);
     ss.work_us += t * 1e3;
     cudaEventElapsedTime(&t, e1, ev[kEvSelect]);
     ss.select_us += t * 1e3;
@@ -416,51 +436,136 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
     }
   }
   for (int q : big) {
-    if ((rc = select_large(q, R, M_bits.p, cand_n.p, cand_mid.p, cand_id.p, cap_g, fsat_n.p,
-                           fsat_mid.p, fsat_id.p, out_ids, out_d, out_n, st)))
+    if ((rc = select_large(q, R, p.M_bits, cand_n.p, cand_mid.p, cand_id.p, cap_g, p.fsat_n,
+                           p.fsat_mid, p.fsat_id, out_ids, out_d, out_n, st)))
       return rc;
     ss.launches += 4;
   }
   if (!rerun.empty()) {
-    if (depth > 4) return arg_error("candidate capacity could not be satisfied");
+    // the dropped candidates are re-found by scanning the overflowed
+    // queries again with their final (tight) bound and a larger capacity;
+    // their prepared tables are gathered, not recomputed
+    if (level > 4) return arg_error("candidate capacity could not be satisfied");
     ss.reruns += (int64_t)rerun.size();
     const int nr = (int)rerun.size();
-    DevBuf<int> rows;
-    DevBuf<float> sub_q, sub_lut, sub_d;
-    DevBuf<int64_t> sub_cells, sub_ids;
+    const int64_t w = (int64_t)nslots;
+    DevBuf<int> rows, sub_fn;
+    DevBuf<uint32_t> sub_qt;
+    DevBuf<float> sub_qmin, sub_delta, sub_fm, sub_d;
+    DevBuf<uint8_t> sub_depth;
     DevBuf<unsigned> sub_M;
+    DevBuf<int64_t> sub_cells, sub_fi, sub_ids;
     DevBuf<int32_t> sub_n;
-    if (rows.alloc(nr, st) || sub_q.alloc((int64_t)nr * idx->d, st) || sub_M.alloc(nr, st) ||
-        sub_ids.alloc((int64_t)nr * R, st) || sub_d.alloc((int64_t)nr * R, st) ||
-        sub_n.alloc(nr, st))
+    if (rows.alloc(nr, st) || sub_qt.alloc(nr * w * m * 4, st) || sub_qmin.alloc(nr * w, st) ||
+        sub_delta.alloc(nr * w, st) || sub_depth.alloc(nr * w, st) || sub_M.alloc(nr, st) ||
+        sub_fn.alloc(nr, st) || sub_fm.alloc((int64_t)nr * R, st) ||
+        sub_fi.alloc((int64_t)nr * R, st) || sub_ids.alloc((int64_t)nr * R, st) ||
+        sub_d.alloc((int64_t)nr * R, st) || sub_n.alloc(nr, st) ||
+        (cells && sub_cells.alloc(nr * w, st)))
       return cuda_fail(cudaGetLastError(), "alloc rerun");
     QADC_CUDA(cudaMemcpyAsync(rows.p, rerun.data(), sizeof(int) * nr, cudaMemcpyHostToDevice, st));
-    k_gather_rows_f<<<gridn((int64_t)nr * idx->d), 256, 0, st>>>(queries, rows.p, nr, idx->d, sub_q.p);
-    k_gather_u<<<gridn(nr), 256, 0, st>>>(M_bits.p, rows.p, nr, sub_M.p);
-    const float *lp = nullptr;
-    const int64_t *cp = nullptr;
-    if (lut_in) {
-      if (sub_lut.alloc((int64_t)nr * nslots * m * 16, st)) return kErrCuda;
-      k_gather_rows_f<<<gridn((int64_t)nr * nslots * m * 16), 256, 0, st>>>(lut_in, rows.p, nr,
-                                                                          nslots * m * 16, sub_lut.p);
-      lp = sub_lut.p;
-    }
-    if (cells) {
-      if (sub_cells.alloc((int64_t)nr * nslots, st)) return kErrCuda;
-      k_gather_rows_i<<<gridn((int64_t)nr * nslots), 256, 0, st>>>(cells, rows.p, nr, nslots,
-                                                                   sub_cells.p);
-      cp = sub_cells.p;
-    }
+    k_gather<uint32_t><<<gridn(nr * w * m * 4), 256, 0, st>>>(p.qt, rows.p, nr, (int)(w * m * 4), sub_qt.p);
+    k_gather<float><<<gridn(nr * w), 256, 0, st>>>(p.qmin_f, rows.p, nr, (int)w, sub_qmin.p);
+    k_gather<float><<<gridn(nr * w), 256, 0, st>>>(p.delta_f, rows.p, nr, (int)w, sub_delta.p);
+    k_gather<uint8_t><<<gridn(nr * w), 256, 0, st>>>(p.depth, rows.p, nr, (int)w, sub_depth.p);
+    k_gather<unsigned><<<gridn(nr), 256, 0, st>>>(p.M_bits, rows.p, nr, 1, sub_M.p);
+    k_gather<int><<<gridn(nr), 256, 0, st>>>(p.fsat_n, rows.p, nr, 1, sub_fn.p);
+    k_gather<float><<<gridn((int64_t)nr * R), 256, 0, st>>>(p.fsat_mid, rows.p, nr, R, sub_fm.p);
+    k_gather<int64_t><<<gridn((int64_t)nr * R), 256, 0, st>>>(p.fsat_id, rows.p, nr, R, sub_fi.p);
+    if (cells)
+      k_gather<int64_t><<<gridn(nr * w), 256, 0, st>>>(cells, rows.p, nr, (int)w, sub_cells.p);
+    QADC_CUDA(cudaGetLastError());
+    Prep sp;
+    sp.cells = cells ? sub_cells.p : nullptr;
+    sp.qt = sub_qt.p;
+    sp.qmin_f = sub_qmin.p;
+    sp.delta_f = sub_delta.p;
+    sp.depth = sub_depth.p;
+    sp.M_bits = sub_M.p;
+    sp.fsat_n = sub_fn.p;
+    sp.fsat_mid = sub_fm.p;
+    sp.fsat_id = sub_fi.p;
     const int cap2 = (int)std::min<int64_t>(std::max<int64_t>((int64_t)need + 1024, 2LL * cap_g),
                                             (int64_t)1 << 28);
-    rc = search_impl(idx, sub_q.p, nr, R, ma, init, lp, cp, sub_ids.p, sub_d.p, sub_n.p, st, ss,
-                     sub_M.p, cap2, depth + 1, no_fsat, prmt, force_tc, one_sm);
+    rc = scan_impl(idx, sp, nr, R, ma, init, sub_ids.p, sub_d.p, sub_n.p, st, ss, cap2, level + 1,
+                   prmt, force_tc, one_sm);
     if (rc) return rc;
     k_scatter_out<<<gridn((int64_t)nr * R), 256, 0, st>>>(sub_ids.p, sub_d.p, sub_n.p, rows.p, nr,
                                                           R, out_ids, out_d, out_n);
   }
   QADC_CUDA(cudaGetLastError());
   return kOk;
+}
+
+// Whole search: prepare into stream-ordered buffers, then scan.
+int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int ma, int init,
+                const float *lut_in, const int64_t *cells_in, int64_t *out_ids, float *out_d,
+                int32_t *out_n, cudaStream_t st, SearchStats &ss, int cap_g, bool no_fsat,
+                bool prmt, bool force_tc, bool one_sm) {
+  if (nq == 0) return kOk;
+  const int m = idx->m;
+  const int nslots = idx->K ? ma : 1;
+  const int64_t npairs = (int64_t)nq * nslots;
+  DevBuf<int64_t> cells_b, fsat_id;
+  DevBuf<float> qmax_b, qmin_f, delta_f, fsat_mid;
+  DevBuf<uint32_t> qt_b;
+  DevBuf<unsigned> M_bits;
+  DevBuf<int> fsat_n;
+  DevBuf<uint8_t> depth;
+  if (qmax_b.alloc(nq, st) || qt_b.alloc(npairs * m * 4, st) || qmin_f.alloc(npairs, st) ||
+      delta_f.alloc(npairs, st) || M_bits.alloc(nq, st) || fsat_n.alloc(nq, st) ||
+      fsat_mid.alloc((int64_t)nq * R, st) || fsat_id.alloc((int64_t)nq * R, st) ||
+      depth.alloc(npairs, st) || (idx->K && !cells_in && cells_b.alloc(npairs, st)))
+    return cuda_fail(cudaGetLastError(), "alloc workspace");
+  int rc = prepare_impl(idx, queries, nq, R, ma, init, lut_in, cells_in, no_fsat, st, ss,
+                        cells_in ? nullptr : cells_b.p, qt_b.p, qmin_f.p, delta_f.p, depth.p,
+                        qmax_b.p, M_bits.p, fsat_n.p, fsat_mid.p, fsat_id.p);
+  if (rc) return rc;
+  Prep p;
+  p.cells = idx->K ? (cells_in ? cells_in : cells_b.p) : nullptr;
+  p.qt = qt_b.p;
+  p.qmin_f = qmin_f.p;
+  p.delta_f = delta_f.p;
+  p.depth = depth.p;
+  p.M_bits = M_bits.p;
+  p.fsat_n = fsat_n.p;
+  p.fsat_mid = fsat_mid.p;
+  p.fsat_id = fsat_id.p;
+  rc = scan_impl(idx, p, nq, R, ma, init, out_ids, out_d, out_n, st, ss, cap_g, 0, prmt, force_tc,
+                 one_sm);
+  if (rc) return rc;
+  float t = 0.f;
+  cudaEvent_t *ev = phase_events();
+  cudaEventElapsedTime(&t, ev[kEvStart], ev[kEvProbe]);
+  ss.probe_us += t * 1e3;
+  cudaEventElapsedTime(&t, ev[kEvProbe], ev[kEvTables]);
+  ss.tables_us += t * 1e3;
+  return kOk;
+}
+
+int candidate_capacity(int nq, int R) {
+  // per-query candidate capacity: at least 8192 / 8R, and up to 64K while
+  // the lists stay within ~512 MB (small batches with heavy ties at the
+  // boundary level then never need the rerun pass)
+  const int64_t cap_mem = (512LL << 20) / 12 / std::max(nq, 1);
+  return (int)std::min<int64_t>(
+      std::max<int64_t>({8192, 8LL * R, std::min<int64_t>(65536, cap_mem)}), 1 << 20);
+}
+
+void write_stats(const SearchStats &ss, int64_t *stats) {
+  if (!stats) return;
+  stats[0] = ss.codes;
+  stats[1] = ss.cands;
+  stats[2] = ss.reruns;
+  stats[3] = ss.scan_launches;
+  stats[4] = ss.launches;
+  stats[5] = (int64_t)llround(ss.scan_us);
+  stats[6] = ss.scan_tc;  // scan kernel: 1 = int8 tensor-core, 0 = PRMT
+  stats[7] = (int64_t)llround(ss.probe_us);
+  stats[8] = (int64_t)llround(ss.tables_us);
+  stats[9] = (int64_t)llround(ss.work_us);
+  stats[10] = (int64_t)llround(ss.select_us);
+  for (int i = 11; i < 16; i++) stats[i] = 0;
 }
 
 }  // namespace
@@ -840,15 +945,10 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
     on = dn.p;
   }
   SearchStats ss;
-  // per-query candidate capacity: at least 8192 / 8R, and up to 64K while
-  // the lists stay within ~512 MB (small batches with heavy ties at the
-  // boundary level then never need the rerun pass)
-  const int64_t cap_mem = (512LL << 20) / 12 / std::max(nq, 1);
-  const int cap_g = (int)std::min<int64_t>(
-      std::max<int64_t>({8192, 8LL * R, std::min<int64_t>(65536, cap_mem)}), 1 << 20);
-  int rc = search_impl(idx, q, nq, R, ma, init, lin, cin, oi, od, on, st, ss, nullptr, cap_g, 0,
-                       (flags & QADC_B200_NO_FSAT) != 0, (flags & QADC_B200_SCAN_PRMT) != 0,
-                       (flags & QADC_B200_SCAN_TC) != 0, (flags & QADC_B200_SCAN_TC1) != 0);
+  int rc = search_impl(idx, q, nq, R, ma, init, lin, cin, oi, od, on, st, ss,
+                       candidate_capacity(nq, R), (flags & QADC_B200_NO_FSAT) != 0,
+                       (flags & QADC_B200_SCAN_PRMT) != 0, (flags & QADC_B200_SCAN_TC) != 0,
+                       (flags & QADC_B200_SCAN_TC1) != 0);
   if (rc) return rc;
   if (host) {
     QADC_CUDA(cudaMemcpyAsync(out_ids, oi, (size_t)nq * R * 8, cudaMemcpyDeviceToHost, st));
@@ -856,20 +956,90 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
     QADC_CUDA(cudaMemcpyAsync(out_n, on, (size_t)nq * 4, cudaMemcpyDeviceToHost, st));
     QADC_CUDA(cudaStreamSynchronize(st));
   }
+  write_stats(ss, stats);
+  return kOk;
+}
+
+namespace {
+int check_search_args(const qadc_b200_index *idx, int nq, int R, int ma, int init) {
+  if (!idx) return arg_error("null index");
+  if (R < 1) return arg_error("R must be positive");
+  if (init < 1) return arg_error("init must be positive");
+  if (nq < 0) return arg_error("nq must be non-negative");
+  if (idx->K && (ma < 1 || ma > idx->K)) return arg_error("ma must be in 1..K");
+  if (R > 1 << 20) return arg_error("R too large");
+  return kOk;
+}
+}  // namespace
+
+extern "C" int qadc_b200_search_prepare(qadc_b200_index *idx, const float *queries, int nq, int R,
+                                        int ma, int init, unsigned flags, const float *lut_in,
+                                        const int64_t *cells_in, int64_t *cells, uint32_t *qt,
+                                        float *qmin_f, float *delta_f, uint8_t *depth,
+                                        float *qmax, uint32_t *M_bits, int32_t *fsat_n,
+                                        float *fsat_mid, int64_t *fsat_id, void *stream,
+                                        int64_t *stats) {
+  g_err.clear();
+  if (int rc = check_search_args(idx, nq, R, ma, init)) return rc;
+  const bool inj = flags & QADC_B200_LUT_IN;
+  if (inj && (!lut_in || (idx->K && !cells_in)))
+    return arg_error("LUT injection needs lut_in (and cells_in for an IVF index)");
+  if (!qt || !qmin_f || !delta_f || !depth || !qmax || !M_bits || !fsat_n || !fsat_mid ||
+      !fsat_id || (idx->K && !cells) || (nq > 0 && !queries && !inj))
+    return arg_error("null argument");
+  if (flags & QADC_B200_HOST_IO) return arg_error("search_prepare takes device pointers only");
+  cudaStream_t st = (cudaStream_t)stream;
+  retain_pool_memory();
+  SearchStats ss;
+  int rc = prepare_impl(idx, queries, nq, R, ma, init, inj ? lut_in : nullptr,
+                        inj ? cells_in : nullptr, (flags & QADC_B200_NO_FSAT) != 0, st, ss,
+                        idx->K ? cells : nullptr, qt, qmin_f, delta_f, depth, qmax,
+                        (unsigned *)M_bits, fsat_n, fsat_mid, fsat_id);
+  if (rc) return rc;
   if (stats) {
-    stats[0] = ss.codes;
-    stats[1] = ss.cands;
-    stats[2] = ss.reruns;
-    stats[3] = ss.scan_launches;
-    stats[4] = ss.launches;
-    stats[5] = (int64_t)llround(ss.scan_us);
-    stats[6] = ss.scan_tc;  // scan kernel: 1 = int8 tensor-core, 0 = PRMT
-    stats[7] = (int64_t)llround(ss.probe_us);
-    stats[8] = (int64_t)llround(ss.tables_us);
-    stats[9] = (int64_t)llround(ss.work_us);
-    stats[10] = (int64_t)llround(ss.select_us);
-    for (int i = 11; i < 16; i++) stats[i] = 0;
+    QADC_CUDA(cudaStreamSynchronize(st));
+    float t = 0.f;
+    cudaEvent_t *ev = phase_events();
+    cudaEventElapsedTime(&t, ev[kEvStart], ev[kEvProbe]);
+    ss.probe_us += t * 1e3;
+    cudaEventElapsedTime(&t, ev[kEvProbe], ev[kEvTables]);
+    ss.tables_us += t * 1e3;
+    write_stats(ss, stats);
   }
+  return kOk;
+}
+
+extern "C" int qadc_b200_search_scan(qadc_b200_index *idx, int nq, int R, int ma, int init,
+                                     unsigned flags, const int64_t *cells, const uint32_t *qt,
+                                     const float *qmin_f, const float *delta_f,
+                                     const uint8_t *depth, uint32_t *M_bits,
+                                     const int32_t *fsat_n, const float *fsat_mid,
+                                     const int64_t *fsat_id, int64_t *out_ids, float *out_d,
+                                     int32_t *out_n, void *stream, int64_t *stats) {
+  g_err.clear();
+  if (int rc = check_search_args(idx, nq, R, ma, init)) return rc;
+  if (!qt || !qmin_f || !delta_f || !depth || !M_bits || !fsat_n || !fsat_mid || !fsat_id ||
+      (idx->K && !cells) || !out_ids || !out_d || !out_n)
+    return arg_error("null argument");
+  if (flags & QADC_B200_HOST_IO) return arg_error("search_scan takes device pointers only");
+  cudaStream_t st = (cudaStream_t)stream;
+  retain_pool_memory();
+  Prep p;
+  p.cells = idx->K ? cells : nullptr;
+  p.qt = qt;
+  p.qmin_f = qmin_f;
+  p.delta_f = delta_f;
+  p.depth = depth;
+  p.M_bits = (unsigned *)M_bits;
+  p.fsat_n = fsat_n;
+  p.fsat_mid = fsat_mid;
+  p.fsat_id = fsat_id;
+  SearchStats ss;
+  int rc = scan_impl(idx, p, nq, R, ma, init, out_ids, out_d, out_n, st, ss,
+                     candidate_capacity(nq, R), 0, (flags & QADC_B200_SCAN_PRMT) != 0,
+                     (flags & QADC_B200_SCAN_TC) != 0, (flags & QADC_B200_SCAN_TC1) != 0);
+  if (rc) return rc;
+  write_stats(ss, stats);
   return kOk;
 }
 

@@ -7,9 +7,11 @@
 //   * pq.encode_batch (pq.py:210-217): optional rotation x @ R^T, then the
 //     per-subspace argmin, packed two sub-codes per byte, low nibble =
 //     even sub-code (pq.py:90-105).
-// The rotation is a sequential fp32 FMA chain (OpenBLAS's order is unpinned,
-// SURVEY A.7), and k*d > 2^20 coarse assignment uses the same einsum form
-// instead of the reference's clamped GEMM expansion.
+// The rotation is a sequential fp32 FMA chain (the reference's X @ R^T is an
+// OpenBLAS sgemm whose blocking is not reproduced; codes near a sub-space
+// tie may differ — the index is an input, parity is given the index), and
+// k*d > 2^20 coarse assignment uses the same einsum form instead of the
+// reference's clamped GEMM expansion.
 #include "qadc_b200.h"
 #include "internal.cuh"
 
@@ -44,21 +46,43 @@ __device__ __forceinline__ float sqdist_einsum(const float *__restrict__ a, cons
   return __fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3]));
 }
 
-// y = R x (sequential fp32 FMA chain, the search path's arithmetic), one CTA
-// per 8 vectors.
-__global__ void k_rotate(const float *__restrict__ X, int64_t n, int d, const float *__restrict__ R,
-                         float *__restrict__ Y) {
-  extern __shared__ float sx[];  // 8 * d
-  const int64_t v0 = (int64_t)blockIdx.x * 8;
-  const int nv = (int)(n - v0 < 8 ? n - v0 : 8);
+// y = R x for a tile of 32 vectors per CTA (pq.py:210-217's X @ R^T; the
+// reference's sgemm order is not reproduced: the index is an input and
+// parity is defined given the index). R^T rows are read coalesced through
+// L1 (thread i owns output i), the vectors are staged in shared memory and
+// broadcast; each thread accumulates 16 vectors (sequential fp32 FMA).
+constexpr int kRotTile = 32;
+__global__ void __launch_bounds__(256) k_rotate(const float *__restrict__ X, int64_t n, int d,
+                                                const float *__restrict__ RT,
+                                                float *__restrict__ Y) {
+  extern __shared__ float sx[];  // kRotTile * d
+  const int64_t v0 = (int64_t)blockIdx.x * kRotTile;
+  const int nv = (int)(n - v0 < kRotTile ? n - v0 : kRotTile);
   for (int t = threadIdx.x; t < nv * d; t += blockDim.x) sx[t] = X[v0 * d + t];
+  for (int t = nv * d + threadIdx.x; t < kRotTile * d; t += blockDim.x) sx[t] = 0.f;
   __syncthreads();
-  for (int t = threadIdx.x; t < nv * d; t += blockDim.x) {
-    const int v = t / d, i = t % d;
-    float acc = 0.f;
-    for (int k = 0; k < d; k++) acc = __fmaf_rn(R[(size_t)i * d + k], sx[v * d + k], acc);
-    Y[(v0 + v) * d + i] = acc;
+  const int half = threadIdx.x >> 7;  // vectors half*16 .. half*16+15
+  for (int i = threadIdx.x & 127; i < d; i += 128) {
+    float acc[16];
+#pragma unroll
+    for (int v = 0; v < 16; v++) acc[v] = 0.f;
+    const float *xs = sx + (size_t)half * 16 * d;
+    for (int k = 0; k < d; k++) {
+      const float r = __ldg(RT + (size_t)k * d + i);
+#pragma unroll
+      for (int v = 0; v < 16; v++) acc[v] = __fmaf_rn(r, xs[(size_t)v * d + k], acc[v]);
+    }
+#pragma unroll
+    for (int v = 0; v < 16; v++) {
+      const int vv = half * 16 + v;
+      if (vv < nv) Y[(v0 + vv) * d + i] = acc[v];
+    }
   }
+}
+
+__global__ void k_transpose_sq(const float *__restrict__ in, int d, float *__restrict__ out) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < d * d; t += gridDim.x * blockDim.x)
+    out[(size_t)(t % d) * d + t / d] = in[t];
 }
 
 // One thread per (vector, output byte): sub-quantizers 2b and 2b+1.
@@ -129,16 +153,22 @@ extern "C" int qadc_b200_encode(const float *X, int64_t n, int d, int m, const f
   }
   if (n == 0) return kOk;
   const float *src = X;
-  float *rot = nullptr;
+  float *rot = nullptr, *rt = nullptr;
   if (rotation) {
     QADC_CUDA(cudaMallocAsync(&rot, (size_t)n * d * 4, st));
-    k_rotate<<<(unsigned)((n + 7) / 8), 256, (size_t)8 * d * 4, st>>>(X, n, d, rotation, rot);
+    QADC_CUDA(cudaMallocAsync(&rt, (size_t)d * d * 4, st));
+    k_transpose_sq<<<(d * d + 255) / 256, 256, 0, st>>>(rotation, d, rt);
+    const size_t smem = (size_t)kRotTile * d * 4;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_rotate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_rotate<<<(unsigned)((n + kRotTile - 1) / kRotTile), 256, smem, st>>>(X, n, d, rt, rot);
     src = rot;
   }
   const int64_t work = n * (m / 2);
   const int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 64);
   k_encode<<<grid, 256, 0, st>>>(src, n, m, d / m, codebooks, out);
   if (rot) cudaFreeAsync(rot, st);
+  if (rt) cudaFreeAsync(rt, st);
   QADC_CUDA(cudaGetLastError());
   return kOk;
 }

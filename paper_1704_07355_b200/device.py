@@ -30,6 +30,9 @@ def _np(a, dtype):
 
 
 class DeviceIndex:
+    STAT_KEYS = ("codes", "candidates", "reruns", "scan_launches", "launches", "scan_us",
+                 "scan_tc", "probe_us", "tables_us", "work_us", "select_us")
+
     def __init__(self, handle: int, d: int, m: int, K: int, nlists: int, ncodes: int):
         self._h = handle
         self.d, self.m, self.K, self.nlists, self.ncodes = d, m, K, nlists, ncodes
@@ -142,9 +145,68 @@ class DeviceIndex:
                 _native.dptr(cells_d), _native.dptr(ids), _native.dptr(dist), _native.dptr(cnt),
                 st.cuda_stream, stats.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
         _native.check(rc, "search_batch")
-        keys = ("codes", "candidates", "reruns", "scan_launches", "launches", "scan_us", "scan_tc",
-                "probe_us", "tables_us", "work_us", "select_us")
-        return BatchResult(ids, dist, cnt, {k: int(v) for k, v in zip(keys, stats)})
+        return BatchResult(ids, dist, cnt, {k: int(v) for k, v in zip(self.STAT_KEYS, stats)})
+
+    # the per-query state between the two halves of a search (prepare ->
+    # scan), in the order of qadc_b200_search_prepare's output arguments
+    PREP_KEYS = ("cells", "qt", "qmin_f", "delta_f", "depth", "qmax", "M_bits", "fsat_n",
+                 "fsat_mid", "fsat_id")
+
+    def prep_buffers(self, nq: int, R: int, ma: int = 1, device="cuda") -> dict:
+        """Empty prepared-state tensors for nq queries (see prepare)."""
+        import torch
+
+        w = ma if self.K else 1
+        i64, f32, u8, i32 = torch.int64, torch.float32, torch.uint8, torch.int32
+        return {"cells": torch.zeros((nq, w), dtype=i64, device=device),
+                "qt": torch.empty((nq, w, self.m * 4), dtype=torch.int32, device=device),
+                "qmin_f": torch.empty((nq, w), dtype=f32, device=device),
+                "delta_f": torch.empty((nq, w), dtype=f32, device=device),
+                "depth": torch.empty((nq, w), dtype=u8, device=device),
+                "qmax": torch.empty(nq, dtype=f32, device=device),
+                "M_bits": torch.empty(nq, dtype=i32, device=device),
+                "fsat_n": torch.empty(nq, dtype=i32, device=device),
+                "fsat_mid": torch.empty((nq, R), dtype=f32, device=device),
+                "fsat_id": torch.empty((nq, R), dtype=i64, device=device)}
+
+    def prepare(self, queries, R: int, ma: int = 1, init: int = 1000, with_fsat: bool = True,
+                out: dict | None = None, stream=None) -> dict:
+        """First half of `search`: the Index + Tables phases (adc.py:140-174)
+        of every query — probe order, uint8 tables, qmin / delta, qmax,
+        initial bound and F_sat — into device tensors (`out`, or new ones).
+        `queries` is a (Q, d) float32 device tensor."""
+        import torch
+
+        st = stream if stream is not None else torch.cuda.current_stream()
+        q = queries.to(dtype=torch.float32).contiguous()
+        p = out if out is not None else self.prep_buffers(q.shape[0], R, ma, q.device)
+        flags = 0 if with_fsat else _native.NO_FSAT
+        _native.check(_native.load_library().qadc_b200_search_prepare(
+            self._h, _native.dptr(q), q.shape[0], R, ma, init, flags, None, None,
+            *[_native.dptr(p[k]) for k in self.PREP_KEYS], st.cuda_stream, None), "search_prepare")
+        return p
+
+    def scan(self, prep: dict, R: int, ma: int = 1, init: int = 1000, stream=None,
+             scan: str = "auto") -> BatchResult:
+        """Second half of `search`: work list, scan and exact top-R over a
+        prepared state (prepare, possibly assembled from other ranks)."""
+        import torch
+
+        st = stream if stream is not None else torch.cuda.current_stream()
+        nq = prep["M_bits"].shape[0]
+        dev = prep["M_bits"].device
+        ids = torch.empty((nq, R), dtype=torch.int64, device=dev)
+        dist = torch.empty((nq, R), dtype=torch.float32, device=dev)
+        cnt = torch.empty(nq, dtype=torch.int32, device=dev)
+        flags = {"auto": 0, "prmt": _native.SCAN_PRMT, "tc": _native.SCAN_TC,
+                 "tc1": _native.SCAN_TC | _native.SCAN_TC1}[scan]
+        stats = np.zeros(16, dtype=np.int64)
+        _native.check(_native.load_library().qadc_b200_search_scan(
+            self._h, nq, R, ma, init, flags, *[_native.dptr(prep[k]) for k in self.PREP_KEYS
+                                               if k != "qmax"],
+            _native.dptr(ids), _native.dptr(dist), _native.dptr(cnt), st.cuda_stream,
+            stats.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "search_scan")
+        return BatchResult(ids, dist, cnt, {k: int(v) for k, v in zip(self.STAT_KEYS, stats)})
 
     def tables(self, queries, R: int, ma: int = 1, init: int = 1000, stream=None) -> dict:
         """The Index + Tables phases of `search` (adc.py:140-174) with their

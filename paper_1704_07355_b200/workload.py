@@ -321,6 +321,73 @@ def ivf_rows(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, device="cuda",
     return rows, rid, row_off
 
 
+def encode_torch(pq: _PQ, resid):
+    """pq.encode_batch (pq.py:210-217) restated in plain torch for the
+    REFERENCE arm's index setup (no product kernels in that process):
+    rotation x @ R^T in fp32 (TF32 off), per sub-space argmin of
+    ||c||^2 - 2 y.c (ties to the lowest index), two sub-codes per byte,
+    low nibble first (pq.py:90-105). Near-tie codes may differ from the
+    GPU encoder's exact einsum form; the index is an input of the timed
+    path."""
+    import torch
+
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        y = resid
+        if pq.rotation is not None:
+            y = resid @ torch.from_numpy(np.ascontiguousarray(pq.rotation, np.float32)).to(
+                resid.device).t()
+        cb = torch.from_numpy(pq.codebooks).to(resid.device)  # (m, 16, dsub)
+        m, dsub = cb.shape[0], cb.shape[2]
+        sc = (cb * cb).sum(-1)[None] - 2.0 * torch.einsum("njd,jkd->njk",
+                                                         y.view(-1, m, dsub), cb)
+        c = sc.argmin(-1).to(torch.uint8)  # (n, m)
+        return (c[:, 0::2] | (c[:, 1::2] << 4)).contiguous()
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def ivf_rows_torch(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, keep, device="cuda"):
+    """Reference-arm index setup in plain torch (no product library): the
+    same seeded base as ivf_rows (configs 4 / 2 chunk grids), the same
+    TF32 coarse assignment, and encode_torch for the members of the lists
+    flagged in `keep` (bool, K) only — the CPU sample scans nothing else.
+    Returns (codes, ids, row_off) row-ordered, other lists empty."""
+    import torch
+
+    C = torch.from_numpy(np.ascontiguousarray(coarse, dtype=np.float32)).to(device)
+    cn = (C.double() ** 2).sum(1).float()
+    keep_d = torch.as_tensor(keep, dtype=torch.bool, device=device)
+    if cfg.sharding == "range":
+        spans = [(g * CFG4_CHUNK, min(n, (g + 1) * CFG4_CHUNK), g)
+                 for g in range(-(-n // CFG4_CHUNK))]
+    else:
+        chunk = 1 << 22
+        spans = [(c0, min(n, c0 + chunk), c0 // chunk) for c0 in range(0, n, chunk)]
+    codes, labels, ids = [], [], []
+    for a, b, g in spans:
+        k = b - a
+        if cfg.sharding == "range":
+            X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000 + 4, centre_seed=CORPUS,
+                                      stream=datagen.STREAM_BASE * 100_000 + g, device=device)
+        else:
+            X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000, centre_seed=CORPUS,
+                                      stream=datagen.STREAM_BASE * 100 + g, device=device)
+        lab = assign_tensor_core(X, C, cn)
+        sel = keep_d[lab].nonzero().flatten()
+        if sel.numel():
+            codes.append(encode_torch(pq, X[sel] - C[lab[sel]]))
+            labels.append(lab[sel])
+            ids.append(sel + a)
+        del X, lab
+    if not codes:
+        z = torch.zeros(0, dtype=torch.int64, device=device)
+        return (torch.zeros((0, pq.m // 2), dtype=torch.uint8, device=device), z,
+                torch.zeros(C.shape[0] + 1, dtype=torch.int64, device=device))
+    return _sorted_rows(torch.cat(codes), torch.cat(labels), torch.cat(ids), C.shape[0])
+
+
 def make_ivf_index(pq: _PQ, coarse: np.ndarray, rows, ids, row_off, device="cuda"):
     import torch
 

@@ -174,9 +174,88 @@ def test_ivf_list_shards_with_global_prefix_equal_unsharded(gpu):
             rotation=Rt, coarse=C, ids=torch.cat(ids).contiguous())
         sh.set_prefix(pre_rows, pre_off, szn, ids=pre_ids)
         parts.append(sh.search(qs, R, ma=ma, init=init, with_fsat=(shard == 0)))
+        # query-sharded Tables phase (dist.sharded_prepare's exchange, the
+        # all_gather emulated by concatenation): two halves of the batch
+        # prepared separately give the same state as the whole batch, and
+        # scanning it gives this shard's search result bit for bit
+        qd = torch.from_numpy(qs).cuda()
+        halves = [sh.prepare(qd[:13], R, ma=ma, init=init), sh.prepare(qd[13:], R, ma=ma, init=init)]
+        prep = {k: torch.cat([h[k] for h in halves]).contiguous() for k in halves[0]}
+        whole = sh.prepare(qd, R, ma=ma, init=init)
+        for k in prep:
+            assert torch.equal(prep[k], whole[k]), k
+        if shard != 0:
+            prep["fsat_n"].zero_()
+        res2 = sh.scan(prep, R, ma=ma, init=init)
+        assert np.array_equal(res2.ids.cpu().numpy(), parts[-1].ids)
+        assert np.array_equal(res2.distances.cpu().numpy().view(np.uint32),
+                              parts[-1].distances.view(np.uint32))
     gi, gd, gc = merge_sorted_lists(torch.from_numpy(np.concatenate([x.ids for x in parts], 1)),
                                     torch.from_numpy(np.concatenate([x.distances for x in parts],
                                                                     1)), R)
     assert np.array_equal(gi.numpy(), want.ids)
     assert np.array_equal(gd.numpy().view(np.uint32), want.distances.view(np.uint32))
     assert np.array_equal(gc.numpy(), want.counts)
+
+
+class _FakePrepIndex:
+    """CPU stand-in for DeviceIndex.prepare: a deterministic per-query
+    function with the same output names, shapes and dtypes (the exchange
+    under test only moves rows)."""
+
+    K, m = 64, 32
+
+    def prepare(self, queries, R, ma=1, init=1000, with_fsat=True):
+        nq = queries.shape[0]
+        s = (queries.double().sum(1) * 1000).long()
+        ar = torch.arange(ma)
+        p = {"cells": (s[:, None] * 7 + ar) % self.K,
+             "qt": ((s[:, None, None] + torch.arange(self.m * 4)) % 127).int().expand(
+                 nq, ma, self.m * 4).contiguous(),
+             "qmin_f": queries[:, :ma].float().contiguous(),
+             "delta_f": queries[:, -ma:].float().contiguous(),
+             "depth": (s[:, None] % 5 + ar).to(torch.uint8),
+             "qmax": queries.max(1).values.float(),
+             "M_bits": (s % 1000).int(),
+             "fsat_n": (s % 3).int() if with_fsat else torch.zeros(nq, dtype=torch.int32),
+             "fsat_mid": queries[:, :1].expand(nq, R).float().contiguous(),
+             "fsat_id": (s[:, None] + torch.arange(R)).long()}
+        return p
+
+
+def _prep_worker(rank, world, port, nq, q):
+    from paper_1704_07355_b200.dist import sharded_prepare
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    qs = torch.from_numpy(np.random.default_rng(5).random((nq, 16)).astype(np.float32))
+    got = sharded_prepare(_FakePrepIndex(), qs, 10, 4, 1000)
+    q.put((rank, {k: v.numpy() for k, v in got.items()}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nq", [9, 16])
+def test_gloo_world2_sharded_prepare_equals_local(nq):
+    """Query-sharded Index + Tables phases (dist.sharded_prepare): each of
+    two ranks prepares half the batch (odd sizes padded), the halves are
+    all-gathered, and every rank's state equals preparing the whole batch
+    locally — except F_sat, which only the prefix owner (rank 0) keeps."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + (os.getpid() + nq) % 2000
+    procs = [ctx.Process(target=_prep_worker, args=(r, world, port, nq, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    qs = torch.from_numpy(np.random.default_rng(5).random((nq, 16)).astype(np.float32))
+    want = {k: v.numpy() for k, v in _FakePrepIndex().prepare(qs, 10, 4, 1000).items()}
+    for rank, g in got.items():
+        for k, v in want.items():
+            if k == "fsat_n" and rank != 0:
+                assert not g[k].any()
+            else:
+                assert np.array_equal(g[k], v), (rank, k)
