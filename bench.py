@@ -193,6 +193,15 @@ def host_info():
             "openblas": blas}
 
 
+def _product_lib_mapped() -> bool:
+    """Whether libqadc_b200.so is mapped into this process (the reference
+    arm must never load it)."""
+    try:
+        return "libqadc_b200" in open("/proc/self/maps").read()
+    except OSError:
+        return False
+
+
 def config_of(cfg, ivf_cfg, n, nq, ma, world):
     """The workload's config dict, identical in both arms."""
     c = {"workload": cfg.name, "m": cfg.m, "d": cfg.mix.d, "Q": nq, "R": cfg.R,
@@ -698,6 +707,7 @@ def run_reference(args):
                          "kind": "reference" if use_ref else "port", "sample": desc},
         "cpu_host": host_info(),
         "index_setup_s": round(t_build, 1),
+        "product_library_loaded": _product_lib_mapped(),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

@@ -85,31 +85,50 @@ __global__ void k_transpose_sq(const float *__restrict__ in, int d, float *__res
     out[(size_t)(t % d) * d + t / d] = in[t];
 }
 
-// One thread per (vector, output byte): sub-quantizers 2b and 2b+1.
-__global__ void k_encode(const float *__restrict__ X, int64_t n, int m, int dsub,
-                         const float *__restrict__ codebooks, uint8_t *__restrict__ out) {
-  const int mrows = m / 2;
-  const int d = m * dsub;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * mrows;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = t / mrows;
-    const int b = (int)(t % mrows);
-    uint8_t byte = 0;
-    for (int h = 0; h < 2; h++) {
-      const int j = 2 * b + h;
-      const float *x = X + v * d + (size_t)j * dsub;
+// PQ encoding of a tile of 32 vectors per CTA: the tile (rows padded to
+// d + 1 words: conflict-free column reads) and the codebooks sit in shared
+// memory; warp w takes sub-spaces w, w + 8, ..., lane = vector, so every
+// codebook read is a warp-wide broadcast. Per sub-space: argmin over the 16
+// centroids of the einsum-order squared distance (ties to the lowest
+// index), then two sub-codes per byte, low nibble = even sub-code.
+constexpr int kEncTile = 32;
+__global__ void __launch_bounds__(256) k_encode(const float *__restrict__ X, int64_t n, int m,
+                                                int dsub, const float *__restrict__ codebooks,
+                                                uint8_t *__restrict__ out) {
+  extern __shared__ float esm[];
+  const int d = m * dsub, dp = d + 1;
+  float *sx = esm;                                  // [kEncTile][d + 1]
+  float *scb = sx + (size_t)kEncTile * dp;          // [m][16][dsub]
+  uint8_t *sc = (uint8_t *)(scb + (size_t)m * 16 * dsub);  // [kEncTile][m]
+  const int64_t v0 = (int64_t)blockIdx.x * kEncTile;
+  const int nv = (int)(n - v0 < kEncTile ? n - v0 : kEncTile);
+  for (int t = threadIdx.x; t < m * 16 * dsub; t += blockDim.x) scb[t] = codebooks[t];
+  for (int t = threadIdx.x; t < nv * d; t += blockDim.x) {
+    const int v = t / d, c = t - v * d;
+    sx[v * dp + c] = X[v0 * d + t];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane < nv) {
+    for (int j = w; j < m; j += 8) {
+      const float *x = sx + (size_t)lane * dp + (size_t)j * dsub;
       int best = 0;
       float bd = 0.f;
       for (int i = 0; i < 16; i++) {
-        const float dd = sqdist_einsum(x, codebooks + ((size_t)j * 16 + i) * dsub, dsub);
+        const float dd = sqdist_einsum(x, scb + ((size_t)j * 16 + i) * dsub, dsub);
         if (i == 0 || dd < bd) {
           bd = dd;
           best = i;
         }
       }
-      byte |= (uint8_t)(best << (4 * h));
+      sc[lane * m + j] = (uint8_t)best;
     }
-    out[t] = byte;
+  }
+  __syncthreads();
+  const int mrows = m / 2;
+  for (int t = threadIdx.x; t < nv * mrows; t += blockDim.x) {
+    const int v = t / mrows, b = t - v * mrows;
+    out[(v0 + v) * mrows + b] = (uint8_t)(sc[v * m + 2 * b] | (sc[v * m + 2 * b + 1] << 4));
   }
 }
 
@@ -164,9 +183,16 @@ extern "C" int qadc_b200_encode(const float *X, int64_t n, int d, int m, const f
     k_rotate<<<(unsigned)((n + kRotTile - 1) / kRotTile), 256, smem, st>>>(X, n, d, rt, rot);
     src = rot;
   }
-  const int64_t work = n * (m / 2);
-  const int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 64);
-  k_encode<<<grid, 256, 0, st>>>(src, n, m, d / m, codebooks, out);
+  const size_t esmem = ((size_t)kEncTile * (d + 1) + (size_t)m * 16 * (d / m)) * 4 +
+                       (size_t)kEncTile * m;
+  if (esmem > 227 * 1024) {
+    set_error("encode: d too large for the shared-memory tile");
+    return kErrArgs;
+  }
+  if (esmem > 48 * 1024)
+    cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem);
+  k_encode<<<(unsigned)((n + kEncTile - 1) / kEncTile), 256, esmem, st>>>(src, n, m, d / m,
+                                                                        codebooks, out);
   if (rot) cudaFreeAsync(rot, st);
   if (rt) cudaFreeAsync(rt, st);
   QADC_CUDA(cudaGetLastError());

@@ -152,7 +152,7 @@ class IvfConfig:
     init: int
     K: int
     nprobe: int
-    coarse_file: str  # "" = coarse model trained on the GPU at setup (config 4)
+    coarse_file: str  # bench_data/: GPU Lloyd (tools/train_coarse.py)
     codebooks_file: str
     rotation_file: str
     sharding: str  # "lists" (config 2) or "range" (config 4)
@@ -163,7 +163,8 @@ IVF_CONFIGS = {
                       10_000, 100, 1000, 4096, 16, "cfg2_coarse_K4096.npy",
                       "cfg2_m32_codebooks.npy", "cfg2_rotation.npy", "lists"),
     "cfg4": IvfConfig("cfg4_ivf_opq_K65536_m32_N1e9_Q1e4", datagen.SIFT_LIKE, 32, 1_000_000_000,
-                      10_000, 100, 1000, 65536, 64, "", "", "cfg2_rotation.npy", "range"),
+                      10_000, 100, 1000, 65536, 64, "cfg4_coarse_K65536.npy",
+                      "cfg4_m32_codebooks.npy", "cfg2_rotation.npy", "range"),
 }
 
 # config 4 base: a global grid of 10^6-vector chunks (chunk g = ids
@@ -173,9 +174,6 @@ CFG4_CHUNK = 1_000_000
 
 
 def load_ivf_model(cfg: IvfConfig):
-    if not cfg.coarse_file:
-        with _phase("train_model"):
-            return train_ivf_model_gpu(cfg)
     pq = _PQ(np.load(BENCH_DATA / cfg.codebooks_file), np.load(BENCH_DATA / cfg.rotation_file))
     return pq, np.load(BENCH_DATA / cfg.coarse_file)
 
@@ -202,53 +200,6 @@ def assign_tensor_core(X, C, cn=None, chunk: int = 16384):
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
     return out
-
-
-def train_ivf_model_gpu(cfg: IvfConfig, n_learn: int = 1 << 21, iters: int = 8,
-                        pq_learn: int = 1 << 18, pq_iters: int = 25, seed: int = 0):
-    """Config 4 model, trained on the GPU at setup (seeded): the reference's
-    NumPy k-means cannot train K=65536 (SURVEY 7 "Config-4 index build"),
-    so coarse centroids = Lloyd k-means (seeded random-sample init, empty
-    cells re-seeded from random learn points) on 2^21 learn vectors, OPQ
-    rotation = config 2's seeded orthogonal matrix, residual PQ codebooks =
-    Lloyd (16 centroids per 4-dim subspace) on 2^18 rotated residuals.
-    The model is an INPUT of the index; parity is given the index."""
-    import torch
-
-    dev = torch.device("cuda")
-    X = datagen.mixture_torch(cfg.mix, n_learn, seed=SEED * 1000 + 999, centre_seed=CORPUS,
-                              stream=datagen.STREAM_LEARN, device=dev)
-    g = torch.Generator(device="cpu").manual_seed(seed)
-    C = X[torch.randperm(n_learn, generator=g)[: cfg.K].to(dev)].clone()
-    for _ in range(iters):
-        lab = assign_tensor_core(X, C)
-        cnt = torch.bincount(lab, minlength=cfg.K)
-        S = torch.zeros((cfg.K, cfg.mix.d), dtype=torch.float64, device=dev)
-        S.index_add_(0, lab, X.double())
-        newC = (S / cnt.clamp(min=1).unsqueeze(1).double()).float()
-        empty = (cnt == 0).nonzero().flatten()
-        if empty.numel():
-            pick = torch.randperm(n_learn, generator=g)[: empty.numel()].to(dev)
-            newC[empty] = X[pick]
-        C = newC
-    rot = np.load(BENCH_DATA / cfg.rotation_file)
-    Rt = torch.from_numpy(rot).to(dev)
-    lab = assign_tensor_core(X[:pq_learn], C)
-    Y = (X[:pq_learn] - C[lab]) @ Rt.t()
-    m, dsub = cfg.m, cfg.mix.d // cfg.m
-    Ys = Y.view(pq_learn, m, dsub).transpose(0, 1).contiguous()  # (m, n, dsub)
-    idx = torch.randperm(pq_learn, generator=g)[:16].to(dev)
-    cb = Ys[:, idx, :].clone()  # (m, 16, dsub)
-    for _ in range(pq_iters):
-        d2 = ((Ys[:, :, None, :] - cb[:, None, :, :]) ** 2).sum(-1)  # (m, n, 16)
-        a = d2.argmin(-1)
-        oh = torch.nn.functional.one_hot(a, 16).float()  # (m, n, 16)
-        cnt = oh.sum(1)  # (m, 16)
-        sums = torch.bmm(oh.transpose(1, 2), Ys)  # (m, 16, dsub)
-        cb = torch.where(cnt.unsqueeze(-1) > 0, sums / cnt.clamp(min=1).unsqueeze(-1), cb)
-    del X, Y, Ys
-    pq = _PQ(cb.cpu().numpy().astype(np.float32), rot)
-    return pq, C.cpu().numpy().astype(np.float32)
 
 
 def _sorted_rows(codes, labels, ids, K):
