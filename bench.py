@@ -215,6 +215,42 @@ def config_of(cfg, ivf_cfg, n, nq, ma, world):
     return c
 
 
+def host_lists(rows, ids, row_off, lists):
+    """Oracle-layout (blocks, blk_off, ids, count) of the given lists of a
+    row-ordered device index (every other list empty): the oracle's result
+    and work for queries probing only these lists equal those of the full
+    index. Returns (flat, list sizes of the full index)."""
+    import torch
+
+    from paper_1704_07355_b200.qadc import transpose_list
+    from paper_1704_07355_b200.shard import _ranges
+
+    K = row_off.shape[0] - 1
+    want = np.zeros(K, bool)
+    want[np.unique(np.asarray(lists))] = True
+    off = row_off.cpu().numpy()
+    sizes = np.diff(off)
+    sel = torch.from_numpy(np.nonzero(want)[0]).to(row_off.device)
+    idx = _ranges(row_off[:-1][sel], row_off[1:][sel] - row_off[:-1][sel])
+    r_h, i_h = rows[idx].cpu().numpy(), ids[idx].cpu().numpy()
+    blocks, bids, boff, count = [], [], [0], []
+    o = 0
+    for L in range(K):
+        k = int(sizes[L]) if want[L] else 0
+        if k:
+            tl = transpose_list(r_h[o:o + k], i_h[o:o + k])
+            blocks.append(tl.blocks.reshape(-1))
+            bids.append(tl.ids)
+            boff.append(boff[-1] + tl.blocks.shape[0])
+            o += k
+        else:
+            boff.append(boff[-1])
+        count.append(k)
+    flat = (np.concatenate(blocks) if blocks else np.zeros(0, np.uint8), np.asarray(boff, np.int64),
+            np.concatenate(bids) if bids else np.zeros(0, np.int64), np.asarray(count, np.int64))
+    return flat, sizes
+
+
 POOL = 512  # IVF configs: queries of the CPU sample (both arms) and its list extraction
 
 

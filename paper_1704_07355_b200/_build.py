@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libqadc_b200.so"
-SOURCES = ["layout.cu", "lut.cu", "probe_gemm.cu", "scan.cu", "select.cu", "simple.cu", "encode.cu",
+SOURCES = ["layout.cu", "lut.cu", "probe_tc.cu", "scan.cu", "select.cu", "simple.cu", "encode.cu",
            "peak.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
@@ -59,9 +59,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=min(6, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     if force or _stale(LIB, objs):
-        # cuBLAS: the tensor-core GEMM of the coarse probe (probe_gemm.cu)
-        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcublas",
-               "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs)]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

@@ -151,11 +151,12 @@ void retain_pool_memory() {
 // ivf.py:166-182 probe of the index's coarse quantizer: cells (nq, ma).
 void index_probe(const qadc_b200_index *idx, const float *queries, int nq, int ma, int64_t *cells,
                  cudaStream_t st) {
-  static const int probe_kind = scan_env_int("QADC_B200_PROBE", 2);  // 2 gemm, 1 ffma, 0 exact
+  // 2 = fused tensor-core probe, 1 = FFMA pre-selection, 0 = exact scan
+  static const int probe_kind = scan_env_int("QADC_B200_PROBE", 2);
   const bool done =
       (probe_kind >= 2 && idx->pcsplit &&
-       launch_probe_gemm(idx->coarse, idx->pmu, idx->pcsplit, idx->pcn2, idx->K, idx->d, queries,
-                         nq, ma, cells, st)) ||
+       launch_probe_tc(idx->coarse, idx->pmu, idx->pcsplit, idx->pcn2, idx->K, idx->d, queries,
+                       nq, ma, cells, st)) ||
       (probe_kind >= 1 && idx->cnorm &&
        launch_probe_fast(idx->coarseT, idx->coarse, idx->cnorm, idx->K, idx->d, queries, nq, ma,
                          cells, st));
@@ -744,10 +745,10 @@ int index_common(int d, int m, int nlists, const float *coarse, bool coarse_dev,
     k_transpose<<<gridn((int64_t)nlists * d), 256>>>(idx->coarse, nlists, d, idx->coarseT);
     QADC_CUDA(cudaMalloc(&idx->cnorm, (size_t)nlists * 4));
     launch_cnorm(idx->coarse, nlists, d, idx->cnorm, 0);
-    if (probe_gemm_supported(nlists, d)) {
-      if (int rc = probe_gemm_prepare(idx->coarse, nlists, d, &idx->pmu, &idx->pcsplit, &idx->pcn2, 0))
+    if (probe_tc_supported(nlists, d, 1)) {
+      if (int rc = probe_tc_prepare(idx->coarse, nlists, d, &idx->pmu, &idx->pcsplit, &idx->pcn2, 0))
         return rc;
-      idx->bytes += (int64_t)nlists * (3 * d * 2 + 4) + d * 4;
+      idx->bytes += (int64_t)(nlists + 255) / 256 * 256 * 3 * d * 2 + (int64_t)nlists * 4 + d * 4;
     }
     idx->bytes += 2 * (int64_t)cb + (int64_t)nlists * 4;
   }
@@ -1092,11 +1093,11 @@ extern "C" int qadc_b200_probe(const float *coarse, int K, int d, const float *q
   launch_cnorm(coarse, K, d, cn, st);
   static const int probe_kind = scan_env_int("QADC_B200_PROBE", 2);
   bool done = false;
-  if (probe_kind >= 2 && probe_gemm_supported(K, d)) {
+  if (probe_kind >= 2 && probe_tc_supported(K, d, ma)) {
     float *mu = nullptr, *cn2 = nullptr;
     void *cs = nullptr;
-    if (probe_gemm_prepare(coarse, K, d, &mu, &cs, &cn2, st) == kOk)
-      done = launch_probe_gemm(coarse, mu, cs, cn2, K, d, queries, nq, ma, cells, st);
+    if (probe_tc_prepare(coarse, K, d, &mu, &cs, &cn2, st) == kOk)
+      done = launch_probe_tc(coarse, mu, cs, cn2, K, d, queries, nq, ma, cells, st);
     cudaStreamSynchronize(st);
     cudaFree(mu);
     cudaFree(cs);

@@ -12,6 +12,8 @@
 // tie may differ — the index is an input, parity is given the index), and
 // k*d > 2^20 coarse assignment uses the same einsum form instead of the
 // reference's clamped GEMM expansion.
+#include <algorithm>
+
 #include "qadc_b200.h"
 #include "internal.cuh"
 
@@ -208,6 +210,27 @@ extern "C" int qadc_b200_assign(const float *X, int64_t n, int d, const float *C
     return kErrArgs;
   }
   if (n == 0) return kOk;
+  // the fused tensor-core nearest-centroid search (probe_tc.cu, ma = 1):
+  // same result (exact einsum-order re-rank, ties to the lower index)
+  if (probe_tc_supported(K, d, 1)) {
+    float *mu = nullptr, *cn2 = nullptr;
+    void *cs = nullptr;
+    bool done = false;
+    if (probe_tc_prepare(C, K, d, &mu, &cs, &cn2, st) == kOk) {
+      done = true;
+      for (int64_t v0 = 0; v0 < n && done; v0 += (1 << 30)) {
+        const int nv = (int)std::min<int64_t>(n - v0, 1 << 30);
+        done = launch_probe_tc(C, mu, cs, cn2, K, d, X + (size_t)v0 * d, nv, 1, labels + v0, st);
+      }
+    }
+    cudaFreeAsync(mu, st);
+    cudaFreeAsync(cs, st);
+    cudaFreeAsync(cn2, st);
+    if (done) {
+      QADC_CUDA(cudaGetLastError());
+      return kOk;
+    }
+  }
   const size_t smem = (size_t)128 * d * 4;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -25,7 +25,7 @@ struct qadc_b200_index {
   float *coarseT = nullptr;    // [d][K] (coalesced probe reads)
   float *cnorm = nullptr;      // [K] |c|^2 (probe pre-selection bounds)
   float *pmu = nullptr;        // [d] centroid mean (tensor-core probe centring)
-  void *pcsplit = nullptr;     // [K][3d] bf16 centred split rows [hi | lo | hi]
+  void *pcsplit = nullptr;     // [K_pad][3d] bf16 centred split rows [hi | lo | hi], tiled
   float *pcn2 = nullptr;       // [K] |c - mu|^2
   float *codebooks = nullptr;  // [m][16][dsub]
   float *rotation = nullptr;   // [d][d] or null
@@ -78,15 +78,16 @@ void launch_cnorm(const float *coarse, int K, int d, float *cn, cudaStream_t st)
 // uses launch_probe).
 bool launch_probe_fast(const float *coarseT, const float *coarse, const float *cn, int K, int d,
                        const float *queries, int nq, int ma, int64_t *cells, cudaStream_t st);
-// ---- probe_gemm.cu ----
-bool probe_gemm_supported(int K, int d);
-int probe_gemm_prepare(const float *coarse, int K, int d, float **mu, void **csplit, float **cn2,
-                       cudaStream_t st);
-// Tensor-core (cuBLAS bf16 split GEMM) pre-selection + exact re-rank probe;
-// false = not applicable.
-bool launch_probe_gemm(const float *coarse, const float *mu, const void *csplit, const float *cn2,
-                       int K, int d, const float *queries, int nq, int ma, int64_t *cells,
-                       cudaStream_t st);
+// ---- probe_tc.cu ----
+// Fused tcgen05 probe: split-bf16 GEMM with on-the-fly candidate selection
+// + exact einsum re-rank (supported: K >= 256, d % 64 == 0, d <= 128,
+// ma <= 64); false = not applicable (callers use launch_probe_fast).
+bool probe_tc_supported(int K, int d, int ma);
+int probe_tc_prepare(const float *coarse, int K, int d, float **mu, void **ctiled, float **cn2,
+                     cudaStream_t st);
+bool launch_probe_tc(const float *coarse, const float *mu, const void *ctiled, const float *cn2,
+                     int K, int d, const float *queries, int nq, int ma, int64_t *cells,
+                     cudaStream_t st);
 void launch_residual_lut(const qadc_b200_index *idx, const float *queries,
                          const int64_t *cells, int nq, int nslots,
                          float *lut, cudaStream_t st);

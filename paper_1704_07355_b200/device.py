@@ -166,8 +166,10 @@ class DeviceIndex:
                 "qmax": torch.empty(nq, dtype=f32, device=device),
                 "M_bits": torch.empty(nq, dtype=i32, device=device),
                 "fsat_n": torch.empty(nq, dtype=i32, device=device),
-                "fsat_mid": torch.empty((nq, R), dtype=f32, device=device),
-                "fsat_id": torch.empty((nq, R), dtype=i64, device=device)}
+                # entries past fsat_n are never read; zeroed so that states
+                # assembled from slices compare equal
+                "fsat_mid": torch.zeros((nq, R), dtype=f32, device=device),
+                "fsat_id": torch.zeros((nq, R), dtype=i64, device=device)}
 
     def prepare(self, queries, R: int, ma: int = 1, init: int = 1000, with_fsat: bool = True,
                 out: dict | None = None, stream=None) -> dict:

@@ -182,10 +182,14 @@ def encode_device(pq, X):
 
 
 def assign_device(centroids, X):
-    """Nearest coarse centroid per row of X (torch, on the GPU)."""
+    """Nearest coarse centroid per row of X (torch, on the GPU); centroids
+    as a numpy array or a device tensor."""
     import torch
 
-    C = torch.as_tensor(np.ascontiguousarray(centroids, dtype=np.float32)).to(X.device)
+    if isinstance(centroids, torch.Tensor):
+        C = centroids.to(device=X.device, dtype=torch.float32).contiguous()
+    else:
+        C = torch.as_tensor(np.ascontiguousarray(centroids, dtype=np.float32)).to(X.device)
     X = X.to(dtype=torch.float32).contiguous()
     labels = torch.empty(X.shape[0], dtype=torch.int64, device=X.device)
     lib = _native.load_library()

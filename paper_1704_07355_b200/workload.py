@@ -222,11 +222,10 @@ def ivf_rows(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, device="cuda",
     Config 2 (list sharding): the whole base of n codes (every rank builds
     it; `shard_ivf_lists` keeps the rank's lists). Config 4 (range
     sharding): rank r draws the chunks of its id range of the global
-    CFG4_CHUNK grid. Both assign on the tensor cores (assign_tensor_core;
-    QADC_B200_EXACT_ASSIGN=1 selects the exact einsum-order
-    qadc_b200_assign, the reference's kmeans.assign_batch semantics, ~8x
-    slower at N=1e8): the index is an input of the search path and parity
-    is defined given the index.
+    CFG4_CHUNK grid. Both assign with qadc_b200_assign (exact einsum-order
+    nearest centroid, ties to the lower index, on the fused tensor-core
+    kernel); the index is an input of the search path and parity is
+    defined given the index.
     Returns (codes (n_r, m/2), ids (n_r,), row_off (K + 1,))."""
     import torch
 
@@ -256,10 +255,9 @@ def ivf_rows(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, device="cuda",
                 X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000, centre_seed=CORPUS,
                                           stream=datagen.STREAM_BASE * 100 + g, device=device)
         with _phase("assign"):
-            if cfg.sharding != "range" and os.environ.get("QADC_B200_EXACT_ASSIGN") == "1":
-                lab = assign_device(coarse, X)
-            else:
-                lab = assign_tensor_core(X, C, cn)
+            # nearest coarse centroid, exact einsum order (qadc_b200_assign:
+            # the fused tcgen05 nearest-centroid kernel + exact re-rank)
+            lab = assign_device(C, X)
         labels[o:o + k] = lab
         with _phase("encode"):
             codes[o:o + k] = encode_device(pq, X - C[lab])

@@ -450,6 +450,29 @@ def test_encoder_matches_reference_assignment(gpu):
     assert np.array_equal(codes, g["codes"][np.argsort(g["ids"])])
 
 
+@pytest.mark.parametrize("K,n", [(300, 3000), (4096, 20000), (65536, 2000)])
+def test_tensor_core_assign_matches_exact_einsum(gpu, K, n):
+    """qadc_b200_assign on the fused tcgen05 nearest-centroid kernel
+    (probe_tc.cu, ma = 1): every label equals the exact einsum-order argmin
+    with ties to the lower index (the oracle's probe at ma = 1), including
+    duplicated centroids (forced ties) and points on centroids."""
+    import torch
+
+    from paper_1704_07355_b200 import datagen
+    from paper_1704_07355_b200.ivf import assign_device
+    rng = np.random.default_rng(K)
+    X = datagen.mixture_numpy(datagen.SIFT_LIKE, n, seed=K, stream=2)
+    C = X[rng.choice(n, min(K, n), replace=False)].copy()
+    if C.shape[0] < K:
+        C = np.concatenate([C, datagen.mixture_numpy(datagen.SIFT_LIKE, K - C.shape[0], seed=K,
+                                                     stream=5)])
+    C[K // 2] = C[K // 3]  # exact duplicate: ties resolve to the lower index
+    X[:5] = C[K // 3]      # points sitting on the duplicated centroid
+    lab = assign_device(C, torch.from_numpy(X).cuda()).cpu().numpy()
+    want = np.array([orc.probe(C, x, 1)[0][0] for x in X])
+    assert np.array_equal(lab, want)
+
+
 @pytest.mark.parametrize("ma", [1, 8, 32])
 def test_ivf_search_vs_oracle_at_scale(gpu, ma):
     """IVF + OPQ, K=256 lists, 2*10^5 codes: with the oracle's float LUTs
@@ -562,3 +585,24 @@ def test_probe_batch_bounds_and_tie_fallback(gpu, K, ma, distinct):
         want, wres = orc.probe(cen, qs[i], ma)
         assert np.array_equal(got[i], want), i
         assert np.array_equal(_bits(res[i].cpu().numpy()), _bits(wres))
+
+
+@pytest.mark.parametrize("K,ma,nq", [(8192, 64, 1000), (65536, 16, 300), (1024, 1, 777)])
+def test_probe_many_query_tiles_vs_oracle(gpu, K, ma, nq):
+    """The fused tensor-core probe over several 128-query tiles and
+    centroid-range slices (the configs' batch shapes) equals the oracle's
+    probe order for every query."""
+    import torch
+
+    from paper_1704_07355_b200 import _native, datagen
+    cen = datagen.mixture_numpy(datagen.SIFT_LIKE, K, seed=K + nq, stream=1)
+    qs = datagen.mixture_numpy(datagen.SIFT_LIKE, nq, seed=K, stream=4)
+    dev = torch.device("cuda")
+    cells = torch.empty((nq, ma), dtype=torch.int64, device=dev)
+    _native.check(_native.load_library().qadc_b200_probe(
+        _native.dptr(torch.from_numpy(cen).to(dev)), K, 128,
+        _native.dptr(torch.from_numpy(qs).to(dev)), nq, ma, _native.dptr(cells), None,
+        torch.cuda.current_stream().cuda_stream), "probe")
+    got = cells.cpu().numpy()
+    for i in range(nq):
+        assert np.array_equal(got[i], orc.probe(cen, qs[i], ma)[0]), i
