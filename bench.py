@@ -31,9 +31,14 @@ same query sample scheme, all host threads.
 
 from __future__ import annotations
 
+import os
+
+# the stock reference's numpy runs single-threaded per worker process
+# (one process per core, OPENBLAS_NUM_THREADS=1)
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
 import argparse
 import json
-import os
 import statistics
 import subprocess
 import sys
@@ -251,6 +256,138 @@ def host_lists(rows, ids, row_off, lists):
     return flat, sizes
 
 
+# ---------------------------------------------------------------- stock reference
+
+STOCK = ROOT / "baseline" / "_ref"  # pip install --target of /root/reference/pkg (git-ignored)
+
+
+def stock_reference():
+    """The UNMODIFIED reference package (`qadc`, installed by
+    `pip install --no-index --no-build-isolation --no-deps --target
+    baseline/_ref /root/reference/pkg`), or None if it is not installed."""
+    if not (STOCK / "qadc").exists():
+        return None
+    if str(STOCK) not in sys.path:
+        sys.path.insert(0, str(STOCK))
+    try:
+        import qadc
+        from qadc import kernels
+        if not kernels.have_extension():
+            return None
+        return qadc
+    except Exception:
+        return None
+
+
+def stock_index(coarse, m, d, rows, ids, row_off, lists):
+    """A reference IvfIndex (transposed16 layout) holding the given lists of
+    a row-ordered device index (every other list empty); flat when coarse
+    is None."""
+    from qadc import ivf, kmeans
+    from qadc import qadc as rq
+
+    off = row_off.cpu().numpy()
+    K = off.shape[0] - 1
+    want = np.zeros(K, bool)
+    want[np.unique(np.asarray(lists))] = True
+    empty = rq.transpose_list(np.zeros((0, m // 2), np.uint8), np.zeros(0, np.int64))
+    out = []
+    for L in range(K):
+        a, b = int(off[L]), int(off[L + 1])
+        if want[L] and b > a:
+            out.append(rq.transpose_list(rows[a:b].cpu().numpy(), ids[a:b].cpu().numpy()))
+        else:
+            out.append(empty)
+    cb = None if coarse is None else kmeans.Codebook(np.ascontiguousarray(coarse, np.float32))
+    return ivf.IvfIndex(d=d, m=m, b=4, coarse=cb, lists=out, layout=ivf.LAYOUT_TRANSPOSED)
+
+
+_STOCK = {}
+
+
+def _stock_worker(task):
+    from qadc import adc
+    idx, pq, R, ma, init = (_STOCK[k] for k in ("index", "pq", "R", "ma", "init"))
+    lo, qs = task
+    out = []
+    for q in qs:
+        r = adc.search(idx, pq, q, R=R, ma=ma, method="qadc", init=init, variant="simd256")
+        out.append((r.ids, r.distances))
+    return lo, out
+
+
+def stock_pool(ref_index, codebooks, rotation, R, ma, init, nq):
+    """A fork pool of one worker process per core (at most nq) sharing the
+    reference index copy-on-write; returns (pool, pq, procs)."""
+    import multiprocessing as mp
+
+    from qadc import pq as rpq
+    pq = rpq.ProductQuantizer(m=codebooks.shape[0], b=4, codebooks=codebooks, rotation=rotation)
+    procs = max(1, min(os.cpu_count() or 1, nq))
+    _STOCK.update(index=ref_index, pq=pq, R=R, ma=ma, init=init)
+    return mp.get_context("fork").Pool(procs), pq, procs
+
+
+def stock_all_cores(pool, procs, qs, R):
+    """One pass of the stock adc.search over qs on the worker pool (disjoint
+    contiguous slices); returns (wall seconds, ids, dists padded to R)."""
+    per = -(-qs.shape[0] // procs)
+    tasks = [(i, qs[i:i + per]) for i in range(0, qs.shape[0], per)]
+    t0 = time.perf_counter()
+    parts = pool.map(_stock_worker, tasks)
+    wall = time.perf_counter() - t0
+    ri = np.full((qs.shape[0], R), -1, np.int64)
+    rd = np.full((qs.shape[0], R), np.inf, np.float32)
+    for lo, out in parts:
+        for j, (i_, d_) in enumerate(out):
+            ri[lo + j, : i_.shape[0]] = i_
+            rd[lo + j, : d_.shape[0]] = d_
+    return wall, ri, rd
+
+
+def stock_single_core(ref_index, pq, qs, R, ma, init, codes_per_query):
+    """The stock adc.search sequentially on one core with the reference's
+    own Index / Tables / Scan phase times (bench.py:176-192)."""
+    from qadc import adc
+    ph = np.zeros(3)
+    t0 = time.perf_counter()
+    for q in qs:
+        r = adc.search(ref_index, pq, q, R=R, ma=ma, method="qadc", init=init, variant="simd256")
+        ph += (r.timings.index_ms, r.timings.tables_ms, r.timings.scan_ms)
+    wall = time.perf_counter() - t0
+    n = qs.shape[0]
+    return {"queries": n, "qps": n / wall,
+            "codes_per_s": float(np.sum(codes_per_query[:n])) / wall,
+            "index_ms": round(ph[0] / n, 3), "tables_ms": round(ph[1] / n, 3),
+            "scan_ms": round(ph[2] / n, 3), "total_ms": round(wall * 1e3 / n, 3)}
+
+
+def stock_baseline(ref_index, codebooks, rotation, qs_single, qs_all, R, ma, init,
+                   codes_per_query, seconds):
+    """SURVEY 8d CPU baseline with the stock reference: single-core phases
+    and all-core throughput (one process per core, passes repeated for
+    about `seconds`). Returns (cpu_baseline dict, all-core results)."""
+    pool, pq, procs = stock_pool(ref_index, codebooks, rotation, R, ma, init, qs_all.shape[0])
+    try:
+        single = stock_single_core(ref_index, pq, qs_single, R, ma, init, codes_per_query)
+        walls, res = [], None
+        t_end = time.perf_counter() + seconds
+        while True:
+            w, ri, rd = stock_all_cores(pool, procs, qs_all, R)
+            walls.append(w)
+            res = (ri, rd)
+            if time.perf_counter() >= t_end:
+                break
+    finally:
+        pool.close()
+        pool.join()
+    wall = statistics.median(walls)
+    codes = float(np.sum(codes_per_query[: qs_all.shape[0]]))
+    return {"value": codes / wall, "unit": UNIT, "cores": procs, "kind": "reference",
+            "qps": qs_all.shape[0] / wall, "passes": len(walls),
+            "single_core": single}, res
+
+
 POOL = 512  # IVF configs: queries of the CPU sample (both arms) and its list extraction
 
 
@@ -358,24 +495,17 @@ def ivf_parity(index, pq, coarse, flat, pool, R, init, ma, gpu_i, gpu_d, cpu_res
 def measure_recall(cfg, pq, n, qs, ids, codes=None):
     """R@{1,10,100} (reference bench.py:110-122) against exact float64
     nearest neighbours of the same GPU-drawn base (regenerated chunk by
-    chunk with the shard generator's seeds). For a flat index (`codes`
-    given) the float-table ADC top-100 of the same codes is measured too,
-    so the quantized-table recall loss (the paper's QADC vs ADC figure)
-    sits beside it."""
+    chunk with the build's seeds, recall.ground_truth = synth.py:45-70's
+    definition). For a flat index (`codes` given) the float-table ADC
+    top-100 of the same codes is measured too, so the quantized-table
+    recall loss (the paper's QADC vs ADC figure) sits beside it."""
     import torch
 
-    from paper_1704_07355_b200 import datagen
     from paper_1704_07355_b200.adc import compute_tables
     from paper_1704_07355_b200.recall import ground_truth, recall_at
-    from paper_1704_07355_b200.workload import CORPUS, SEED
+    from paper_1704_07355_b200.workload import base_chunks
 
-    def chunks():
-        step = 4 * datagen.CHUNK
-        for c0 in range(0, n, step):
-            k = min(step, n - c0)
-            yield c0, datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000, centre_seed=CORPUS,
-                                            stream=datagen.STREAM_BASE * 100 + c0 // step)
-    gt = ground_truth(chunks(), qs, depth=1)[:, 0]
+    gt = ground_truth(base_chunks(cfg, n), qs, depth=1)[:, 0]
     out = {f"R@{r}": recall_at(ids, gt, r) for r in (1, 10, 100)}
     if codes is not None:
         T = torch.from_numpy(np.stack([compute_tables(pq, q).tables for q in qs])).cuda()
@@ -398,8 +528,6 @@ def measure_recall(cfg, pq, n, qs, ids, codes=None):
         out["adc_float"] = {f"R@{r}": recall_at(fi, gt, r) for r in (1, 10, 100)}
     return out | {"queries": int(qs.shape[0])}
 
-
-# ---------------------------------------------------------------- arms
 
 def run_b200(args):
     import torch
@@ -616,6 +744,8 @@ def run_b200(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_host"] = host_info()
+            from oracle import parity
+            gi_np, gd_np = out_i.numpy(), out_d.numpy()
             if ivf_cfg is not None:
                 pool = qs[: min(POOL, nq)]
                 t = index.tables(torch.from_numpy(pool).cuda(), R, ma=ma, init=init)
@@ -623,10 +753,25 @@ def run_b200(args):
                 flat, sizes = host_lists(rows, row_ids, row_off, cells)
                 cb_res, cpu_res = cpu_reference_run_ivf(pq, coarse, flat, sizes, pool, cells, R,
                                                         init, ma, args.cpu_seconds, nq)
-                out["cpu_baseline"] = cb_res
-                out["parity"] = ivf_parity(index, pq, coarse, flat, pool, R, init, ma,
-                                           out_i.numpy(), out_d.numpy(), cpu_res,
-                                           args.parity_queries)
+                out["parity"] = ivf_parity(index, pq, coarse, flat, pool, R, init, ma, gi_np,
+                                           gd_np, cpu_res, args.parity_queries)
+                codes_pq = sizes[cells].sum(1)
+                if stock_reference() is not None:
+                    ref_index = stock_index(coarse, pq.m, pq.d, rows, row_ids, row_off, cells)
+                    n1, na = min(16, pool.shape[0]), min(256, pool.shape[0])
+                    st_res, (si, sd) = stock_baseline(ref_index, pq.codebooks, pq.rotation,
+                                                      pool[:n1], pool[:na], R, ma, init, codes_pq,
+                                                      args.cpu_seconds / 2)
+                    st_res["sample"] = (f"{na} of {nq} queries (single core: {n1}), nprobe={ma}, "
+                                        "over the lists they probe of the full index: the stock "
+                                        "reference package (baseline/_ref) adc.search(method="
+                                        "'qadc', variant='simd256'), one process per core")
+                    st_res["restated_kernels"] = cb_res
+                    out["cpu_baseline"] = st_res
+                    out["parity"]["vs_stock_reference"] = parity.compare_results(
+                        gi_np[:na], gd_np[:na], si, sd)
+                else:
+                    out["cpu_baseline"] = cb_res
             else:
                 from paper_1704_07355_b200.qadc import transpose_list
                 tl = transpose_list(codes.cpu().numpy(), np.arange(n, dtype=np.int64))
@@ -634,10 +779,26 @@ def run_b200(args):
                         tl.ids, np.array([n], np.int64))
                 cb_res, (oi, od, on), k = cpu_reference_run(pq.codebooks, flat, n, qs, R, init,
                                                             args.cpu_seconds)
-                out["cpu_baseline"] = cb_res
-                from oracle import parity
                 out["parity"] = {"vs_cpu_reference": parity.compare_results(
-                    out_i.numpy()[:k], out_d.numpy()[:k], oi, od)}
+                    gi_np[:k], gd_np[:k], oi, od)}
+                if stock_reference() is not None:
+                    ids_d = torch.arange(n, dtype=torch.int64)
+                    ref_index = stock_index(None, pq.m, pq.d, codes, ids_d,
+                                            torch.tensor([0, n]), [0])
+                    n1, na = min(4, nq), min(64, nq)
+                    st_res, (si, sd) = stock_baseline(ref_index, pq.codebooks, None, qs[:n1],
+                                                      qs[:na], R, 1, init, np.full(nq, n),
+                                                      args.cpu_seconds / 2)
+                    st_res["sample"] = (f"{na} of {nq} queries (single core: {n1}) over the full "
+                                        f"N={n} index: the stock reference package "
+                                        "(baseline/_ref) adc.search(method='qadc', "
+                                        "variant='simd256'), one process per core")
+                    st_res["restated_kernels"] = cb_res
+                    out["cpu_baseline"] = st_res
+                    out["parity"]["vs_stock_reference"] = parity.compare_results(
+                        gi_np[:na], gd_np[:na], si, sd)
+                else:
+                    out["cpu_baseline"] = cb_res
     if out is not None and args.recall and world == 1:
         out["recall"] = measure_recall(cfg, pq, n, qs[: args.recall], out_i.numpy()[: args.recall],
                                        codes=None if ivf_cfg is not None else codes)
@@ -647,12 +808,15 @@ def run_b200(args):
 
 
 def run_reference(args):
-    """CPU reference arm: the reference's compiled qadc_scan_u8 (oracle/_ref)
-    driven by the restated adc.search orchestration (oracle/), all host
-    threads, on a bounded query sample per step. The index is built in
-    plain torch on the GPU (workload.ivf_rows_torch / encode_torch): no
-    product kernel runs, and libqadc_b200.so is never loaded, in this
-    process. Rank 0 only."""
+    """CPU reference arm, rank 0 only: the stock reference package
+    (baseline/_ref: `pip install --no-deps --target` of /root/reference/pkg)
+    running its own adc.search(method="qadc", variant="simd256"), one
+    process per host core, on a bounded query sample per step (the
+    restated orchestration with the reference's compiled scan kernels,
+    oracle/ + oracle/_ref, if the stock package is absent). The index is
+    built in plain torch on the GPU (workload.ivf_rows_torch /
+    encode_torch): no product kernel runs, and libqadc_b200.so is never
+    loaded, in this process."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
@@ -673,64 +837,86 @@ def run_reference(args):
     qs = queries(cfg, nq)
     nthreads = os.cpu_count() or 1
     use_ref = orc.ref_lib() is not None
+    stock = stock_reference() is not None
     t_build = time.perf_counter()
     if ivf_cfg is not None:
         pq, coarse = load_ivf_model(ivf_cfg)
-        pool = qs[: min(POOL, nq)]
+        rot = pq.rotation
+        sample = qs[: min(256 if stock else POOL, nq)]
         from concurrent.futures import ThreadPoolExecutor
         with ThreadPoolExecutor(nthreads) as ex:
-            cells = np.stack(list(ex.map(lambda q: orc.probe(coarse, q, ma)[0], pool)))
+            cells = np.stack(list(ex.map(lambda q: orc.probe(coarse, q, ma)[0], sample)))
         keep = np.zeros(ivf_cfg.K, bool)
         keep[np.unique(cells)] = True
         rows, row_ids, row_off = ivf_rows_torch(ivf_cfg, pq, coarse, n, keep)
-        flat, sizes = host_lists(rows, row_ids, row_off, cells)
-        del rows, row_ids
-        codes = int(sizes[cells].sum())
-        desc = (f"{pool.shape[0]} of {nq} queries, nprobe={ma}, over the lists they probe of "
+        sizes = np.diff(row_off.cpu().numpy())
+        codes_pq = sizes[cells].sum(1)
+        what = (f"{sample.shape[0]} of {nq} queries, nprobe={ma}, over the lists they probe of "
                 f"the full N={n} index (built in plain torch)")
-
-        def one():
-            t0 = time.perf_counter()
-            orc.search_batch(pool, pq.codebooks, pq.rotation, coarse, ma, flat, cfg.R, cfg.init,
-                             use_ref_scan=use_ref, nthreads=nthreads)
-            return codes / (time.perf_counter() - t0), time.perf_counter() - t0
+        if stock:
+            ref_index = stock_index(coarse, pq.m, pq.d, rows, row_ids, row_off, cells)
+        else:
+            flat, _ = host_lists(rows, row_ids, row_off, cells)
+        del rows, row_ids
     else:
         pq = load_pq(cfg)
+        coarse, rot = None, None
         from paper_1704_07355_b200 import datagen
-        from paper_1704_07355_b200.qadc import transpose_list
         from paper_1704_07355_b200.workload import CORPUS, SEED
         parts = []
         for c0 in range(0, n, 4 * datagen.CHUNK):
             k = min(4 * datagen.CHUNK, n - c0)
             X = datagen.mixture_torch(cfg.mix, k, seed=SEED * 1000, centre_seed=CORPUS,
                                       stream=datagen.STREAM_BASE * 100 + c0 // (4 * datagen.CHUNK))
-            parts.append(encode_torch(pq, X).cpu().numpy())
-        tl = transpose_list(np.concatenate(parts), np.arange(n, dtype=np.int64))
-        flat = (tl.blocks.reshape(-1), np.array([0, tl.blocks.shape[0]], np.int64), tl.ids,
-                np.array([n], np.int64))
-        probe = qs[: max(1, min(nthreads, nq))]
-        t0 = time.perf_counter()
-        orc.search_batch(probe, pq.codebooks, None, None, 1, flat, cfg.R, cfg.init,
-                         use_ref_scan=use_ref, nthreads=nthreads)
-        per_q = (time.perf_counter() - t0) / probe.shape[0]
-        per_step = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
-        k = int(max(probe.shape[0], min(nq, per_step / max(per_q, 1e-6))))
-        sample = qs[:k]
-        desc = f"{k} of {nq} queries over the full N={n} index (encoded in plain torch)"
-
-        def one():
-            t0 = time.perf_counter()
-            orc.search_batch(sample, pq.codebooks, None, None, 1, flat, cfg.R, cfg.init,
-                             use_ref_scan=use_ref, nthreads=nthreads)
-            return k * n / (time.perf_counter() - t0), time.perf_counter() - t0
+            parts.append(encode_torch(pq, X).cpu())
+        codes_h = torch.cat(parts)
+        sample = qs[: min(64 if stock else nq, nq)]
+        codes_pq = np.full(nq, n)
+        what = f"{sample.shape[0]} of {nq} queries over the full N={n} index (encoded in plain torch)"
+        if stock:
+            ref_index = stock_index(None, pq.m, pq.d, codes_h, torch.arange(n), torch.tensor([0, n]),
+                                    [0])
+        else:
+            from paper_1704_07355_b200.qadc import transpose_list
+            tl = transpose_list(codes_h.numpy(), np.arange(n, dtype=np.int64))
+            flat = (tl.blocks.reshape(-1), np.array([0, tl.blocks.shape[0]], np.int64), tl.ids,
+                    np.array([n], np.int64))
     t_build = time.perf_counter() - t_build
+    codes = float(np.sum(codes_pq[: sample.shape[0]]))
     vals, walls = [], []
-    for i in range(args.warmup + args.steps):
-        v, w = one()
-        if i >= args.warmup:
-            vals.append(v)
-            walls.append(w)
+    if stock:
+        pool, spq, procs = stock_pool(ref_index, pq.codebooks, rot, cfg.R, ma, cfg.init,
+                                      sample.shape[0])
+        try:
+            for i in range(args.warmup + args.steps):
+                w, _, _ = stock_all_cores(pool, procs, sample, cfg.R)
+                if i >= args.warmup:
+                    vals.append(codes / w)
+                    walls.append(w)
+        finally:
+            pool.close()
+            pool.join()
+        single = stock_single_core(ref_index, spq, sample[: min(8, sample.shape[0])], cfg.R, ma,
+                                   cfg.init, codes_pq)
+        kind, cores = "reference", procs
+        desc = what + ("; the stock reference package (baseline/_ref) adc.search(method='qadc', "
+                       "variant='simd256'), one process per core")
+    else:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            orc.search_batch(sample, pq.codebooks, rot, coarse, ma, flat, cfg.R, cfg.init,
+                             use_ref_scan=use_ref, nthreads=nthreads)
+            w = time.perf_counter() - t0
+            if i >= args.warmup:
+                vals.append(codes / w)
+                walls.append(w)
+        single = None
+        kind, cores = ("reference" if use_ref else "port"), nthreads
+        desc = what + "; restated orchestration (oracle/) + the reference's compiled scan"
     value = statistics.median(vals)
+    cpu = {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc}
+    if single is not None:
+        cpu["single_core"] = single
     return {
         "impl": "reference", "metric": METRICS[args.config], "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -739,8 +925,7 @@ def run_reference(args):
         "data": "synthetic (BASELINE mixture generator, same seeds and model files as the B200 "
                 "arm; index built in plain torch)",
         "config": config_of(cfg, ivf_cfg, n, nq, ma, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads,
-                         "kind": "reference" if use_ref else "port", "sample": desc},
+        "cpu_baseline": cpu,
         "cpu_host": host_info(),
         "index_setup_s": round(t_build, 1),
         "product_library_loaded": _product_lib_mapped(),

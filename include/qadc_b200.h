@@ -262,6 +262,14 @@ QADC_API int qadc_b200_int_peak(double *out);
  * N=256, K=32 instructions, one CTA per SM) on this device. */
 QADC_API int qadc_b200_mma_peak(double *out);
 
+/* Diagnostics of the fused tensor-core probe (probe_tc.cu), device
+ * pointers: cells (nq, ma); S (128 x 256 fp32) = the raw split-bf16 dot
+ * products of the first CTA's first centroid tile; counts = [slices, then
+ * per-(slice, query) candidate counts]; mu_out (d) = the centring mean. */
+QADC_API int qadc_b200_debug_probe_tc(const float *coarse, int K, int d, const float *queries,
+                                      int nq, int ma, int64_t *cells, float *S, int *counts,
+                                      float *mu_out, void *stream);
+
 /* kmeans.py:52-78 assign_batch: nearest of K centroids (K, d) per row of
  * X (n, d), einsum-order distances, ties to the lowest index. */
 QADC_API int qadc_b200_assign(const float *X, int64_t n, int d, const float *C,

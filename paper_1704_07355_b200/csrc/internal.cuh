@@ -87,7 +87,7 @@ int probe_tc_prepare(const float *coarse, int K, int d, float **mu, void **ctile
                      cudaStream_t st);
 bool launch_probe_tc(const float *coarse, const float *mu, const void *ctiled, const float *cn2,
                      int K, int d, const float *queries, int nq, int ma, int64_t *cells,
-                     cudaStream_t st);
+                     cudaStream_t st, float *dbg_S = nullptr, int *dbg_counts = nullptr);
 void launch_residual_lut(const qadc_b200_index *idx, const float *queries,
                          const int64_t *cells, int nq, int nslots,
                          float *lut, cudaStream_t st);

@@ -33,9 +33,10 @@
 // HBM already in the canonical no-swizzle K-major core-matrix layout, so a
 // 16 / 32 KB block is one contiguous copy), warp 1 issues
 // tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = 256, K = 16; A resident
-// in shared memory for the whole CTA, B streamed through a 3-stage ring in
+// in shared memory for the whole CTA, B streamed through a 2-stage ring in
 // K-chunks of 64), warps 2-5 drain the double-buffered TMEM accumulator
-// (2 x 256 columns) with tcgen05.ld and run the selection.
+// (2 x 256 columns) with tcgen05.ld and run the selection (a per-query
+// max-heap of the kept U values in shared memory).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -49,7 +50,7 @@ namespace {
 constexpr int kNM = 128;          // queries per CTA (MMA M, TMEM lanes)
 constexpr int kNN = 256;          // centroids per tile (MMA N)
 constexpr int kNKC = 64;          // bf16 K elements per staged chunk (128-byte rows)
-constexpr int kNStages = 3;       // B ring depth
+constexpr int kNStages = 2;       // B ring depth (shared memory also holds the kept-set heaps)
 constexpr int kNMaxMa = 64;       // fused selection keeps <= 64 per query
 constexpr int kNThreads = 192;    // warp 0 copies, warp 1 MMA, warps 2-5 epilogue
 constexpr int kNABlock = kNM * kNKC * 2;  // 16 KB
@@ -73,9 +74,9 @@ __device__ __forceinline__ uint64_t nn_desc(uint32_t saddr) {
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\tNN_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@P1 bra NN_DONE;\n\tbra NN_WAIT;\n\tNN_DONE:\n\t}" ::"r"(mbar),
-      "r"(parity), "n"(1000000)
+      "r"(parity)
       : "memory");
 }
 
@@ -90,12 +91,23 @@ __device__ __forceinline__ void bulk_copy(uint32_t dst, const void *src, uint32_
 
 // Index / query side: centroid mean (fp64 accumulation), centred split-bf16
 // rows in the tiled layout (rows padded to RT with zeros), |v'|^2.
-__global__ void k_nn_mean(const float *__restrict__ C, int K, int d, float *__restrict__ mu) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= d) return;
+// One CTA per dimension: fp64 partial sums over strided rows, then a
+// block reduction (the serial per-dimension loop took ms at K = 65536).
+__global__ void __launch_bounds__(256) k_nn_mean(const float *__restrict__ C, int K, int d,
+                                                 float *__restrict__ mu) {
+  __shared__ double part[8];
+  const int t = blockIdx.x;
   double s = 0.0;
-  for (int k = 0; k < K; k++) s += (double)C[(size_t)k * d + t];
-  mu[t] = (float)(s / K);
+  for (int k = threadIdx.x; k < K; k += blockDim.x) s += (double)C[(size_t)k * d + t];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < 8; w++) tot += part[w];
+    mu[t] = (float)(tot / K);
+  }
 }
 
 // One warp per row r < n_pad. coarse rows [hi | lo | hi], query rows
@@ -131,6 +143,14 @@ __global__ void k_nn_split(const float *__restrict__ V, int64_t n, int64_t n_pad
   if (lane == 0 && r < n) n2[r] = (float)acc;
 }
 
+// Pre-filter cell term: c2p = c2 (1 - e) rounded down (e = eps + 64u);
+// padded to a multiple of 32 cells with +huge (never passes).
+__global__ void k_nn_c2p(const float *__restrict__ c2, int K, int K_pad, float f,
+                         float *__restrict__ out) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K_pad; k += gridDim.x * blockDim.x)
+    out[k] = k < K ? __fmul_rd(c2[k], f) : 3.0e38f;
+}
+
 struct NnArgs {
   const uint8_t *qtiled;  // [q_tiles][nch][16 KB]
   const float *qn2;       // [nq]
@@ -141,6 +161,10 @@ struct NnArgs {
   uint64_t *cand;         // [slices][nq_pad][cap]  (A bits << 32 | cell)
   int *cand_n;            // [slices][nq_pad]  (> cap: overflow)
   float *tops;            // [slices][nq_pad][kNMaxMa]
+  float *dbg_S;           // diagnostics: raw dot products of CTA (0, 0), tile t0 ([128][256]) or null
+  unsigned *bound;        // [nq_pad] per-query bound shared by the slices (float bits, atomicMin)
+  const float *c2p;       // [K] c2 (1 - eps - 64u) rounded down: the pre-filter's cell term
+  float pre_q;            // 1 - eps - 64u (the pre-filter's query factor, see the epilogue)
 };
 
 __global__ void __launch_bounds__(kNThreads, 1) k_nn_tc(const __grid_constant__ NnArgs a) {
@@ -249,21 +273,36 @@ __global__ void __launch_bounds__(kNThreads, 1) k_nn_tc(const __grid_constant__ 
     }
   } else {
     // ---- epilogue: one thread per query (TMEM lane) ----
+    // Per batch of 32 cells: masks of candidates (L <= T) and of kept-set
+    // insertions (U < T) from one branch-free pass, then only the set bits
+    // are visited (a warp iterates as often as its busiest lane, not once
+    // per cell whenever any lane inserts). The kept set is a max-heap of
+    // ma values in shared memory, slot-major (bank = lane: conflict-free
+    // for any slot pattern); its root is T.
     const int quarter = w & 3;  // warps 2..5 -> lanes 64, 96, 0, 32
     const int row = quarter * 32 + lane;
     const int q = qtile * kNM + row;
     const bool live = q < a.nq;
     const float a2 = live ? a.qn2[q] : 0.f;
     const float onep = __fadd_ru(1.f, a.gam), onem = __fsub_rd(1.f, a.gam);
-    float set[kNMaxMa];
-#pragma unroll
-    for (int i = 0; i < kNMaxMa; i++) set[i] = i < a.ma ? __int_as_float(0x7f800000) : -1.f;
-    float T = __int_as_float(0x7f800000);
+    const int ma = a.ma;
+    float *heap = (float *)(sB + (size_t)kNStages * kNBBlock) + row;     // [ma][kNM]
+    float *stage = heap + (size_t)kNMaxMa * kNM;                           // [32][kNM] S
+    for (int i = 0; i < ma; i++) heap[i * kNM] = __int_as_float(0x7f800000);
+    float T = __int_as_float(0x7f800000);  // this slice's kept-set root
     int nc = 0;
     uint64_t *cand = a.cand + ((size_t)slice * a.nq_pad + (live ? q : 0)) * a.cap;
+    // The slices of a query share a bound Tg = min over slices of their
+    // kept-set roots (each >= U*, the global ma-th smallest U, so Tg >= U*):
+    // a cell is kept / emitted only below min(T, Tg). Slices later in the
+    // grid then start from an almost converged bound.
+    unsigned *gb = a.bound + (live ? q : 0);
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+    float Tg = __uint_as_float(*(volatile unsigned *)gb);
     for (int t = t0, j = 0; t < t1; t++, j++) {
       const int buf = j & 1;
+      // the shared bound is read once per tile, requested before the wait
+      const unsigned tg_next = *(volatile unsigned *)gb;
       mbar_wait(tfull_b(buf), (uint32_t)(j >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
@@ -282,44 +321,87 @@ __global__ void __launch_bounds__(kNThreads, 1) k_nn_tc(const __grid_constant__ 
             : "r"(trow + (uint32_t)(buf * kNN + b * 32)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int kb = t * kNN + b * 32;
+        if (a.dbg_S && qtile == 0 && slice == 0 && j == 0) {
 #pragma unroll
-        for (int i = 0; i < 32; i++) {
-          const int k = kb + i;
-          if (k >= a.K) break;  // warp-uniform (k does not depend on the lane)
-          const float c2 = __ldg(a.cn2 + k);
-          const float n2 = __fadd_ru(a2, c2);
-          const float A = __fmaf_rn(-2.f, __uint_as_float(v[i]), __fadd_rn(a2, c2));
-          const float mg = __fmul_ru(a.eps, n2);
-          const float L = fmaxf(__fmul_rd(__fsub_rd(A, mg), onem), 0.f);
-          if (L <= T && live) {
-            const float U = fmaxf(__fmul_ru(__fadd_ru(A, mg), onep), 0.f);
-            if (nc < a.cap) cand[nc] = ((uint64_t)__float_as_uint(A) << 32) | (uint32_t)k;
-            nc++;
-            if (U < T) {  // replace the current max of the kept set
-              bool done = false;
+          for (int i = 0; i < 32; i++) a.dbg_S[row * kNN + b * 32 + i] = __uint_as_float(v[i]);
+        }
+        // pass 1 (branch-free, ~4 instructions per cell): a conservative
+        // pre-filter that never rejects a cell with L <= Tu. With
+        // Y = fl(c2 (1 - e) - 2 S), e = eps + 64u, L <= Tu implies
+        //   Y <= Tu / (1 - g) - a2 (1 - e) + 64u (a2 + Tu)
+        // (A = a2 + c2 - 2 S and mg = eps (a2 + c2) up to rounding terms
+        // of size u (a2 + 2 c2), which the extra 64u on both sides cover:
+        // |S| <= (a2 + c2) / 2). Survivors get the exact L / U.
+        const int nk = min(32, a.K - kb);
+        const float Tu = fminf(T, Tg);
+        const float thr = __fadd_ru(__fadd_ru(__fdiv_ru(Tu, onem), -a.pre_q * a2),
+                                    __fmul_ru(3.9e-6f, __fadd_ru(a2, Tu)));
+        uint32_t pmask = 0;
+        const float4 *cp4 = (const float4 *)(a.c2p + kb);
 #pragma unroll
-              for (int s2 = 0; s2 < kNMaxMa; s2++) {
-                const bool hit = !done && set[s2] == T;
-                set[s2] = hit ? U : set[s2];
-                done |= hit;
-              }
-              float mx = set[0];
+        for (int i4 = 0; i4 < 8; i4++) {
+          const float4 c4 = __ldg(cp4 + i4);
+          const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
-              for (int s2 = 1; s2 < kNMaxMa; s2++) mx = fmaxf(mx, set[s2]);
-              T = mx;
-            }
+          for (int u = 0; u < 4; u++) {
+            const int i = 4 * i4 + u;
+            stage[i * kNM] = __uint_as_float(v[i]);
+            pmask |= (uint32_t)(__fmaf_rn(-2.f, __uint_as_float(v[i]), cc[u]) <= thr) << i;
           }
         }
+        pmask &= live ? (nk >= 32 ? 0xffffffffu : ((1u << nk) - 1u)) : 0u;
+        // exact bounds of the pre-filter's survivors: candidates (every
+        // cell with L <= Tu; T only decreases, so the batch-start Tu is
+        // conservative) and kept-set insertions (U below the current root
+        // and the shared bound)
+        const float T_before = T;
+        while (pmask) {
+          const int i = __ffs(pmask) - 1;
+          pmask &= pmask - 1;
+          const int k = kb + i;
+          const float S = stage[i * kNM];
+          const float c2 = __ldg(a.cn2 + k);
+          const float n2 = __fadd_ru(a2, c2);
+          const float A = __fmaf_rn(-2.f, S, __fadd_rn(a2, c2));
+          const float mg = __fmul_ru(a.eps, n2);
+          const float L = fmaxf(__fmul_rd(__fsub_rd(A, mg), onem), 0.f);
+          if (!(L <= Tu)) continue;
+          if (nc < a.cap) cand[nc] = ((uint64_t)__float_as_uint(A) << 32) | (uint32_t)k;
+          nc++;
+          const float U = fmaxf(__fmul_ru(__fadd_ru(A, mg), onep), 0.f);
+          if (!(U < fminf(T, Tu))) continue;
+          // replace the root of the kept-set max-heap, sift down
+          int pos = 0;
+          for (;;) {
+            const int l = 2 * pos + 1;
+            if (l >= ma) break;
+            int c = l;
+            float cv = heap[l * kNM];
+            if (l + 1 < ma) {
+              const float rv = heap[(l + 1) * kNM];
+              if (rv > cv) {
+                c = l + 1;
+                cv = rv;
+              }
+            }
+            if (!(cv > U)) break;
+            heap[pos * kNM] = cv;
+            pos = c;
+          }
+          heap[pos * kNM] = U;
+          T = heap[0];
+        }
+        if (T < T_before && T < __uint_as_float(0x7f800000) && live)
+          atomicMin(gb, __float_as_uint(T));
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty_b(buf)) : "memory");
+      Tg = fminf(Tg, __uint_as_float(tg_next));
     }
     if (live) {
       a.cand_n[(size_t)slice * a.nq_pad + q] = nc;
       float *tp = a.tops + ((size_t)slice * a.nq_pad + q) * kNMaxMa;
-#pragma unroll
-      for (int i = 0; i < kNMaxMa; i++)
-        if (i < a.ma) tp[i] = set[i];
+      for (int i = 0; i < ma; i++) tp[i] = heap[i * kNM];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -347,20 +429,30 @@ __global__ void __launch_bounds__(kNRerankWarps * 32) k_nn_rerank(
   for (int s = 0; s < slices; s++) overflow |= a.cand_n[(size_t)s * a.nq_pad + q] > a.cap;
   float Ustar = 0.f;
   if (!overflow) {
+    // U* = the ma-th smallest of the slices' kept sets; only their finite
+    // entries can matter (slices after the first mostly kept nothing below
+    // the shared bound), so those are compacted before the sort
     const int n = slices * ma;
-    for (int i = lane; i < vcap; i += 32) {
-      uint64_t key = ~0ull;
+    int nf = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      float u = __int_as_float(0x7f800000);
       if (i < n) {
         const int s = i / ma, j = i - s * ma;
-        key = (uint64_t)__float_as_uint(a.tops[((size_t)s * a.nq_pad + q) * kNMaxMa + j]);
+        u = a.tops[((size_t)s * a.nq_pad + q) * kNMaxMa + j];
       }
-      v[i] = key;
+      const bool fin = u < 3.0e38f;
+      const unsigned bal = __ballot_sync(0xffffffffu, fin);
+      if (fin) v[nf + __popc(bal & ((1u << lane) - 1))] = (uint64_t)__float_as_uint(u);
+      nf += __popc(bal);
     }
-    __syncwarp();
     int p2 = 1;
-    while (p2 < n) p2 <<= 1;
+    while (p2 < max(nf, ma)) p2 <<= 1;
+    for (int i = nf + lane; i < p2; i += 32) v[i] = ~0ull;
+    __syncwarp();
     warp_sort_u64(v, p2);
-    Ustar = __uint_as_float((uint32_t)v[min(ma, a.K) - 1]);
+    Ustar = nf >= min(ma, a.K) ? __uint_as_float((uint32_t)v[min(ma, a.K) - 1])
+                               : __int_as_float(0x7f800000);
   }
   __syncwarp();
   const float a2 = a.qn2[q];
@@ -447,7 +539,7 @@ int probe_tc_prepare(const float *coarse, int K, int d, float **mu, void **ctile
   QADC_CUDA(cudaMalloc(mu, (size_t)d * 4));
   QADC_CUDA(cudaMalloc(ctiled, (size_t)k_pad * 3 * d * 2));
   QADC_CUDA(cudaMalloc(cn2, (size_t)K * 4));
-  k_nn_mean<<<(d + 127) / 128, 128, 0, st>>>(coarse, K, d, *mu);
+  k_nn_mean<<<d, 256, 0, st>>>(coarse, K, d, *mu);
   k_nn_split<kNN><<<(unsigned)((k_pad * 32 + 255) / 256), 256, 0, st>>>(
       coarse, K, k_pad, d, *mu, true, (uint8_t *)*ctiled, *cn2);
   QADC_CUDA(cudaGetLastError());
@@ -456,9 +548,10 @@ int probe_tc_prepare(const float *coarse, int K, int d, float **mu, void **ctile
 
 bool launch_probe_tc(const float *coarse, const float *mu, const void *ctiled, const float *cn2,
                      int K, int d, const float *queries, int nq, int ma, int64_t *cells,
-                     cudaStream_t st) {
+                     cudaStream_t st, float *dbg_S, int *dbg_counts) {
   if (nq <= 0) return true;
   if (!probe_tc_supported(K, d, ma)) return false;
+  (void)cudaGetLastError();  // a stale error of an earlier call must not read as ours
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -472,10 +565,11 @@ bool launch_probe_tc(const float *coarse, const float *mu, const void *ctiled, c
   // overflowing query falls back to the exact scan, still exact)
   const int cap = ma == 1 ? 64 : (ma >= 16 ? 1024 : 512);
   // slices of the centroid range: whole waves of one-CTA-per-SM work
+  static const int max_sl = std::max(1, std::min(16, scan_env_int("QADC_B200_PROBE_SLICES", 5)));
   auto pick_slices = [&](int qtiles) {
     int best = 1;
     double best_t = 1e30;
-    for (int s = 1; s <= 16 && s <= c_tiles; s++) {
+    for (int s = 1; s <= max_sl && s <= c_tiles; s++) {
       const int per = (c_tiles + s - 1) / s;
       const double waves = std::ceil((double)qtiles * s / nsm);
       const double t = waves * per + 0.02 * s * per;  // small cost per extra slice (merges)
@@ -497,15 +591,23 @@ bool launch_probe_tc(const float *coarse, const float *mu, const void *ctiled, c
   float *qn2 = nullptr, *tops = nullptr;
   uint64_t *cand = nullptr;
   int *cand_n = nullptr;
-  if (cudaMallocAsync(&qt, (size_t)qpad_max * 3 * d * 2, st) != cudaSuccess ||
+  unsigned *bound = nullptr;
+  float *c2p = nullptr;
+  const double u = 1.0 / 16777216.0;
+  const float eps = (float)(1.0 / 32768.0 + (4.0 * 3 * d + 16.0) * u);
+  const float pre_f = (float)(1.0 - (double)eps - 64.0 * u);
+  if (cudaMallocAsync(&c2p, (size_t)c_tiles * kNN * 4, st) != cudaSuccess ||
+      cudaMallocAsync(&bound, (size_t)qpad_max * 4, st) != cudaSuccess ||
+      cudaMallocAsync(&qt, (size_t)qpad_max * 3 * d * 2, st) != cudaSuccess ||
       cudaMallocAsync(&qn2, (size_t)qpad_max * 4, st) != cudaSuccess ||
       cudaMallocAsync(&cand, (size_t)max_slices * qpad_max * cap * 8, st) != cudaSuccess ||
       cudaMallocAsync(&cand_n, (size_t)max_slices * qpad_max * 4, st) != cudaSuccess ||
       cudaMallocAsync(&tops, (size_t)max_slices * qpad_max * kNMaxMa * 4, st) != cudaSuccess)
     return false;
-  const size_t smem = (size_t)nch * kNABlock + (size_t)kNStages * kNBBlock;
+  k_nn_c2p<<<(c_tiles * kNN + 255) / 256, 256, 0, st>>>(cn2, K, c_tiles * kNN, pre_f, c2p);
+  const size_t smem = (size_t)nch * kNABlock + (size_t)kNStages * kNBBlock +
+                      (size_t)(kNMaxMa + 32) * kNM * 4;  // + kept-set heaps and the S stage
   cudaFuncSetAttribute(k_nn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const double u = 1.0 / 16777216.0;
   bool ok = true;
   for (int64_t q0 = 0; q0 < nq && ok; q0 += chunk_q) {
     const int n = (int)std::min<int64_t>(chunk_q, nq - q0);
@@ -524,11 +626,17 @@ bool launch_probe_tc(const float *coarse, const float *mu, const void *ctiled, c
     a.ma = ma;
     a.cap = cap;
     a.nq_pad = qtiles * kNM;
-    a.eps = (float)(1.0 / 32768.0 + (4.0 * 3 * d + 16.0) * u);
+    a.eps = eps;
     a.gam = (float)((d + 4) * u);
     a.cand = cand;
     a.cand_n = cand_n;
     a.tops = tops;
+    a.dbg_S = q0 == 0 ? dbg_S : nullptr;
+    a.bound = bound;
+    a.c2p = c2p;
+    a.pre_q = pre_f;
+    // 0x7f7f7f7f = 3.4e38: above every real U
+    cudaMemsetAsync(bound, 0x7f, (size_t)a.nq_pad * 4, st);
     k_nn_split<kNM><<<(unsigned)(((int64_t)a.nq_pad * 32 + 255) / 256), 256, 0, st>>>(
         queries + (size_t)q0 * d, n, a.nq_pad, d, mu, false, qt, qn2);
     k_nn_tc<<<dim3(qtiles, slices), kNThreads, smem, st>>>(a);
@@ -539,7 +647,15 @@ bool launch_probe_tc(const float *coarse, const float *mu, const void *ctiled, c
     k_nn_rerank<<<(n + kNRerankWarps - 1) / kNRerankWarps, kNRerankWarps * 32, rsmem, st>>>(
         a, slices, coarse, queries + (size_t)q0 * d, d, cells + (size_t)q0 * ma, vcap);
     ok = cudaGetLastError() == cudaSuccess;
+    if (dbg_counts && q0 == 0) {  // diagnostics: slices, then per-(slice, query) candidate counts
+      const int nc = std::min(slices * a.nq_pad, 1 << 20);
+      cudaMemcpyAsync(dbg_counts, &slices, 4, cudaMemcpyHostToDevice, st);
+      cudaMemcpyAsync(dbg_counts + 1, cand_n, (size_t)nc * 4, cudaMemcpyDeviceToDevice, st);
+      cudaStreamSynchronize(st);
+    }
   }
+  cudaFreeAsync(bound, st);
+  cudaFreeAsync(c2p, st);
   cudaFreeAsync(qt, st);
   cudaFreeAsync(qn2, st);
   cudaFreeAsync(cand, st);
@@ -550,3 +666,24 @@ bool launch_probe_tc(const float *coarse, const float *mu, const void *ctiled, c
 }
 
 }  // namespace qadc
+
+// Diagnostics (C ABI, device pointers): the fused probe on nq queries with
+// the raw dot products of the first CTA's first tile (S, 128 x 256 fp32)
+// and the candidate counts ([0] = slices, then slices x nq_pad ints).
+extern "C" __attribute__((visibility("default"))) int qadc_b200_debug_probe_tc(const float *coarse, int K, int d, const float *queries,
+                                        int nq, int ma, int64_t *cells, float *S, int *counts,
+                                        float *mu_out, void *stream) {
+  using namespace qadc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!probe_tc_supported(K, d, ma)) return kErrArgs;
+  float *mu = nullptr, *cn2 = nullptr;
+  void *cs = nullptr;
+  if (int rc = probe_tc_prepare(coarse, K, d, &mu, &cs, &cn2, st)) return rc;
+  const bool ok = launch_probe_tc(coarse, mu, cs, cn2, K, d, queries, nq, ma, cells, st, S, counts);
+  cudaStreamSynchronize(st);
+  if (mu_out) cudaMemcpy(mu_out, mu, (size_t)d * 4, cudaMemcpyDeviceToDevice);
+  cudaFree(mu);
+  cudaFree(cs);
+  cudaFree(cn2);
+  return ok ? kOk : kErrCuda;
+}

@@ -270,6 +270,25 @@ def ivf_rows(cfg: IvfConfig, pq: _PQ, coarse: np.ndarray, n: int, device="cuda",
     return rows, rid, row_off
 
 
+def base_chunks(cfg, n: int, device="cuda"):
+    """(offset, vectors) chunks of the base exactly as the index build draws
+    it (same seeds and chunk grid; shard 0 of an exhaustive config), for
+    the recall harness's ground truth."""
+    if isinstance(cfg, IvfConfig) and cfg.sharding == "range":
+        for g in range(-(-n // CFG4_CHUNK)):
+            a, b = g * CFG4_CHUNK, min(n, (g + 1) * CFG4_CHUNK)
+            yield a, datagen.mixture_torch(cfg.mix, b - a, seed=SEED * 1000 + 4,
+                                           centre_seed=CORPUS,
+                                           stream=datagen.STREAM_BASE * 100_000 + g, device=device)
+        return
+    step = 4 * datagen.CHUNK  # == ivf_rows' list-sharded chunk (1 << 22)
+    for c0 in range(0, n, step):
+        yield c0, datagen.mixture_torch(cfg.mix, min(step, n - c0), seed=SEED * 1000,
+                                        centre_seed=CORPUS,
+                                        stream=datagen.STREAM_BASE * 100 + c0 // step,
+                                        device=device)
+
+
 def encode_torch(pq: _PQ, resid):
     """pq.encode_batch (pq.py:210-217) restated in plain torch for the
     REFERENCE arm's index setup (no product kernels in that process):

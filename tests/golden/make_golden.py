@@ -57,6 +57,12 @@ def main(only=None):
     if only == "cfg2":
         make_search_cfg2(HERE / "search_cfg2_k4096.npz", n=100_000, nq=16, mas=(16, 64))
         return
+    if only == "gt":
+        make_ground_truth(HERE / "ground_truth.npz")
+        return
+    if only == "qivf":
+        make_qivf(HERE / "ref_index.qivf", HERE / "ref_index.npz")
+        return
     from qadc import adc, ivf, kernels, qadc as rq
     from qadc import pq as rpq
     from qadc.heap import NeighborHeap
@@ -262,6 +268,50 @@ def make_search(path, mix, m, n, nq, Rs, init, opq, K, mas):
             out[f"ma{ma}_luts"] = luts
             out[f"ma{ma}_cells"] = cells
     np.savez_compressed(path, **out)
+
+
+def make_qivf(path, expect_path):
+    """A QIVF v1 file written by the reference's own ivf.save_index
+    (ivf.py:185-244): IVF K=5 with empty and padded lists, transposed
+    layout; plus the lists it holds, for the reader test."""
+    from qadc import ivf, kmeans
+    from qadc import qadc as rq
+
+    rng = np.random.default_rng(9)
+    sizes = [0, 17, 32, 1, 40]
+    lists, codes, ids = [], [], []
+    nid = 0
+    for s in sizes:
+        c = rng.integers(0, 256, (s, 4), dtype=np.uint8)
+        i = np.arange(nid, nid + s, dtype=np.int64) * 3
+        nid += s
+        lists.append(rq.transpose_list(c, i))
+        codes.append(c)
+        ids.append(i)
+    cen = rng.random((5, 8)).astype(np.float32)
+    idx = ivf.IvfIndex(d=8, m=8, b=4, coarse=kmeans.Codebook(cen), lists=lists,
+                       layout=ivf.LAYOUT_TRANSPOSED)
+    ivf.save_index(idx, path)
+    np.savez_compressed(expect_path, centroids=cen, sizes=np.asarray(sizes),
+                        codes=np.concatenate(codes), ids=np.concatenate(ids))
+
+
+def make_ground_truth(path):
+    """synth.ground_truth (synth.py:45-70): exact nearest neighbours, ties
+    to the lower id, on a seeded mixture base with duplicated rows (forced
+    distance ties) and a query equal to a base row."""
+    from qadc import synth
+    from qadc.vecio import Dataset
+
+    from paper_1704_07355_b200 import datagen
+
+    mix = datagen.Mixture(d=32, components=16, centre_high=10.0, sigma=1.0)
+    base = datagen.mixture_numpy(mix, 5000, seed=3, stream=datagen.STREAM_BASE)
+    base[4000:4100] = base[100:200]  # duplicates: ties resolve to the lower id
+    queries = datagen.mixture_numpy(mix, 24, seed=3, stream=datagen.STREAM_QUERY)
+    queries[0] = base[150]
+    gt = synth.ground_truth(Dataset.from_array(base), Dataset.from_array(queries), depth=10)
+    np.savez_compressed(path, base=base, queries=queries, ids=gt.ids)
 
 
 def make_search_cfg2(path, n, nq, mas, R=100, init=1000):

@@ -599,9 +599,9 @@ def test_probe_many_query_tiles_vs_oracle(gpu, K, ma, nq):
     qs = datagen.mixture_numpy(datagen.SIFT_LIKE, nq, seed=K, stream=4)
     dev = torch.device("cuda")
     cells = torch.empty((nq, ma), dtype=torch.int64, device=dev)
+    cd, qd = torch.from_numpy(cen).to(dev), torch.from_numpy(qs).to(dev)  # alive during the call
     _native.check(_native.load_library().qadc_b200_probe(
-        _native.dptr(torch.from_numpy(cen).to(dev)), K, 128,
-        _native.dptr(torch.from_numpy(qs).to(dev)), nq, ma, _native.dptr(cells), None,
+        _native.dptr(cd), K, 128, _native.dptr(qd), nq, ma, _native.dptr(cells), None,
         torch.cuda.current_stream().cuda_stream), "probe")
     got = cells.cpu().numpy()
     for i in range(nq):

@@ -7,6 +7,8 @@ import ctypes
 import re
 from pathlib import Path
 
+from conftest import golden
+
 import numpy as np
 import pytest
 
@@ -232,21 +234,21 @@ def test_qivf_round_trip(tmp_path, rng):
         ivf.load_index(tmp_path / "x.qivf")
 
 
-def test_qivf_reads_reference_written_file(tmp_path):
-    """A QIVF v1 file written by the reference's own save_index loads here."""
-    import sys
-    src = Path("/tmp/qadc_ref_golden/src")
-    if not src.exists():
-        pytest.skip("reference build not present on this host")
-    sys.path.insert(0, str(src))
-    from qadc import ivf as rivf
-    from qadc import qadc as rq
-    lst = rq.transpose_list(np.arange(40, dtype=np.uint8).reshape(20, 2), np.arange(20) * 3)
-    ridx = rivf.IvfIndex(d=8, m=4, b=4, coarse=None, lists=[lst], layout=rivf.LAYOUT_TRANSPOSED)
-    rivf.save_index(ridx, tmp_path / "r.qivf")
-    back = ivf.load_index(tmp_path / "r.qivf")
-    assert np.array_equal(back.lists[0].blocks, lst.blocks)
-    assert np.array_equal(back.lists[0].ids, lst.ids)
+def test_qivf_reads_reference_written_file():
+    """A QIVF v1 file written by the reference's own save_index
+    (tests/golden/ref_index.qivf, made by make_golden.py qivf: IVF K=5 with
+    empty, partial and padded lists) loads here with identical lists."""
+    from paper_1704_07355_b200.qadc import untranspose_list
+    from conftest import GOLDEN
+    want = golden("ref_index.npz")
+    back = ivf.load_index(GOLDEN / "ref_index.qivf")
+    assert np.array_equal(back.coarse.centroids, want["centroids"])
+    off = np.concatenate([[0], np.cumsum(want["sizes"])])
+    assert len(back.lists) == want["sizes"].shape[0]
+    for L, lst in enumerate(back.lists):
+        codes, ids = untranspose_list(lst)
+        assert np.array_equal(codes, want["codes"][off[L]:off[L + 1]])
+        assert np.array_equal(ids, want["ids"][off[L]:off[L + 1]])
 
 
 # ---------------------------------------------------------------- workload
@@ -258,3 +260,25 @@ def test_mixture_generator_shapes_and_determinism():
     assert np.array_equal(a, b)
     g = datagen.mixture_numpy(datagen.GIST_LIKE, 10, seed=3, stream=2)
     assert g.shape == (10, 960) and g.max() < 2.0
+
+
+def test_recall_ground_truth_matches_reference_synth():
+    """recall.ground_truth (the GPU recall harness's exact k-NN, here on the
+    CPU device) equals the reference's synth.ground_truth (synth.py:45-70,
+    committed output): ids in exact fp64 order, ties to the lower id, over
+    a base split into several chunks; recall_at follows bench.py:110-122."""
+    import torch
+
+    from paper_1704_07355_b200.recall import ground_truth, recall_at
+    g = golden("ground_truth.npz")
+    base = torch.from_numpy(g["base"])
+
+    def chunks():
+        for c0 in range(0, base.shape[0], 1700):
+            yield c0, base[c0:c0 + 1700]
+    got = ground_truth(chunks(), g["queries"], depth=10, device="cpu")
+    assert np.array_equal(got, g["ids"])
+    res = np.stack([np.roll(g["ids"][i], i % 3) for i in range(g["ids"].shape[0])])
+    gt1 = g["ids"][:, 0]
+    assert recall_at(res, gt1, 1) == np.mean([i % 3 == 0 for i in range(24)])
+    assert recall_at(res, gt1, 3) == 1.0
