@@ -420,32 +420,43 @@ __global__ void __launch_bounds__(256) k_residual_lut(
   __syncthreads();
   const float *y = sr;
   if (rotation) {
-    if ((d & 7) == 0) {
-      // thread task: 4 consecutive outputs of one pair, 8 lane accumulators
-      // each; per k one float4 segment of R^T row k and one broadcast r[k]
+    if ((d & 7) == 0 && (np & 1) == 0) {
+      // thread task: 4 consecutive outputs of two pairs, 8 lane accumulators
+      // each; per k one float4 segment of R^T row k (L1, shared by the two
+      // pairs) and two broadcast residual values
       const int quads = d >> 2;
-      for (int task = threadIdx.x; task < np * quads; task += blockDim.x) {
-        const int p = task / quads, i0 = (task - p * quads) * 4;
-        const float *r = sr + (size_t)p * d;
-        float a[4][8];
+      for (int task = threadIdx.x; task < (np >> 1) * quads; task += blockDim.x) {
+        const int pp = task / quads, i0 = (task - pp * quads) * 4;
+        const float *r0 = sr + (size_t)(2 * pp) * d;
+        const float *r1 = r0 + d;
+        float a[2][4][8];
 #pragma unroll
-        for (int u = 0; u < 4; u++)
+        for (int h = 0; h < 2; h++)
 #pragma unroll
-          for (int l = 0; l < 8; l++) a[u][l] = 0.f;
+          for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int l = 0; l < 8; l++) a[h][u][l] = 0.f;
 #pragma unroll 1
         for (int k0 = 0; k0 < d; k0 += 8) {
 #pragma unroll
           for (int l = 0; l < 8; l++) {
             const float4 c = __ldg((const float4 *)(rotT + (size_t)(k0 + l) * d + i0));
-            const float rv = r[k0 + l];
-            a[0][l] = __fmaf_rn(c.x, rv, a[0][l]);
-            a[1][l] = __fmaf_rn(c.y, rv, a[1][l]);
-            a[2][l] = __fmaf_rn(c.z, rv, a[2][l]);
-            a[3][l] = __fmaf_rn(c.w, rv, a[3][l]);
+            const float v0 = r0[k0 + l], v1 = r1[k0 + l];
+            a[0][0][l] = __fmaf_rn(c.x, v0, a[0][0][l]);
+            a[0][1][l] = __fmaf_rn(c.y, v0, a[0][1][l]);
+            a[0][2][l] = __fmaf_rn(c.z, v0, a[0][2][l]);
+            a[0][3][l] = __fmaf_rn(c.w, v0, a[0][3][l]);
+            a[1][0][l] = __fmaf_rn(c.x, v1, a[1][0][l]);
+            a[1][1][l] = __fmaf_rn(c.y, v1, a[1][1][l]);
+            a[1][2][l] = __fmaf_rn(c.z, v1, a[1][2][l]);
+            a[1][3][l] = __fmaf_rn(c.w, v1, a[1][3][l]);
           }
         }
-        *(float4 *)(sy + (size_t)p * d + i0) =
-            make_float4(blas8_fold(a[0]), blas8_fold(a[1]), blas8_fold(a[2]), blas8_fold(a[3]));
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+          *(float4 *)(sy + (size_t)(2 * pp + h) * d + i0) =
+              make_float4(blas8_fold(a[h][0]), blas8_fold(a[h][1]), blas8_fold(a[h][2]),
+                          blas8_fold(a[h][3]));
       }
     } else {
       for (int e = threadIdx.x; e < np * d; e += blockDim.x) {

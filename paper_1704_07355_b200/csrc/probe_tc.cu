@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kNThreads, 1) k_nn_tc(const __grid_constant__ 
             pmask |= (uint32_t)(__fmaf_rn(-2.f, __uint_as_float(v[i]), cc[u]) <= thr) << i;
           }
         }
-        pmask &= live ? (nk >= 32 ? 0xffffffffu : ((1u << nk) - 1u)) : 0u;
+        pmask &= (live && nk > 0) ? (nk >= 32 ? 0xffffffffu : ((1u << nk) - 1u)) : 0u;
         // exact bounds of the pre-filter's survivors: candidates (every
         // cell with L <= Tu; T only decreases, so the batch-start Tu is
         // conservative) and kept-set insertions (U below the current root

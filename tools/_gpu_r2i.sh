@@ -1,0 +1,3 @@
+O=gpurun_out/r2i; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 900 python tools/phase_times.py cfg4 > $O/phase_cfg4.txt 2>&1; echo "rc=$?"; grep -v Warn $O/phase_cfg4.txt | head -24
