@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(256) k_probe_fast(
 // accumulators, lane l taking k = l, l + 8, l + 16, ... in ascending k; then
 // t_l = acc_l + acc_{l+4} (l < 4) and y = (t0 + t1) + (t2 + t3). R^T is
 // read through L1 (64 KB, float4 rows: 4 consecutive outputs per thread).
-constexpr int kLutPairs = 16;  // (query, slot) pairs per CTA
+constexpr int kLutPairs = 32;  // (query, slot) pairs per CTA (4 pairs x 4 outputs per thread task)
 
 __device__ __forceinline__ float blas8_fold(const float (&a)[8]) {
   return __fadd_rn(__fadd_rn(__fadd_rn(a[0], a[4]), __fadd_rn(a[1], a[5])),
@@ -420,43 +420,61 @@ __global__ void __launch_bounds__(256) k_residual_lut(
   __syncthreads();
   const float *y = sr;
   if (rotation) {
-    if ((d & 7) == 0 && (np & 1) == 0) {
-      // thread task: 4 consecutive outputs of two pairs, 8 lane accumulators
-      // each; per k one float4 segment of R^T row k (L1, shared by the two
-      // pairs) and two broadcast residual values
+    if ((d & 7) == 0 && (np & 3) == 0) {
+      // thread task: 4 consecutive outputs x 4 pairs. The 8 lane sums of
+      // the OpenBLAS order are produced one lane at a time (16 FMAs over
+      // k = 8 kk + l each) in the fold's order l = 0, 4, 1, 5, 2, 6, 3, 7,
+      // so only the running partial folds stay live: 16 accumulators + 3
+      // partials per output, one float4 of R^T row k (L1, shared by the
+      // 4 pairs) and 4 broadcast residual values per k.
       const int quads = d >> 2;
-      for (int task = threadIdx.x; task < (np >> 1) * quads; task += blockDim.x) {
-        const int pp = task / quads, i0 = (task - pp * quads) * 4;
-        const float *r0 = sr + (size_t)(2 * pp) * d;
-        const float *r1 = r0 + d;
-        float a[2][4][8];
+      for (int task = threadIdx.x; task < (np >> 2) * quads; task += blockDim.x) {
+        const int pg = task / quads, i0 = (task - pg * quads) * 4;
+        const float *r0 = sr + (size_t)(4 * pg) * d;
+        float s0[4][4], s1[4][4], s2[4][4];
 #pragma unroll
-        for (int h = 0; h < 2; h++)
+        for (int li = 0; li < 8; li++) {
+          const int l = (li >> 1) + 4 * (li & 1);  // 0, 4, 1, 5, 2, 6, 3, 7
+          float acc[4][4];
 #pragma unroll
           for (int u = 0; u < 4; u++)
 #pragma unroll
-            for (int l = 0; l < 8; l++) a[h][u][l] = 0.f;
-#pragma unroll 1
-        for (int k0 = 0; k0 < d; k0 += 8) {
+            for (int h = 0; h < 4; h++) acc[u][h] = 0.f;
+#pragma unroll 4
+          for (int k = l; k < d; k += 8) {
+            const float4 c = __ldg((const float4 *)(rotT + (size_t)k * d + i0));
+            const float cc[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-          for (int l = 0; l < 8; l++) {
-            const float4 c = __ldg((const float4 *)(rotT + (size_t)(k0 + l) * d + i0));
-            const float v0 = r0[k0 + l], v1 = r1[k0 + l];
-            a[0][0][l] = __fmaf_rn(c.x, v0, a[0][0][l]);
-            a[0][1][l] = __fmaf_rn(c.y, v0, a[0][1][l]);
-            a[0][2][l] = __fmaf_rn(c.z, v0, a[0][2][l]);
-            a[0][3][l] = __fmaf_rn(c.w, v0, a[0][3][l]);
-            a[1][0][l] = __fmaf_rn(c.x, v1, a[1][0][l]);
-            a[1][1][l] = __fmaf_rn(c.y, v1, a[1][1][l]);
-            a[1][2][l] = __fmaf_rn(c.z, v1, a[1][2][l]);
-            a[1][3][l] = __fmaf_rn(c.w, v1, a[1][3][l]);
+            for (int h = 0; h < 4; h++) {
+              const float rv = r0[(size_t)h * d + k];
+#pragma unroll
+              for (int u = 0; u < 4; u++) acc[u][h] = __fmaf_rn(cc[u], rv, acc[u][h]);
+            }
           }
+#pragma unroll
+          for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+              const float x = acc[u][h];
+              switch (li) {
+                case 0: s0[u][h] = x; break;                                   // a0
+                case 1: s0[u][h] = __fadd_rn(s0[u][h], x); break;              // a0 + a4
+                case 2: s1[u][h] = x; break;                                   // a1
+                case 3: s1[u][h] = __fadd_rn(s1[u][h], x);                     // a1 + a5
+                        s0[u][h] = __fadd_rn(s0[u][h], s1[u][h]); break;       // (a0+a4)+(a1+a5)
+                case 4: s1[u][h] = x; break;                                   // a2
+                case 5: s1[u][h] = __fadd_rn(s1[u][h], x); break;              // a2 + a6
+                case 6: s2[u][h] = x; break;                                   // a3
+                default: s2[u][h] = __fadd_rn(s2[u][h], x);                    // a3 + a7
+                         s1[u][h] = __fadd_rn(s1[u][h], s2[u][h]);             // (a2+a6)+(a3+a7)
+                         s0[u][h] = __fadd_rn(s0[u][h], s1[u][h]);
+              }
+            }
         }
 #pragma unroll
-        for (int h = 0; h < 2; h++)
-          *(float4 *)(sy + (size_t)(2 * pp + h) * d + i0) =
-              make_float4(blas8_fold(a[h][0]), blas8_fold(a[h][1]), blas8_fold(a[h][2]),
-                          blas8_fold(a[h][3]));
+        for (int h = 0; h < 4; h++)
+          *(float4 *)(sy + (size_t)(4 * pg + h) * d + i0) =
+              make_float4(s0[0][h], s0[1][h], s0[2][h], s0[3][h]);
       }
     } else {
       for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
