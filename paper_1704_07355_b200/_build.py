@@ -66,6 +66,29 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_stock_reference(verbose: bool = False) -> None:
+    """The UNMODIFIED reference package for the CPU baseline and the
+    `--impl reference` arm: `pip install --no-index --no-build-isolation
+    --no-deps --target baseline/_ref` of a scratch copy of
+    /root/reference/pkg (its setup.py builds in the source tree, which is
+    read-only). Only where the reference exists and the install is absent;
+    baseline/_ref is git-ignored and travels to the GPU box."""
+    import sys
+    import tempfile
+    src = Path("/root/reference/pkg")
+    target = ROOT / "baseline" / "_ref"
+    if not src.exists() or list(target.glob("qadc/_kernels*.so")):
+        return
+    with tempfile.TemporaryDirectory() as tmp:
+        work = Path(tmp) / "pkg"
+        shutil.copytree(src, work)
+        cmd = [sys.executable, "-m", "pip", "install", "--no-index", "--no-build-isolation",
+               "--no-deps", "--target", str(target), "."]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, cwd=work, check=True, stdout=None if verbose else subprocess.DEVNULL)
+
+
 def build_oracle(verbose: bool = False) -> None:
     """Test infrastructure: oracle/_build (restatement) and, when the
     reference sources are present, oracle/_ref (the reference's own C)."""
@@ -78,3 +101,4 @@ def build_oracle(verbose: bool = False) -> None:
 if __name__ == "__main__":
     build_library(verbose=True)
     build_oracle(verbose=True)
+    build_stock_reference(verbose=True)

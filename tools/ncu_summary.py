@@ -1,7 +1,8 @@
-"""Write profiles/scan_ncu_summary.json from an `ncu --set full` report of
-the scan kernel (developer tool; bench.py reads the DRAM traffic from it).
+"""Write profiles/scan_ncu_<config>.json from an `ncu --set full` report of
+the scan kernel (developer tool; bench.py reads that config's DRAM traffic
+per launch from it).
 
-    python tools/ncu_summary.py gpurun_out/s20/scan_tc_cfg1.ncu-rep "<kernel label>" "<command>"
+    python tools/ncu_summary.py gpurun_out/r2g/scan_prmt_cfg4.ncu-rep "<kernel label>" "<command>" cfg4
 """
 import csv
 import json
@@ -10,6 +11,7 @@ import sys
 from pathlib import Path
 
 rep, label, cmd = sys.argv[1], sys.argv[2], sys.argv[3]
+config = sys.argv[4] if len(sys.argv) > 4 else "cfg1"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
@@ -58,7 +60,11 @@ out = {
     "block_size": num("launch__block_size"),
     "grid": num("launch__grid_size"),
     "dram_throughput_pct": num("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+    "fmaheavy_pipe_active_pct": num("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+    "lsu_shared_wavefronts_pct": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+    "instructions_executed": num("smsp__inst_executed.sum"),
+    "achieved_warps_per_sm": num("sm__warps_active.avg.per_cycle_active"),
 }
-json.dump(out, open(Path(__file__).resolve().parents[1] / "profiles" / "scan_ncu_summary.json", "w"),
-          indent=1)
+json.dump(out, open(Path(__file__).resolve().parents[1] / "profiles" / f"scan_ncu_{config}.json",
+               "w"), indent=1)
 print(json.dumps(out, indent=1))
