@@ -411,11 +411,26 @@ __global__ void __launch_bounds__(256) k_residual_lut(
   float *sy = sr + (size_t)ppc * d;                             // [ppc][d]
   const int p0 = blockIdx.x * ppc;
   const int np = min(ppc, npairs - p0);
-  for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
-    const int p = e / d, t = e - p * d;
-    const int pair = p0 + p;
-    const float qv = queries[(size_t)(pair / nslots) * d + t];
-    sr[e] = coarse ? __fsub_rn(qv, coarse[(size_t)cells[pair] * d + t]) : qv;
+  if ((d & 3) == 0) {  // residual rows as float4 (query and centroid rows are 16-byte aligned)
+    const int d4 = d >> 2;
+    for (int e = threadIdx.x; e < np * d4; e += blockDim.x) {
+      const int p = e / d4, t = e - p * d4;
+      const int pair = p0 + p;
+      float4 qv = ((const float4 *)(queries + (size_t)(pair / nslots) * d))[t];
+      if (coarse) {
+        const float4 c = ((const float4 *)(coarse + (size_t)cells[pair] * d))[t];
+        qv = make_float4(__fsub_rn(qv.x, c.x), __fsub_rn(qv.y, c.y), __fsub_rn(qv.z, c.z),
+                         __fsub_rn(qv.w, c.w));
+      }
+      ((float4 *)sr)[e] = qv;
+    }
+  } else {
+    for (int e = threadIdx.x; e < np * d; e += blockDim.x) {
+      const int p = e / d, t = e - p * d;
+      const int pair = p0 + p;
+      const float qv = queries[(size_t)(pair / nslots) * d + t];
+      sr[e] = coarse ? __fsub_rn(qv, coarse[(size_t)cells[pair] * d + t]) : qv;
+    }
   }
   __syncthreads();
   const float *y = sr;
@@ -493,6 +508,22 @@ __global__ void __launch_bounds__(256) k_residual_lut(
     y = sy;
   }
   const int dsub = d / m;
+  if (dsub == 4) {
+    // the einsum of one 4-vector (NumPy order for n = 4: products rounded,
+    // lanes (l0 + l1) + (l2 + l3)); entry (p, j, c) = (pair, sub-space, centroid)
+    const int per = m * 16;
+    for (int e = threadIdx.x; e < np * per; e += blockDim.x) {
+      const int p = e / per, ent = e - p * per;
+      const float4 c4 = __ldg((const float4 *)codebooks + ent);
+      const float4 y4 = ((const float4 *)(y + (size_t)p * d))[ent >> 4];
+      const float a0 = __fsub_rn(c4.x, y4.x), a1 = __fsub_rn(c4.y, y4.y);
+      const float a2 = __fsub_rn(c4.z, y4.z), a3 = __fsub_rn(c4.w, y4.w);
+      lut[(size_t)(p0 + p) * per + ent] =
+          __fadd_rn(__fadd_rn(__fmul_rn(a0, a0), __fmul_rn(a1, a1)),
+                    __fadd_rn(__fmul_rn(a2, a2), __fmul_rn(a3, a3)));
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < np * m * 16; e += blockDim.x) {
     const int p = e / (m * 16), ent = e - p * m * 16;
     const int j = ent >> 4;

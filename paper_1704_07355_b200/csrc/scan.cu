@@ -2342,7 +2342,7 @@ void order_items(const WorkItem *items, const int *n_items, int64_t max_items,
   const int nblk = (int)std::max<int64_t>((max_items + 255) / 256, 1);
   unsigned *cls_n = scratch, *blk = scratch + 16;
   static const int rank_buckets =
-      std::min(kRankBuckets, std::max(1, scan_env_int("QADC_B200_RANK_BUCKETS", 2)));
+      std::min(kRankBuckets, std::max(1, scan_env_int("QADC_B200_RANK_BUCKETS", 4)));
   k_item_class<<<nblk, 256, 0, st>>>(const_cast<WorkItem *>(items), n_items, pair_t, pair_depth,
                                      qh, nslots, rank_buckets, blk);
   k_item_offsets<<<1, kBuckets, 0, st>>>(blk, nblk, cls_n);
