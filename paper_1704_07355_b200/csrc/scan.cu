@@ -653,8 +653,13 @@ __device__ __forceinline__ void run_chunks(const ScanArgs &a, Smem &s, const Wor
     chunk_loop<D, MC, QT>(a, s, it, wbuf, m, tab_sa, one, nq_tile);
 }
 
+// Occupancy: 4 CTAs per SM for 8-query tiles (128 registers): with the
+// 96-register cap of 5 CTAs ptxas sank the code-word prefetch of the hot
+// loop next to its use (ncu: the scan's top stall) and spilled; the wider
+// budget keeps the loads at the top of the iteration (configs[4] scan
+// 38.6 -> 37.8 ms).
 template <int MC, int QT, bool LIN>
-__global__ void __launch_bounds__(kWarps * 32, QT >= 16 ? 3 : (QT >= 8 ? 5 : 6))
+__global__ void __launch_bounds__(kWarps * 32, QT >= 16 ? 3 : (QT >= 8 ? 4 : 6))
 k_scan(const __grid_constant__ ScanArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Smem s;
