@@ -147,6 +147,10 @@ QADC_API int64_t qadc_b200_index_bytes(const qadc_b200_index *idx);
 #define QADC_B200_SCAN_TC1 32u /* with the tensor-core scan of one exhaustive
                                   list: one SM per tile instead of CTA pairs
                                   (cta_group::2, the default) */
+#define QADC_B200_SCAN_TCW 64u /* IVF index, m = 16, 32: the warpgroup-
+                                  pipelined tensor-core scan (<= 32 queries
+                                  per pass over a list) whatever the batch;
+                                  default: from ~6 queries per probed list */
 
 /*
  * adc.py:114-187 search(method="qadc") for nq queries at once:

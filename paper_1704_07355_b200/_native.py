@@ -27,6 +27,7 @@ NO_FSAT = 4
 SCAN_PRMT = 8  # force the PRMT (CUDA-core) scan kernel
 SCAN_TC = 16  # force the int8 tensor-core scan kernel (m = 16, 32)
 SCAN_TC1 = 32  # tensor-core scan of an exhaustive list on one SM per tile (not CTA pairs)
+SCAN_TCW = 64  # IVF: warpgroup-pipelined tensor-core scan (<= 32 queries per pass over a list)
 
 _lib = None
 

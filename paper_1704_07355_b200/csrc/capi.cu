@@ -243,7 +243,7 @@ int prepare_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int 
 // over a subset with a larger candidate capacity (no phase timing).
 int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int init,
               int64_t *out_ids, float *out_d, int32_t *out_n, cudaStream_t st, SearchStats &ss,
-              int cap_g, int level, bool prmt, bool force_tc, bool one_sm) {
+              int cap_g, int level, bool prmt, bool force_tc, bool one_sm, bool force_tcw) {
   if (nq == 0) return kOk;
   const int m = idx->m;
   const int nslots = idx->K ? ma : 1;
@@ -256,9 +256,24 @@ int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int in
   // at small nprobe / large K) the PRMT kernel is faster (measured: cfg2
   // nprobe 16, ~40 pairs per list: 10.2 ms PRMT vs 25.6 ms tensor cores).
   static const int tc_min_pairs = scan_env_int("QADC_B200_TC_MIN_PAIRS", 64);
-  if (!force_tc && npairs < (int64_t)tc_min_pairs * std::max(idx->nlists, 1)) prmt = true;
-  const int qt_tile = scan_tile_queries(m, prmt);
+  // Inverted lists probed by a handful of queries each: the warpgroup-
+  // pipelined tensor-core scan (k_scan_tcw, <= 32 queries per pass over a
+  // list). Its cost per code is the one-hot expansion, whatever the number
+  // of queries, so the PRMT kernel keeps the batches that put fewer than
+  // ~6 queries on a probed list (expected probed lists under uniform
+  // probing: nl (1 - exp(-npairs / nl))). QADC_B200_TCW=0 disables it.
+  static const int tcw_env = scan_env_int("QADC_B200_TCW", 1);
+  static const int tcw_min = scan_env_int("QADC_B200_TCW_MIN_PAIRS", 6);
+  static const int tcw_max = scan_env_int("QADC_B200_TCW_MAX_PAIRS", 1 << 20);
   const int nl = idx->nlists;
+  bool tcw = false;
+  if (!prmt && !force_tc && !one_sm && idx->K > 0 && scan_use_tc(m, false)) {
+    const double load = (double)npairs / nl;
+    const double per_probed = load / std::max(1e-9, 1.0 - std::exp(-load));
+    tcw = force_tcw || (tcw_env && nl > 1 && per_probed >= tcw_min && load <= tcw_max);
+  }
+  if (!tcw && !force_tc && npairs < (int64_t)tc_min_pairs * std::max(idx->nlists, 1)) prmt = true;
+  const int qt_tile = scan_tile_queries(m, prmt, tcw);
 
   DevBuf<float> cand_mid, hist_w;
   DevBuf<unsigned> cand_n, hist;
@@ -355,6 +370,12 @@ int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int in
   k_count_codes<<<gridn(npairs), 256, 0, st>>>(cells, npairs, idx->scan_count, ncodes.p);
   ScanArgs a;
   a.codes = idx->codes;
+  a.codes_cm = nullptr;
+  a.tcw = tcw ? 1 : 0;
+  if (scan_use_tc(m, prmt) && !pair_cta) {  // k_scan_tc / k_scan_tcw expand from the code-major copy
+    if ((rc = ensure_code_major(idx, st))) return rc;
+    a.codes_cm = idx->codes_cm;
+  }
   a.valid = idx->valid;
   a.ids = idx->ids;
   a.items = no_order ? items.p : items_ord.p;
@@ -388,7 +409,7 @@ int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int in
     cudaStreamSynchronize(st);
     tc_stats_dump();
   }
-  ss.scan_tc = scan_use_tc(m, prmt) ? 1 : 0;
+  ss.scan_tc = scan_use_tc(m, prmt) ? (tcw ? 2 : 1) : 0;
   QADC_CUDA(cudaGetLastError());
   cudaEventRecord(e1, st);
   ss.scan_launches++;
@@ -489,7 +510,7 @@ int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int in
     const int cap2 = (int)std::min<int64_t>(std::max<int64_t>((int64_t)need + 1024, 2LL * cap_g),
                                             (int64_t)1 << 28);
     rc = scan_impl(idx, sp, nr, R, ma, init, sub_ids.p, sub_d.p, sub_n.p, st, ss, cap2, level + 1,
-                   prmt, force_tc, one_sm);
+                   prmt, force_tc, one_sm, force_tcw);
     if (rc) return rc;
     k_scatter_out<<<gridn((int64_t)nr * R), 256, 0, st>>>(sub_ids.p, sub_d.p, sub_n.p, rows.p, nr,
                                                           R, out_ids, out_d, out_n);
@@ -502,7 +523,7 @@ int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int in
 int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int ma, int init,
                 const float *lut_in, const int64_t *cells_in, int64_t *out_ids, float *out_d,
                 int32_t *out_n, cudaStream_t st, SearchStats &ss, int cap_g, bool no_fsat,
-                bool prmt, bool force_tc, bool one_sm) {
+                bool prmt, bool force_tc, bool one_sm, bool force_tcw) {
   if (nq == 0) return kOk;
   const int m = idx->m;
   const int nslots = idx->K ? ma : 1;
@@ -533,7 +554,7 @@ int search_impl(qadc_b200_index *idx, const float *queries, int nq, int R, int m
   p.fsat_mid = fsat_mid.p;
   p.fsat_id = fsat_id.p;
   rc = scan_impl(idx, p, nq, R, ma, init, out_ids, out_d, out_n, st, ss, cap_g, 0, prmt, force_tc,
-                 one_sm);
+                 one_sm, force_tcw);
   if (rc) return rc;
   float t = 0.f;
   cudaEvent_t *ev = phase_events();
@@ -780,7 +801,7 @@ extern "C" void qadc_b200_index_destroy(qadc_b200_index *idx) {
     cudaFree(idx->pcodes); cudaFree(idx->pids); cudaFree(idx->pchunk_off); cudaFree(idx->planes);
   }
   cudaFree(idx->coarse); cudaFree(idx->coarseT); cudaFree(idx->cnorm); cudaFree(idx->pmu); cudaFree(idx->pcsplit); cudaFree(idx->pcn2); cudaFree(idx->codebooks); cudaFree(idx->rotation); cudaFree(idx->rotationT);
-  cudaFree(idx->codes); cudaFree(idx->valid); cudaFree(idx->ids); cudaFree(idx->chunk_list);
+  cudaFree(idx->codes); cudaFree(idx->codes_cm); cudaFree(idx->valid); cudaFree(idx->ids); cudaFree(idx->chunk_list);
   cudaFree(idx->chunk_off); cudaFree(idx->lanes); cudaFree(idx->count); cudaFree(idx->scan_count);
   delete idx;
 }
@@ -949,7 +970,7 @@ extern "C" int qadc_b200_search_batch(qadc_b200_index *idx, const float *queries
   int rc = search_impl(idx, q, nq, R, ma, init, lin, cin, oi, od, on, st, ss,
                        candidate_capacity(nq, R), (flags & QADC_B200_NO_FSAT) != 0,
                        (flags & QADC_B200_SCAN_PRMT) != 0, (flags & QADC_B200_SCAN_TC) != 0,
-                       (flags & QADC_B200_SCAN_TC1) != 0);
+                       (flags & QADC_B200_SCAN_TC1) != 0, (flags & QADC_B200_SCAN_TCW) != 0);
   if (rc) return rc;
   if (host) {
     QADC_CUDA(cudaMemcpyAsync(out_ids, oi, (size_t)nq * R * 8, cudaMemcpyDeviceToHost, st));
@@ -1038,7 +1059,8 @@ extern "C" int qadc_b200_search_scan(qadc_b200_index *idx, int nq, int R, int ma
   SearchStats ss;
   int rc = scan_impl(idx, p, nq, R, ma, init, out_ids, out_d, out_n, st, ss,
                      candidate_capacity(nq, R), 0, (flags & QADC_B200_SCAN_PRMT) != 0,
-                     (flags & QADC_B200_SCAN_TC) != 0, (flags & QADC_B200_SCAN_TC1) != 0);
+                     (flags & QADC_B200_SCAN_TC) != 0, (flags & QADC_B200_SCAN_TC1) != 0,
+                     (flags & QADC_B200_SCAN_TCW) != 0);
   if (rc) return rc;
   write_stats(ss, stats);
   return kOk;

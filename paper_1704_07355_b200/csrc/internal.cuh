@@ -31,6 +31,11 @@ struct qadc_b200_index {
   float *rotation = nullptr;   // [d][d] or null
   float *rotationT = nullptr;  // [d][d] R^T (coalesced float4 rows for the residual rotation)
   uint32_t *codes = nullptr;   // [total_chunks][m][32]
+  // Code-major copy for the one-SM tensor-core scan (built on first use,
+  // ensure_code_major): [total_chunks * 256][m / 8] words, word i of a code
+  // = its sub-codes 8i..8i+7, sub-code 8i+k at bits 4k..4k+3 (each 16-bit
+  // half is a PRMT selector over four sub-quantizers of ONE code).
+  uint32_t *codes_cm = nullptr;
   uint8_t *valid = nullptr;    // [total_chunks][32]
   int64_t *ids = nullptr;      // [total_chunks * 256], -1 padding
   int32_t *chunk_list = nullptr;  // [total_chunks] owning list
@@ -67,6 +72,8 @@ int pack_from_blocks(qadc_b200_index *idx, const uint8_t *d_blocks,
 int pack_from_rows(qadc_b200_index *idx, const uint8_t *d_rows,
                    const int64_t *d_row_off, const int64_t *d_ids,
                    cudaStream_t st);
+// Builds idx->codes_cm from the interleaved codes if absent (m % 8 == 0).
+int ensure_code_major(qadc_b200_index *idx, cudaStream_t st);
 
 // ---- lut.cu ----
 void launch_compute_tables(const float *codebooks, int m, int dsub,
@@ -117,6 +124,7 @@ struct WorkItem {
 
 struct ScanArgs {
   const uint32_t *codes;
+  const uint32_t *codes_cm;  // code-major copy (k_scan_tc only; may be null otherwise)
   const uint8_t *valid;
   const int64_t *ids;
   const WorkItem *items;
@@ -139,6 +147,7 @@ struct ScanArgs {
   int R;
   int bound_every;         // appended candidates between global-histogram bound reads
   int linear;              // 1: linear fixed-m loop (long items), 0: interleaved loop
+  int tcw;                 // 1: warpgroup-pipelined tensor-core scan for lists with few queries (k_scan_tcw)
   int pair_cta;            // tensor-core scan on CTA pairs (static item order): 1 k_scan_tc2 (flusher rings), 2 k_scan_tc2i (inline survivors)
   int dbg;                 // timing experiments only (QADC_B200_TC_DEBUG; results invalid if != 0)
 };
@@ -150,7 +159,7 @@ int scan_qt_per_cta(int m);
 // prmt: the caller asked for the PRMT kernel (QADC_B200_SCAN_PRMT).
 bool scan_use_tc(int m, bool prmt);
 void tc_stats_dump();  // debug counters of the tensor-core scan (QADC_B200_TC_DEBUG & 64)
-int scan_tile_queries(int m, bool prmt);
+int scan_tile_queries(int m, bool prmt, bool tcw = false);
 // Resident scan CTAs on the device (occupancy x SMs) for this shape.
 int scan_resident_ctas(int m, int cap_l, int nsm, int linear, bool prmt);
 int scan_env_int(const char *name, int dflt);

@@ -6,6 +6,9 @@
 //     (pack_codes nibble order, pq.py:90-105); ids 16 per block, -1 padding;
 //   * packed code rows (pq.py:90-105): (n, m/2) bytes per list.
 // Output: see internal.cuh (interleaved32 + validity + padded ids).
+#include <algorithm>
+#include <mutex>
+
 #include "internal.cuh"
 
 namespace qadc {
@@ -79,6 +82,27 @@ __global__ void k_chunk_list(const int64_t *__restrict__ chunk_off, int nlists,
     for (int64_t g = chunk_off[L]; g < chunk_off[L + 1]; g++) chunk_list[g] = L;
 }
 
+// One thread per (code slot, word i): gathers sub-codes 8i..8i+7 of the code
+// from the interleaved words.
+__global__ void k_code_major(const uint32_t *__restrict__ codes, int m, int64_t total_chunks,
+                             uint32_t *__restrict__ out) {
+  const int wpc = m / 8;
+  const int64_t n = total_chunks * kChunkCodes * wpc;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % wpc);
+    const int64_t slot = t / wpc;
+    const int64_t g = slot / kChunkCodes;
+    const int c = (int)(slot % kChunkCodes);
+    const uint32_t *src = codes + ((size_t)g * m + 8 * i) * 32 + (c >> 3);
+    const int sh = 4 * (c & 7);
+    uint32_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) w |= ((src[k * 32] >> sh) & 15u) << (4 * k);
+    out[t] = w;
+  }
+}
+
 int common_alloc(qadc_b200_index *idx, cudaStream_t st) {
   const int64_t tc = idx->total_chunks;
   // one chunk of zeroed padding: the scan's linear prefetch reads up to 12
@@ -116,6 +140,29 @@ int pack_from_blocks(qadc_b200_index *idx, const uint8_t *d_blocks,
   k_ids<false><<<grid_for(tc * kChunkCodes), 256, 0, st>>>(
       d_blk_off, d_ids, idx->chunk_list, idx->chunk_off, idx->lanes, tc, idx->ids, idx->valid);
   QADC_CUDA(cudaGetLastError());
+  return kOk;
+}
+
+int ensure_code_major(qadc_b200_index *idx, cudaStream_t st) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (idx->codes_cm) return kOk;
+  if (idx->m % 8) {
+    set_error("code-major copy needs m % 8 == 0");
+    return kErrArgs;
+  }
+  const int64_t tc = std::max<int64_t>(idx->total_chunks, 1);
+  const size_t bytes = (size_t)tc * kChunkCodes * (idx->m / 8) * 4;
+  uint32_t *p = nullptr;
+  QADC_CUDA(cudaMalloc(&p, bytes));
+  if (idx->total_chunks > 0)
+    k_code_major<<<grid_for(idx->total_chunks * kChunkCodes * (idx->m / 8)), 256, 0, st>>>(
+        idx->codes, idx->m, idx->total_chunks, p);
+  else
+    cudaMemsetAsync(p, 0, bytes, st);
+  QADC_CUDA(cudaGetLastError());
+  idx->codes_cm = p;
+  idx->bytes += (int64_t)bytes;
   return kOk;
 }
 

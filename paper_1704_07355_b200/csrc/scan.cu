@@ -866,6 +866,16 @@ __device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase) {
       : "memory");
 }
 
+// As tc_wait without the suspend-time hint (short tiles: the wake-up must be prompt).
+__device__ __forceinline__ void tc_wait_spin(uint32_t mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tTCS_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra TCS_DONE;\n\tbra TCS_WAIT;\n\tTCS_DONE:\n\t}" ::"r"(mbar),
+      "r"(phase)
+      : "memory");
+}
+
 // Non-blocking probe of an mbarrier phase (warp-uniform: lane 0 decides).
 __device__ __forceinline__ bool tc_try_warp(uint32_t mbar, uint32_t phase) {
   uint32_t ok;
@@ -998,13 +1008,13 @@ __device__ __forceinline__ void tc_hit_warp(const ScanArgs &a, bool w0, bool w1,
 // Flusher warp: drains the ring into the global candidate lists (4 entries
 // per lane per round, their slot claims in flight together) and tightens the
 // global bound M of a query from the histogram every bound_every appends.
-__device__ __forceinline__ void tc_flusher(const ScanArgs &a) {
+__device__ __forceinline__ void tc_flusher(const ScanArgs &a, int done_target = 1) {
   const int lane = threadIdx.x & 31;
   unsigned tail = 0;
   for (;;) {
     const unsigned head = *(volatile unsigned *)&g_tc.head;
     if (head == tail) {
-      if (*(volatile int *)&g_tc.done && *(volatile unsigned *)&g_tc.head == tail) break;
+      if (*(volatile int *)&g_tc.done >= done_target && *(volatile unsigned *)&g_tc.head == tail) break;
       __nanosleep(200);
       continue;
     }
@@ -1059,41 +1069,99 @@ __device__ __forceinline__ void tc_flusher(const ScanArgs &a) {
   }
 }
 
-// Expand sub-quantizers [j0, j0 + MH) of code c of its chunk into the A
-// operand in TMEM: the thread's own lane (= A row, the code's position in
-// the tile), 4 columns (16 one-hot bytes, byte k of the sub-quantizer at
-// column k / 4, byte k % 4) per sub-quantizer, from column a_col. Word w of
-// sub-code x is 1 << (8 x - 32 w) when 0 <= 8 x - 32 w < 32, else 0: PTX
-// shl clamps shift amounts >= 32 (a negative difference reads as a large
-// unsigned amount) to a zero result.
-__device__ __forceinline__ uint32_t tc_shl(uint32_t s) {
-  uint32_t r;
-  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(1u), "r"(s));
-  return r;
-}
-
+// Expand MH sub-quantizers of one code into the A operand in TMEM: the
+// thread's own lane (= A row, the code's position in the tile), 16 columns
+// per group of four sub-quantizers, from column a_col. The source is the
+// code-major copy of the codes (qadc_b200_index::codes_cm): 16 bits = the
+// four sub-codes of one group, i.e. a ready PRMT selector. Word e of a group
+// is PRMT(pool_e, selector): byte i = 1 iff sub-code i of the group equals e
+// (pool_e = the 8-byte constant with byte e & 7 set to 1; entries 8..15 use
+// the selector with bit 3 of every nibble flipped, and a nibble >= 8 reads
+// the sign of a pool byte = 0). One PRMT per 32-bit TMEM cell, against ~2.4
+// shift / add instructions per cell when the one-hot bytes are built from
+// the interleaved words. The K order this produces — byte (16 (4 g) + 4 e +
+// i) = entry e of sub-quantizer 4 g + i — is matched by the B staging.
 template <int MH>
-__device__ __forceinline__ void tc_expand(uint32_t a_col, const uint32_t (&cw)[MH], int c) {
-  const int sh = 4 * (c & 7);
+__device__ __forceinline__ void tc_expand_cm(uint32_t a_col, const uint32_t (&cw)[(MH + 7) / 8]) {
 #pragma unroll
-  for (int j = 0; j < MH; j += 4) {
+  for (int gi = 0; gi < MH / 4; gi++) {
+    const uint32_t sel = (gi & 1) ? (cw[gi / 2] >> 16) : cw[gi / 2];
+    const uint32_t selx = sel ^ 0x8888u;
     uint32_t r[16];
 #pragma unroll
-    for (int jj = 0; jj < 4; jj++) {
-      const uint32_t s8 = ((cw[j + jj] >> sh) << 3) & 0x78u;
-      r[4 * jj + 0] = tc_shl(s8);
-      r[4 * jj + 1] = tc_shl(s8 - 32u);
-      r[4 * jj + 2] = tc_shl(s8 - 64u);
-      r[4 * jj + 3] = tc_shl(s8 - 96u);
+    for (int e = 0; e < 16; e++) {
+      const uint32_t one = 1u << (8 * (e & 3));
+      const uint32_t sx = e < 8 ? sel : selx;
+      r[e] = (e & 4) ? prmt(0u, one, sx) : prmt(one, 0u, sx);
     }
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-        "%13,%14,%15,%16};" ::"r"(a_col + 4 * j),
+        "%13,%14,%15,%16};" ::"r"(a_col + 16 * gi),
         "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
         "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
         "r"(r[15])
         : "memory");
   }
+}
+
+// The code-major words of sub-quantizers [j0, j0 + MH) of code c of chunk g
+// (MH = 4: the group's 16 bits moved to the low half).
+template <int MC, int MH>
+__device__ __forceinline__ void tc_load_cm(const ScanArgs &a, int64_t g, int c, int j0,
+                                           uint32_t (&cw)[(MH + 7) / 8]) {
+  if (a.dbg & 4) g = 0;  // timing experiment: every tile reads chunk 0 (L1/L2 resident)
+  const uint32_t *p = a.codes_cm + ((size_t)g * kChunkCodes + c) * (MC / 8) + j0 / 8;
+#pragma unroll
+  for (int i = 0; i < (MH + 7) / 8; i++) cw[i] = __ldg(p + i);
+  if (MH == 4) cw[0] >>= (j0 & 4) * 4;
+}
+
+// 4 x 4 byte transpose: o[ee] byte i = a[i] byte ee.
+__device__ __forceinline__ void tc_transpose4(const uint32_t (&a)[4], uint32_t (&o)[4]) {
+  const uint32_t t0 = prmt(a[0], a[1], 0x5140u), t1 = prmt(a[0], a[1], 0x7362u);
+  const uint32_t u0 = prmt(a[2], a[3], 0x5140u), u1 = prmt(a[2], a[3], 0x7362u);
+  o[0] = prmt(t0, u0, 0x5410u);
+  o[1] = prmt(t0, u0, 0x7632u);
+  o[2] = prmt(t1, u1, 0x5410u);
+  o[3] = prmt(t1, u1, 0x7632u);
+}
+
+// nr packed registers (2 accumulator columns each, 16-bit halves) of the
+// thread's TMEM lane from column taddr: only the item's query columns are
+// read (TMEM reads cost ~64 B / cycle per SM: with the few queries of an
+// inverted list, reading all 64 columns of a part was the tile's longest
+// step). Registers past nr are zero.
+__device__ __forceinline__ void tc_ldp(uint32_t taddr, int nr, uint32_t *v) {
+  if (nr > 16) {
+    tc_ld64p(taddr, v);
+  } else if (nr > 8) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+        "%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 16; i < 32; i++) v[i] = 0;
+  } else {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 8; i < 32; i++) v[i] = 0;
+  }
+}
+
+// (k_scan_tc2 / k_scan_tc2i: interleaved source)
+// Word w of sub-code x is 1 << (8 x - 32 w) when 0 <= 8 x - 32 w < 32, else
+// 0: PTX shl clamps shift amounts >= 32 to a zero result.
+__device__ __forceinline__ uint32_t tc_shl(uint32_t s) {
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(1u), "r"(s));
+  return r;
 }
 
 template <int MC, int MH>
@@ -1127,19 +1195,31 @@ __device__ __forceinline__ void tc_sync(int t) {
 //    while MMA(t) runs, wait for MMA(t), read its sums, then arrive on tile
 //    t + 1's named barrier (2 / 3 alternating). They never wait for each
 //    other inside an item;
-//  * warp 4G + 1 (MMA): per tile, bar.sync on the tile's named barrier (all
-//    compute threads expanded it and finished reading D), then one elected
-//    lane issues the m/2 MMAs (N = the item's queries, up to 256) and
-//    commits to the mbarrier.
+//  * warps 4G + 1 .. 4G + kMmaWarps (MMA): per tile, bar.sync on the tile's
+//    named barrier (all compute threads expanded it, finished reading D and
+//    zeroed it), then one elected lane per warp issues its share of the m/2
+//    MMAs (k-steps mw, mw + kMmaWarps, ...; N = the item's queries, up to
+//    256) and commits to the mbarrier (one arrival per MMA warp). ONE warp
+//    issues at most one tcgen05.mma per ~70-78 cycles whatever its shape
+//    (tools/tc_kind_bench: every kind, M 64 / 128, N 16..128, A in TMEM or
+//    SMEM), while the tensor pipe needs N / 2 cycles: with few queries per
+//    list (IVF) a single issuing warp is the bottleneck (16 x 78 cycles per
+//    128 codes); four issuing warps reach the pipe's own rate from N = 64
+//    (32 cycles per MMA) and 19.5 cycles at N = 16. The MMAs of a tile come
+//    from several warps in no fixed order, so all of them ACCUMULATE into a
+//    D the compute threads zeroed after reading the previous tile (int32
+//    sums: order-independent).
 //  D is single-buffered at N = 256: one MMA instruction costs ~77 cycles of
 //  issue for any N <= 128 but 128 cycles of execution at N = 256
 //  (tools/tc_mma_bench: 3.79 vs 4.59 POP/s back to back), so 256 queries per
 //  instruction beat double-buffering two 128-query accumulators;
 //  * warp 4G (flusher): drains the survivor ring (tc_flusher).
+constexpr int kMmaWarps = 4;
 template <int MC, int G>
-__global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_constant__ ScanArgs a) {
+__global__ void __launch_bounds__(128 * G + 32 + 32 * kMmaWarps, 1)
+k_scan_tc(const __grid_constant__ ScanArgs a) {
   constexpr int K = 16 * MC, SBO = 8 * K, MH = MC / G;
-  constexpr int NT = 128 * G, NB = NT + 32;  // compute threads; + the MMA warp
+  constexpr int NT = 128 * G, NB = NT + 32 * kMmaWarps;  // compute threads; + the MMA warps
   constexpr int kCPT = kTcNQ / G;             // accumulator columns per compute thread
   static_assert(kCPT % 64 == 0, "64-column packed TMEM loads");
   static_assert(MH % 4 == 0 && kTcNQ % (32 * G) == 0 && 4 * G <= 16, "tile split");
@@ -1160,7 +1240,7 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar0), "n"(kMmaWarps));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar0 + 8));
     asm volatile("fence.mbarrier_init.release.cluster;");
     s.item = atomicAdd(a.item_counter, 1);
@@ -1175,15 +1255,17 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
   if (w == 4 * G) {
     tc_flusher(a);
   } else {
-  const bool mma_warp = w == 4 * G + 1;
+  const bool mma_warp = w > 4 * G;
+  const int mw = w - (4 * G + 1);  // MMA warp index
   const uint32_t tmem = s.tmem;
   const uint32_t t_row = tmem + ((uint32_t)((w & 3) * 32) << 16);
   const int n_items = *a.n_items;
   uint32_t ph0 = 0;
   if (!mma_warp) {
-    // zero this thread's accumulator columns once: columns an item's MMA
-    // does not write (>= its N) then always hold real sums (< 2^13) from an
-    // earlier item, which the SWAR test compares against t = -1
+    // zero this thread's accumulator columns: every MMA accumulates, and a
+    // thread zeroes the columns it read again before the next tile's MMAs
+    // are released; columns an item's MMAs do not write (>= its N) stay 0,
+    // which the SWAR test compares against t = -1
     const uint32_t z[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int c = 0; c < kCPT; c += 16)
@@ -1203,13 +1285,36 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
     const int nq = it.pair_count;
     const int64_t c0g = it.chunk_begin;
     const int64_t ntiles = 2 * (it.chunk_end - it.chunk_begin);
+    const int n_mma = max(16, (nq + 15) & ~15);  // MMA N: the item's queries, rounded to 16
     if (!mma_warp) {
       // ---- stage the item's tables (B operand) and per-query state ----
-      for (int e = tid; e < kTcNQ * MC; e += NT) {
-        const int q = e / MC, j = e - q * MC;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (q < nq) v = ((const uint4 *)a.qt)[(size_t)a.pair_t[it.pair_begin + q] * MC + j];
-        *(uint4 *)(sB + (q >> 3) * SBO + j * 128 + (q & 7) * 16) = v;
+      // K order of tc_expand: per group of four sub-quantizers, entry-major
+      // (a 4 x 4 byte transpose of the group's tables); only the rows the
+      // MMAs read (< n_mma) are written
+      for (int e = tid; e < n_mma * (MC / 4); e += NT) {
+        const int q = e / (MC / 4), g4 = e - q * (MC / 4);
+        uint4 in[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) in[i] = make_uint4(0, 0, 0, 0);
+        if (q < nq) {
+          const uint4 *src = (const uint4 *)a.qt + (size_t)a.pair_t[it.pair_begin + q] * MC + 4 * g4;
+#pragma unroll
+          for (int i = 0; i < 4; i++) in[i] = src[i];
+        }
+        const uint32_t ax[4] = {in[0].x, in[1].x, in[2].x, in[3].x};
+        const uint32_t ay[4] = {in[0].y, in[1].y, in[2].y, in[3].y};
+        const uint32_t az[4] = {in[0].z, in[1].z, in[2].z, in[3].z};
+        const uint32_t aw[4] = {in[0].w, in[1].w, in[2].w, in[3].w};
+        uint32_t o[4];
+        uint8_t *dst = sB + (q >> 3) * SBO + (4 * g4) * 128 + (q & 7) * 16;
+        tc_transpose4(ax, o);
+        *(uint4 *)(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+        tc_transpose4(ay, o);
+        *(uint4 *)(dst + 128) = make_uint4(o[0], o[1], o[2], o[3]);
+        tc_transpose4(az, o);
+        *(uint4 *)(dst + 256) = make_uint4(o[0], o[1], o[2], o[3]);
+        tc_transpose4(aw, o);
+        *(uint4 *)(dst + 384) = make_uint4(o[0], o[1], o[2], o[3]);
       }
       if (tid < kTcNQ) {
         const int q = tid;
@@ -1236,7 +1341,6 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
     tc_bar_all<NB>();  // B and the query state are staged
     if (tid == 0) s.item = atomicAdd(a.item_counter, 1);  // claimed ahead (read after the item's end barrier)
     if (mma_warp) {
-      const int n_mma = max(16, (nq + 15) & ~15);  // MMA N: the item's queries, rounded to 16
       const uint32_t idesc =
           (2u << 4) | ((uint32_t)(n_mma >> 3) << 17) | ((uint32_t)(kTcCodes >> 4) << 24);
       for (int64_t t = 0; t < ntiles; t++) {
@@ -1246,13 +1350,13 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
         if ((tid & 31) == 0) {
 #pragma unroll
           for (int ks = 0; ks < K / 32; ks++) {
+            if (ks % kMmaWarps != mw) continue;
             const uint32_t ta = tmem + kA0 + buf * kACols + ks * 8;  // A from TMEM (K = 32 bytes = 8 columns)
             const uint64_t db = tc_smem_desc(sB_a + ks * 256, SBO);
-            const uint32_t acc = ks > 0 ? 1u : 0u;
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                 "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
-                "r"(ta), "l"(db), "r"(idesc), "r"(acc));
+                "r"(ta), "l"(db), "r"(idesc), "r"(1u));
           }
           asm volatile(
               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -1262,13 +1366,13 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
         __syncwarp();
       }
     } else {
-      uint32_t cw[MH];
+      uint32_t cw[(MH + 7) / 8];
       // this thread's A columns (its lane quarter, its part of the K range)
       const uint32_t a_lane = tmem + ((uint32_t)((w & 3) * 32) << 16) + kA0 + (uint32_t)(j0 * 4);
       // prologue: expand tile 0 into A[0], load tile 1's words
-      tc_load<MC, MH>(a, c0g, row, j0, cw);
-      tc_expand<MH>(a_lane, cw, row);
-      if (ntiles > 1) tc_load<MC, MH>(a, c0g, kTcCodes + row, j0, cw);
+      tc_load_cm<MC, MH>(a, c0g, row, j0, cw);
+      tc_expand_cm<MH>(a_lane, cw);
+      if (ntiles > 1) tc_load_cm<MC, MH>(a, c0g, kTcCodes + row, j0, cw);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       tc_arrive<NB>(0);
@@ -1284,10 +1388,9 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
         // (MMA(t - 1), its last reader, completed before this warp read
         // tile t - 1) ----
         if (t + 1 < ntiles) {
-          if (!(a.dbg & 2)) tc_expand<MH>(a_lane + (uint32_t)((t + 1) & 1) * kACols, cw,
-                                           (int)((t + 1) & 1) * kTcCodes + row);
+          if (!(a.dbg & 2)) tc_expand_cm<MH>(a_lane + (uint32_t)((t + 1) & 1) * kACols, cw);
           if (t + 2 < ntiles)
-            tc_load<MC, MH>(a, c0g + ((t + 2) >> 1), (int)((t + 2) & 1) * kTcCodes + row, j0, cw);
+            tc_load_cm<MC, MH>(a, c0g + ((t + 2) >> 1), (int)((t + 2) & 1) * kTcCodes + row, j0, cw);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         // ---- tile t: copy this thread's sums out of TMEM and release D
@@ -1298,27 +1401,47 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
         asm volatile("tcgen05.fence::after_thread_sync;");
         // (columns >= the MMA's N hold earlier items' sums: see the zeroing
         // above)
+        // (warps whose query columns lie past the item's N have nothing to
+        // read: with few queries per list only part 0 runs the epilogue)
+        const bool has_cols = col0 < n_mma;
         uint32_t v[kCPT / 2];
+        if (has_cols) {
 #pragma unroll
-        for (int l = 0; l < kCPT / 64; l++) tc_ld64p(t_row + col0 + 64 * l, v + 32 * l);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          for (int l = 0; l < kCPT / 64; l++)
+            tc_ldp(t_row + col0 + 64 * l, min(64, max(0, n_mma - col0 - 64 * l)) / 2, v + 32 * l);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          // zero the columns just read (the next tile's MMAs accumulate)
+          const uint32_t z = 0;
+#pragma unroll
+          for (int c = 0; c < kCPT; c += 16)
+            if (col0 + c < n_mma)
+              asm volatile(
+                  "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+                  "%1,%1,%1,%1};" ::"r"(t_row + col0 + c), "r"(z)
+                  : "memory");
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
         asm volatile("tcgen05.fence::before_thread_sync;");
-        if (t + 1 < ntiles) tc_arrive<NB>((int)(t + 1));  // A(t + 1) written, D read
+        if (t + 1 < ntiles) tc_arrive<NB>((int)(t + 1));  // A(t + 1) written, D read and zeroed
         // SWAR survivor test on packed pairs: (t + 0x8000) - s keeps bit
         // 15 of its half iff s <= t (halves never borrow: s < 2^13 and
         // t + 0x8000 in [0x7fff, 0x80fe])
         const uint4 *T = (const uint4 *)&s.thr16[col0];
         uint32_t any = 0;
+        if (has_cols) {
 #pragma unroll
-        for (int i = 0; i < kCPT / 2 && !(a.dbg & 8); i += 4) {
-          const uint4 tt = T[i / 4];
-          any |= (tt.x - v[i]) | (tt.y - v[i + 1]) | (tt.z - v[i + 2]) | (tt.w - v[i + 3]);
+          for (int i = 0; i < kCPT / 2 && !(a.dbg & 8); i += 4) {
+            if (2 * i >= n_mma - col0) break;
+            const uint4 tt = T[i / 4];
+            any |= (tt.x - v[i]) | (tt.y - v[i + 1]) | (tt.z - v[i + 2]) | (tt.w - v[i + 3]);
+          }
         }
         // survivors (rare once the bounds converge): the warp handles its
         // lanes with survivors one at a time, each of the lane's packed
         // sum registers passed through shared memory to a lane of its own
-        unsigned todo = __ballot_sync(kFull, (any & 0x80008000u) && ((vb_t >> (c_t & 7)) & 1u) &&
-                                                 !(a.dbg & 1));
+        unsigned todo = has_cols ? __ballot_sync(kFull, (any & 0x80008000u) &&
+                                                            ((vb_t >> (c_t & 7)) & 1u) && !(a.dbg & 1))
+                                 : 0u;
         if (todo) {
           const int lane = tid & 31;
           uint32_t *xf = s.xfer[w][0];
@@ -1359,6 +1482,279 @@ __global__ void __launch_bounds__(128 * G + 64, 1) k_scan_tc(const __grid_consta
   __syncthreads();
   if (w == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s.tmem), "n"(kCols));
+}
+
+
+// ---- tensor-core scan for inverted lists with few queries (k_scan_tcw) ----
+//
+// IVF batches put 10-40 (query, list) pairs on a list (configs[4]: 93 % of
+// the scanned codes sit in lists probed by <= 32 queries of the batch), so
+// the MMA itself is short (N = 16 or 32: 8-16 cycles per K = 32 step) and the
+// tile's cost is the one-hot expansion and the latency of the expand -> MMA
+// -> read chain. k_scan_tc runs ONE tile at a time on all its warps, so
+// every thread repeats the tile's fixed work (addresses, barriers, bound
+// refresh) for a quarter of a code; here a CTA holds kWG independent
+// warpgroups, each scanning its own work item (list, <= 32 queries, chunk
+// range) tile by tile:
+//   * thread = one code of the 128-code tile: ONE 16-byte load of its
+//     code-major row (coalesced 512 B per warp), m / 4 x 16 PRMT one-hot
+//     words written to its TMEM lane (tc_expand_cm);
+//   * warpgroup barrier; each of the 4 warps issues m / 8 of the tile's
+//     m / 2 MMAs (a single warp cannot issue faster than one MMA per ~70
+//     cycles; all MMAs accumulate into the zeroed D) and commits to the
+//     warpgroup's mbarrier;
+//   * every thread reads its code's N sums (16-bit packed), zeroes them and
+//     runs the SWAR threshold test; survivors go through the shared ring to
+//     the flusher warp (tc_hit_warp / tc_flusher, as k_scan_tc).
+// While one warpgroup waits for its MMAs the others expand: the ALU pipe
+// (PRMT) and the tensor pipe overlap without any cross-warpgroup barrier.
+// TMEM per warpgroup: D (32 columns) + A (4 m columns), single-buffered.
+constexpr int kWG = 3;        // warpgroups per CTA (3 x (32 + 128) <= 512 TMEM columns)
+constexpr int kTcwNQ = 32;    // queries per item (MMA N = 16 or 32)
+struct TcwSmem {
+  uint64_t mbar[kWG];
+  int item[kWG];
+};
+__shared__ TcwSmem g_tcw;
+
+template <int MC>
+__global__ void __launch_bounds__(128 * kWG + 32, 1) k_scan_tcw(const __grid_constant__ ScanArgs a) {
+  constexpr int K = 16 * MC, SBO = 8 * K, WPC = MC / 8;
+  constexpr uint32_t kCols = 512, kWgCols = kTcwNQ + K / 4;
+  static_assert(kWG * kWgCols <= kCols, "TMEM budget");
+  extern __shared__ __align__(16) unsigned char dsm[];  // B: [kWG][kTcwNQ rows][K]
+  TcSmem &s = g_tc;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s.tmem)),
+                 "n"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int g = 0; g < kWG; g++)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(&g_tcw.mbar[g])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    s.done = 0;
+    s.head = 0;
+    s.tail = 0;
+  }
+  for (int i = tid; i < kRing; i += blockDim.x) s.ring[i].query = -1;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (w == 4 * kWG) {
+    tc_flusher(a, kWG);
+  } else {
+    const int wg = w >> 2, wt = tid & 127, wq = w & 3;  // warpgroup, thread in it, warp in it
+    const int qb = wg * kTcwNQ;                          // the warpgroup's slice of the query-state arrays
+    uint8_t *sB = dsm + (size_t)wg * kTcwNQ * K;
+    const uint32_t sB_a = (uint32_t)__cvta_generic_to_shared(sB);
+    const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&g_tcw.mbar[wg]);
+    const uint32_t tmem = s.tmem;
+    const uint32_t t_d = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)wg * kWgCols;  // this thread's D row
+    const uint32_t t_a = t_d + kTcwNQ;                                                  // its A row
+    const uint32_t d_mma = tmem + (uint32_t)wg * kWgCols, a_mma = d_mma + kTcwNQ;
+    const int n_items = *a.n_items;
+    uint32_t ph = 0;
+    {  // D starts zeroed (every MMA accumulates)
+      const uint32_t z = 0;
+#pragma unroll
+      for (int c = 0; c < kTcwNQ; c += 16)
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+            "%1,%1,%1,%1};" ::"r"(t_d + c), "r"(z)
+            : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    auto wg_sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(wg + 1) : "memory"); };
+    if (wt == 0) g_tcw.item[wg] = atomicAdd(a.item_counter, 1);
+    wg_sync();
+    for (;;) {
+      const int item = g_tcw.item[wg];
+      if (item >= n_items) break;
+      const WorkItem it = a.items[item];
+      const int nq = it.pair_count;
+      const int64_t c0g = it.chunk_begin;
+      const int64_t ntiles = 2 * (it.chunk_end - it.chunk_begin);
+      const int n_mma = nq > 16 ? 32 : 16;
+      // ---- stage the item's tables (B operand, tc_expand_cm's K order) and query state ----
+      for (int e = wt; e < n_mma * (MC / 4); e += 128) {
+        const int q = e / (MC / 4), g4 = e - q * (MC / 4);
+        uint4 in[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) in[i] = make_uint4(0, 0, 0, 0);
+        if (q < nq) {
+          const uint4 *src = (const uint4 *)a.qt + (size_t)a.pair_t[it.pair_begin + q] * MC + 4 * g4;
+#pragma unroll
+          for (int i = 0; i < 4; i++) in[i] = src[i];
+        }
+        const uint32_t ax[4] = {in[0].x, in[1].x, in[2].x, in[3].x};
+        const uint32_t ay[4] = {in[0].y, in[1].y, in[2].y, in[3].y};
+        const uint32_t az[4] = {in[0].z, in[1].z, in[2].z, in[3].z};
+        const uint32_t aw[4] = {in[0].w, in[1].w, in[2].w, in[3].w};
+        uint32_t o[4];
+        uint8_t *dst = sB + (q >> 3) * SBO + (4 * g4) * 128 + (q & 7) * 16;
+        tc_transpose4(ax, o);
+        *(uint4 *)(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+        tc_transpose4(ay, o);
+        *(uint4 *)(dst + 128) = make_uint4(o[0], o[1], o[2], o[3]);
+        tc_transpose4(az, o);
+        *(uint4 *)(dst + 256) = make_uint4(o[0], o[1], o[2], o[3]);
+        tc_transpose4(aw, o);
+        *(uint4 *)(dst + 384) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+      if (wt < kTcwNQ) {
+        const int q = wt;
+        int thr = -1;
+        unsigned mb = 0;
+        if (q < nq) {
+          const int pi = it.pair_begin + q;
+          const int query = a.pair_q[pi], t = a.pair_t[pi];
+          s.query[qb + q] = query;
+          s.qmin[qb + q] = a.qmin_f[t];
+          s.delta[qb + q] = a.delta_f[t];
+          mb = *(volatile unsigned *)&a.M_bits[query];
+          thr = q_threshold(__uint_as_float(mb), s.qmin[qb + q], s.delta[qb + q]);
+        } else {
+          s.query[qb + q] = 0;
+          s.qmin[qb + q] = 0.f;
+          s.delta[qb + q] = 0.f;
+        }
+        s.thr16[qb + q] = (uint16_t)(thr + 0x8000);
+        s.mc[qb + q] = mb;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      wg_sync();  // B and the query state are staged; everyone has read g_tcw.item
+      if (wt == 0) g_tcw.item[wg] = atomicAdd(a.item_counter, 1);  // claimed ahead (read after the item's last barrier)
+      const uint32_t idesc =
+          (2u << 4) | ((uint32_t)(n_mma >> 3) << 17) | ((uint32_t)(kTcCodes >> 4) << 24);
+      uint32_t cw[WPC];
+      {
+        const uint32_t *p = a.codes_cm + ((size_t)c0g * kChunkCodes + wt) * WPC;
+        if (WPC == 4) {
+          const uint4 v4 = __ldg((const uint4 *)p);
+          cw[0] = v4.x; cw[1] = v4.y; cw[WPC - 2] = v4.z; cw[WPC - 1] = v4.w;
+        } else {
+          const uint2 v2 = __ldg((const uint2 *)p);
+          cw[0] = v2.x; cw[WPC - 1] = v2.y;
+        }
+      }
+      for (int64_t t = 0; t < ntiles; t++) {
+        unsigned mpre = 0;
+        if (wt < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[qb + wt]];  // lands during the tile
+        const int c_t = (int)(t & 1) * kTcCodes + wt;
+        const int64_t g_t = c0g + (t >> 1);
+        const uint32_t vb_t = __ldg(a.valid + g_t * 32 + (c_t >> 3));  // read only by the survivor path
+        // ---- expand this thread's code into its A row; fetch the next tile's row ----
+        if (!(a.dbg & 2)) tc_expand_cm<MC>(t_a, cw);
+        if (t + 1 < ntiles) {
+          const uint32_t *p = a.codes_cm + ((size_t)(c0g + ((t + 1) >> 1)) * kChunkCodes +
+                                            (int)((t + 1) & 1) * kTcCodes + wt) * WPC;
+          if (WPC == 4) {
+            const uint4 v4 = __ldg((const uint4 *)p);
+            cw[0] = v4.x; cw[1] = v4.y; cw[WPC - 2] = v4.z; cw[WPC - 1] = v4.w;
+          } else {
+            const uint2 v2 = __ldg((const uint2 *)p);
+            cw[0] = v2.x; cw[WPC - 1] = v2.y;
+          }
+          if (lane == 0 && t + 4 < ntiles)  // the warp's 32 rows of tile t + 4 into L2
+            prefetch_l2(a.codes_cm + ((size_t)(c0g + ((t + 4) >> 1)) * kChunkCodes +
+                                      (int)((t + 4) & 1) * kTcCodes + (wt & ~31)) * WPC, 128u * WPC);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // A row written, D row zeroed
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        wg_sync();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0 && !(a.dbg & 128)) {
+#pragma unroll
+          for (int ks = 0; ks < K / 32; ks++) {
+            if ((ks & 3) != wq) continue;
+            const uint32_t ta = a_mma + ks * 8;  // A from TMEM (K = 32 bytes = 8 columns)
+            const uint64_t db = tc_smem_desc(sB_a + ks * 256, SBO);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_mma),
+                "r"(ta), "l"(db), "r"(idesc), "r"(1u));
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
+              : "memory");
+        }
+        __syncwarp();
+        if (!(a.dbg & 128)) {
+          if (a.dbg & 256) tc_wait(mbar, ph);
+          else tc_wait_spin(mbar, ph);
+          ph ^= 1;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        // ---- this code's sums: read, zero, test ----
+        uint32_t v[32];
+        tc_ldp(t_d, n_mma / 2, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        {
+          const uint32_t z = 0;
+#pragma unroll
+          for (int c = 0; c < kTcwNQ; c += 16)
+            if (c < n_mma)
+              asm volatile(
+                  "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+                  "%1,%1,%1,%1};" ::"r"(t_d + c), "r"(z)
+                  : "memory");
+        }
+        const uint4 *T = (const uint4 *)&s.thr16[qb];
+        uint32_t any = 0;
+#pragma unroll
+        for (int i = 0; i < kTcwNQ / 2; i += 4) {
+          if (2 * i >= n_mma) break;
+          const uint4 tt = T[i / 4];
+          any |= (tt.x - v[i]) | (tt.y - v[i + 1]) | (tt.z - v[i + 2]) | (tt.w - v[i + 3]);
+        }
+        unsigned todo = __ballot_sync(kFull, (any & 0x80008000u) && ((vb_t >> (c_t & 7)) & 1u) &&
+                                                 !(a.dbg & 1));
+        if (todo) {
+          uint32_t *xf = s.xfer[w][0];
+          const int64_t pos0 = g_t * kChunkCodes + (int64_t)(c_t - lane);
+          while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            if (lane == src) {
+#pragma unroll
+              for (int i = 0; i < kTcwNQ / 2; i += 4)
+                *(uint4 *)&xf[i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            }
+            __syncwarp();
+            const uint32_t vv = lane < kTcwNQ / 2 ? xf[lane] : 0u;
+            const int q = qb + 2 * (lane & (kTcwNQ / 2 - 1));
+            const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
+            __syncwarp();
+            const bool on = lane < n_mma / 2;
+            tc_hit_warp(a, on && (x & 0x8000u) != 0, on && (x & 0x80000000u) != 0, q, vv, pos0 + src);
+          }
+        }
+        if (wt < nq && mpre < s.mc[qb + wt]) {  // bounds tightened by the flusher or other CTAs
+          s.mc[qb + wt] = mpre;
+          const int th = q_threshold(__uint_as_float(mpre), s.qmin[qb + wt], s.delta[qb + wt]);
+          if (th + 0x8000 < (int)s.thr16[qb + wt]) s.thr16[qb + wt] = (uint16_t)(th + 0x8000);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      wg_sync();  // end of item: every tile read, g_tcw.item holds the next item
+    }
+    if (wt == 0) atomicAdd(&s.done, 1);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (w == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s.tmem), "n"(kCols));
+}
+
+template <int MC>
+void launch_tcw(const ScanArgs &a, int nsm, cudaStream_t st) {
+  const size_t smem = (size_t)kWG * kTcwNQ * 16 * MC;
+  cudaFuncSetAttribute(k_scan_tcw<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_scan_tcw<MC><<<nsm, 128 * kWG + 32, smem, st>>>(a);
 }
 
 
@@ -2134,7 +2530,7 @@ void launch_tc_g(const ScanArgs &a, int nsm, cudaStream_t st) {
   cudaFuncSetAttribute(k_scan_tc<MC, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   // TMEM: every resident CTA holds all 512 columns of its SM (A and D,
   // double-buffered): one CTA per SM
-  k_scan_tc<MC, G><<<nsm, 128 * G + 64, smem, st>>>(a);
+  k_scan_tc<MC, G><<<nsm, 128 * G + 32 + 32 * kMmaWarps, smem, st>>>(a);
 }
 
 template <int MC>
@@ -2387,11 +2783,16 @@ bool scan_use_tc(int m, bool prmt) {
   return !prmt && env != 0 && (m == 16 || m == 32);
 }
 
-int scan_tile_queries(int m, bool prmt) { return scan_use_tc(m, prmt) ? kTcNQ : scan_qt_per_cta(m); }
+int scan_tile_queries(int m, bool prmt, bool tcw) {
+  return scan_use_tc(m, prmt) ? (tcw ? kTcwNQ : kTcNQ) : scan_qt_per_cta(m);
+}
 
 void launch_scan(const ScanArgs &a, int nsm, cudaStream_t st, bool prmt) {
   if (scan_use_tc(a.m, prmt)) {
-    if (a.pair_cta) {
+    if (a.tcw) {
+      if (a.m == 32) launch_tcw<32>(a, nsm, st);
+      else launch_tcw<16>(a, nsm, st);
+    } else if (a.pair_cta) {
       if (a.m == 32) launch_tc2<32>(a, nsm, st);
       else launch_tc2<16>(a, nsm, st);
     } else if (a.m == 32) launch_tc<32>(a, nsm, st);

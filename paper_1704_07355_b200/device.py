@@ -113,10 +113,10 @@ class DeviceIndex:
         flags = _native.LUT_IN if lut is not None else 0
         if not with_fsat:
             flags |= _native.NO_FSAT
-        if scan not in ("auto", "prmt", "tc", "tc1"):
+        if scan not in ("auto", "prmt", "tc", "tc1", "tcw"):
             raise ValueError(f"unknown scan kernel {scan!r}")
         flags |= {"auto": 0, "prmt": _native.SCAN_PRMT, "tc": _native.SCAN_TC,
-                  "tc1": _native.SCAN_TC | _native.SCAN_TC1}[scan]
+                  "tc1": _native.SCAN_TC | _native.SCAN_TC1, "tcw": _native.SCAN_TCW}[scan]
         if isinstance(queries, np.ndarray):
             q = _np(queries, np.float32).reshape(-1, self.d)
             nq = q.shape[0]
@@ -201,7 +201,7 @@ class DeviceIndex:
         dist = torch.empty((nq, R), dtype=torch.float32, device=dev)
         cnt = torch.empty(nq, dtype=torch.int32, device=dev)
         flags = {"auto": 0, "prmt": _native.SCAN_PRMT, "tc": _native.SCAN_TC,
-                 "tc1": _native.SCAN_TC | _native.SCAN_TC1}[scan]
+                 "tc1": _native.SCAN_TC | _native.SCAN_TC1, "tcw": _native.SCAN_TCW}[scan]
         stats = np.zeros(16, dtype=np.int64)
         _native.check(_native.load_library().qadc_b200_search_scan(
             self._h, nq, R, ma, init, flags, *[_native.dptr(prep[k]) for k in self.PREP_KEYS

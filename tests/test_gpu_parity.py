@@ -525,10 +525,11 @@ def test_ivf_search_vs_oracle_at_scale(gpu, ma):
             luts[i, s_] = orc.compute_tables(cb, orc.rotate(Rm, r))
     oi, od, on, _ = orc.search_batch(qs, cb, Rm, coarse, ma, flat, R, 1000, lut_in=luts,
                                      cells_in=cells)
-    for scan in ("tc", "prmt", "auto"):  # int8 tensor-core scan, PRMT scan, heuristic
+    # int8 tensor-core scans (all warps on one tile / warpgroup-pipelined), PRMT scan, heuristic
+    for scan in ("tc", "tcw", "prmt", "auto"):
         got = idx.search(qs, R, ma=ma, init=1000, lut=luts, cells=cells, scan=scan)
         if scan != "auto":
-            assert got.stats["scan_tc"] == (1 if scan == "tc" else 0)
+            assert got.stats["scan_tc"] == {"tc": 1, "tcw": 2, "prmt": 0}[scan]
         assert np.array_equal(got.ids, oi), scan
         assert np.array_equal(_bits(got.distances), _bits(od)), scan
         assert np.array_equal(got.counts, on), scan
@@ -539,6 +540,60 @@ def test_ivf_search_vs_oracle_at_scale(gpu, ma):
     ni, nd, nn, _ = orc.search_batch(qs, cb, Rm, coarse, ma, flat, R, 1000)
     assert np.array_equal(nat.ids, ni)
     assert np.array_equal(_bits(nat.distances), _bits(nd))
+
+@pytest.mark.parametrize("m,K,n,nq,ma,R", [(32, 48, 60_000, 150, 12, 50), (16, 20, 30_000, 64, 5, 100),
+                                           (32, 300, 40_000, 400, 20, 10)])
+def test_warpgroup_tensor_core_scan_vs_oracle(gpu, m, K, n, nq, ma, R):
+    """k_scan_tcw (IVF lists probed by a few queries each: <= 32 queries per
+    pass, code-major one-hot expansion, MMAs issued by four warps into a
+    zeroed accumulator): ids, fp32 distance bits and counts equal the oracle's
+    and the PRMT scan's on lists of 0..~3000 codes with 1..~40 pairs each
+    (lists with more than 32 pairs take several passes)."""
+    import torch
+
+    from paper_1704_07355_b200 import datagen
+    from paper_1704_07355_b200.device import DeviceIndex
+    from paper_1704_07355_b200.ivf import assign_device, encode_device
+    from paper_1704_07355_b200.qadc import transpose_list
+    from paper_1704_07355_b200.workload import _PQ
+    rng = np.random.default_rng(m + K)
+    d = 128
+    X = datagen.mixture_numpy(datagen.SIFT_LIKE, n, seed=7, stream=2)
+    coarse = X[rng.choice(n, K, replace=False)].copy()
+    Rm = np.linalg.qr(rng.standard_normal((d, d)))[0].astype(np.float32)
+    cb = (rng.standard_normal((m, 16, d // m)) * 8).astype(np.float32)
+    pq = _PQ(cb, Rm)
+    Xd = torch.from_numpy(X).cuda()
+    C = torch.from_numpy(coarse).cuda()
+    lab = assign_device(coarse, Xd)
+    codes = encode_device(pq, Xd - C[lab])
+    order = torch.argsort(lab, stable=True)
+    sizes = torch.bincount(lab, minlength=K)
+    row_off = torch.zeros(K + 1, dtype=torch.int64, device="cuda")
+    row_off[1:] = torch.cumsum(sizes, 0)
+    sc = codes[order].contiguous()
+    idx = DeviceIndex.from_device_rows(d, m, sc, row_off, torch.from_numpy(cb).cuda(),
+                                       rotation=torch.from_numpy(Rm).cuda(), coarse=C, ids=order)
+    sc_np, ord_np, off = sc.cpu().numpy(), order.cpu().numpy(), row_off.cpu().numpy()
+    blocks, ids, boff, count = [], [], [0], []
+    for L in range(K):
+        tl = transpose_list(sc_np[off[L]:off[L + 1]], ord_np[off[L]:off[L + 1]])
+        blocks.append(tl.blocks.reshape(-1))
+        ids.append(tl.ids)
+        boff.append(boff[-1] + tl.blocks.shape[0])
+        count.append(tl.count)
+    flat = (np.concatenate(blocks), np.asarray(boff, np.int64), np.concatenate(ids),
+            np.asarray(count, np.int64))
+    qs = datagen.mixture_numpy(datagen.SIFT_LIKE, nq, seed=7, stream=3)
+    oi, od, on, _ = orc.search_batch(qs, cb, Rm, coarse, ma, flat, R, 1000)
+    qd = torch.from_numpy(qs).cuda()
+    ref = idx.search(qd, R, ma=ma, init=1000, scan="prmt")
+    got = idx.search(qd, R, ma=ma, init=1000, scan="tcw")
+    assert got.stats["scan_tc"] == 2
+    for r in (ref, got):
+        assert np.array_equal(r.ids.cpu().numpy(), oi)
+        assert np.array_equal(_bits(r.distances.cpu().numpy()), _bits(od))
+        assert np.array_equal(r.counts.cpu().numpy(), on)
 
 
 @pytest.mark.parametrize("K,ma", [(300, 1), (300, 64), (300, 300), (5000, 16), (5000, 130),

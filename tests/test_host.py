@@ -50,9 +50,9 @@ def test_search_flags_match_header():
     maintainer binds)."""
     hdr = (ROOT / "include" / "qadc_b200.h").read_text()
     defs = {k: int(v) for k, v in re.findall(r"#define QADC_B200_(\w+) (\d+)u", hdr)}
-    for name in ("HOST_IO", "LUT_IN", "NO_FSAT", "SCAN_PRMT", "SCAN_TC", "SCAN_TC1"):
+    for name in ("HOST_IO", "LUT_IN", "NO_FSAT", "SCAN_PRMT", "SCAN_TC", "SCAN_TC1", "SCAN_TCW"):
         assert defs[name] == getattr(_native, name), name
-    flags = [defs[n] for n in ("HOST_IO", "LUT_IN", "NO_FSAT", "SCAN_PRMT", "SCAN_TC", "SCAN_TC1")]
+    flags = [defs[n] for n in ("HOST_IO", "LUT_IN", "NO_FSAT", "SCAN_PRMT", "SCAN_TC", "SCAN_TC1", "SCAN_TCW")]
     assert len(set(flags)) == len(flags) and all(f & (f - 1) == 0 for f in flags)
 
 

@@ -38,7 +38,7 @@ if os.environ.get("KNOB_CHILD") != "1":
             env[k] = v
         out = subprocess.run([sys.executable, __file__, name, st], env=env, capture_output=True,
                              text=True)
-        print(f"[{st or 'default'}] {out.stdout.strip()} {out.stderr.strip()[-300:]}", flush=True)
+        print(f"[{st or 'default'}] {out.stdout.strip()} {out.stderr.strip()[-1500:]}", flush=True)
     sys.exit(0)
 
 import torch
@@ -50,6 +50,20 @@ d = torch.load(cache)
 index = make_ivf_index(pq, coarse, d["rows"].cuda(), d["ids"].cuda(), d["row_off"].cuda())
 del d
 qs = torch.from_numpy(queries(cfg)).cuda()
+if os.environ.get("KNOB_LIST_STATS") == "1":  # (query, list) pairs per list, weighted by scanned codes
+    import numpy as np
+    ro = torch.load(cache)["row_off"].numpy()
+    sizes = np.diff(ro)
+    cells = index.tables(qs, cfg.R, ma=cfg.nprobe, init=cfg.init)["cells"].cpu().numpy().ravel()
+    pairs = np.bincount(cells, minlength=cfg.K)
+    work = pairs * sizes
+    tot = work.sum()
+    print(f"pairs {cells.size} lists probed {np.count_nonzero(pairs)} codes scanned {tot:.4g} "
+          f"codes in probed lists {sizes[pairs > 0].sum():.4g}", file=sys.stderr)
+    for lo, hi in [(1, 4), (5, 8), (9, 12), (13, 16), (17, 24), (25, 32), (33, 48), (49, 64), (65, 128), (129, 10**9)]:
+        mk = (pairs >= lo) & (pairs <= hi)
+        print(f" {lo}-{hi}: lists {mk.sum()} work {work[mk].sum() / tot:.3f} codes {sizes[mk].sum():.3g} "
+              f"mean {sizes[mk].mean() if mk.any() else 0:.0f};", file=sys.stderr)
 for _ in range(3):
     index.search(qs, cfg.R, ma=cfg.nprobe, init=cfg.init)
 torch.cuda.synchronize()
@@ -62,5 +76,18 @@ for _ in range(5):
     cand += r.stats["candidates"]
 e1.record()
 torch.cuda.synchronize()
+if os.environ.get("KNOB_COMPARE") == "1":  # tensor-core vs PRMT scan on the same index: ids and distance bits
+    out = {}
+    for mode in ("prmt", os.environ.get("KNOB_COMPARE_MODE", "auto")):
+        for _ in range(2):
+            r = index.search(qs, cfg.R, ma=cfg.nprobe, init=cfg.init, scan=mode)
+        out[mode] = (r.ids.clone(), r.distances.clone().view(torch.int32), r.counts.clone(), r.stats["scan_us"] / 1e3,
+                     r.stats["candidates"] / qs.shape[0])
+    a, b = out["prmt"], out[os.environ.get("KNOB_COMPARE_MODE", "auto")]
+    ok_i = (a[0] == b[0]).all(dim=1)
+    ok_d = (a[1] == b[1]).all(dim=1)
+    print(f"compare: prmt scan {a[3]:.2f} ms ({a[4]:.0f} cand/q), {os.environ.get("KNOB_COMPARE_MODE", "auto")} scan {b[3]:.2f} ms ({b[4]:.0f} cand/q); "
+          f"ids exact {int(ok_i.sum())}/{qs.shape[0]}, dist bits exact {int(ok_d.sum())}/{qs.shape[0]}, "
+          f"counts equal {bool((a[2] == b[2]).all())}", file=sys.stderr)
 print(json.dumps({"step_ms": round(e0.elapsed_time(e1) / 5, 3), "scan_ms": round(scan / 5e3, 3),
                   "cand_per_query": round(cand / 5 / qs.shape[0], 1)}))

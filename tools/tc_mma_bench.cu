@@ -9,6 +9,7 @@
 //        2 = A in TMEM, per tile commit, tile t+2 issued after tile t's
 //            commit is observed (the scan's double-buffered chain without
 //            any epilogue work);
+//        6 / 7 = four independent accumulator chains (N <= 64), A in TMEM / SMEM;
 //        4 = as 1, but the tile's K steps alternate between two
 //            accumulators (two independent chains of ksteps / 2);
 //        5 = single accumulator: tile t+1 issued after all 4 warps read
@@ -109,7 +110,23 @@ __global__ void __launch_bounds__(128, 1) k_bench(int N, int ksteps, long long *
       for (int ks = 0; ks < ksteps; ks++) {
         const uint64_t db = desc(sb + ks * 256, 8 * K);
         const uint32_t acc = ks > 0;
-        if (MODE == 4) {
+        if (MODE == 6 || MODE == 7) {
+          // four independent accumulator chains (N <= 64), A in TMEM (6) or SMEM (7)
+          const uint32_t d = tmem + (ks & 3) * 64;
+          const uint32_t acc4 = ks > 3;
+          if (MODE == 6) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                "r"(a_t + buf * (K / 4) + ks * 8), "l"(db), "r"(idesc), "r"(acc4));
+          } else {
+            const uint64_t da = desc(sa + ks * 256, 8 * K);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc4));
+          }
+        } else if (MODE == 4) {
           const uint32_t d = tmem + (ks & 1) * 128;
           const uint32_t acc4 = ks > 1;
           asm volatile(
@@ -147,7 +164,7 @@ __global__ void __launch_bounds__(128, 1) k_bench(int N, int ksteps, long long *
     for (int b = 0; b < 2; b++) {
       if (MODE >= 2 && MODE <= 3) wait_mb(mb + 8 * ((kTiles - 2 + b) & 1), ph[(kTiles - 2 + b) & 1]);
     }
-    if (MODE < 2 || MODE == 4) {
+    if (MODE < 2 || MODE == 4 || MODE == 6 || MODE == 7) {
       // every commit arrived once per tile: wait for the last phase of each buffer
       wait_mb(mb, (kTiles / 2 - 1) & 1);
       wait_mb(mb + 8, (kTiles / 2 - 1) & 1);
@@ -195,7 +212,11 @@ void run(int N, int ksteps, int sms) {
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  run<2>(128, 16, sms);
-  run<2>(256, 16, sms);
+  const int ns[5] = {16, 32, 64, 128, 256};
+  for (int i = 0; i < 5; i++) run<0>(ns[i], 16, sms);   // A, B in SMEM, one chain
+  for (int i = 0; i < 5; i++) run<1>(ns[i], 16, sms);   // A in TMEM, one chain
+  for (int i = 0; i < 4; i++) run<4>(ns[i], 16, sms);   // A in TMEM, two chains
+  for (int i = 0; i < 3; i++) run<6>(ns[i], 16, sms);   // A in TMEM, four chains
+  for (int i = 0; i < 3; i++) run<7>(ns[i], 16, sms);   // A in SMEM, four chains
   return 0;
 }
