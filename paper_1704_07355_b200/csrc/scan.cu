@@ -24,6 +24,7 @@
 //    the exact top-R by (midpoint, id).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.cuh"
 
@@ -866,6 +867,14 @@ __device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase) {
       : "memory");
 }
 
+// One elected lane of the (converged) warp.
+__device__ __forceinline__ bool tc_elect_one() {
+  uint32_t pred;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+               : "=r"(pred));
+  return pred != 0;
+}
+
 // As tc_wait without the suspend-time hint (short tiles: the wake-up must be prompt).
 __device__ __forceinline__ void tc_wait_spin(uint32_t mbar, uint32_t phase) {
   asm volatile(
@@ -1524,7 +1533,8 @@ __global__ void __launch_bounds__(128 * kWG + 32, 1) k_scan_tcw(const __grid_con
   static_assert(kWG * kWgCols <= kCols, "TMEM budget");
   extern __shared__ __align__(16) unsigned char dsm[];  // B: [kWG][kTcwNQ rows][K]
   TcSmem &s = g_tc;
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int w = __shfl_sync(kFull, tid >> 5, 0);  // warp-uniform for the compiler
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&s.tmem)),
@@ -1630,115 +1640,132 @@ __global__ void __launch_bounds__(128 * kWG + 32, 1) k_scan_tcw(const __grid_con
       if (wt == 0) g_tcw.item[wg] = atomicAdd(a.item_counter, 1);  // claimed ahead (read after the item's last barrier)
       const uint32_t idesc =
           (2u << 4) | ((uint32_t)(n_mma >> 3) << 17) | ((uint32_t)(kTcCodes >> 4) << 24);
+      // this warp's MMAs: k-steps wq, wq + 4, ... (operands of step i are the
+      // step-0 operands plus compile-time offsets: one register-to-uniform
+      // move per operand and tile instead of one per MMA)
+      const uint32_t ta_w = a_mma + (uint32_t)wq * 8;  // A from TMEM (K = 32 bytes = 8 columns)
+      const uint64_t db_w = tc_smem_desc(sB_a + (uint32_t)wq * 256, SBO);
+      const uint32_t *pc = a.codes_cm + ((size_t)c0g * kChunkCodes + wt) * WPC;  // this thread's row of tile 0
+      const uint8_t *pv = a.valid + c0g * 32 + (wt >> 3);
+      const int64_t pos_w = c0g * kChunkCodes + (wt - lane);  // position of the warp's first code in tile 0
       uint32_t cw[WPC];
-      {
-        const uint32_t *p = a.codes_cm + ((size_t)c0g * kChunkCodes + wt) * WPC;
-        if (WPC == 4) {
-          const uint4 v4 = __ldg((const uint4 *)p);
-          cw[0] = v4.x; cw[1] = v4.y; cw[WPC - 2] = v4.z; cw[WPC - 1] = v4.w;
-        } else {
-          const uint2 v2 = __ldg((const uint2 *)p);
-          cw[0] = v2.x; cw[WPC - 1] = v2.y;
-        }
+      if (WPC == 4) {
+        const uint4 v4 = __ldg((const uint4 *)pc);
+        cw[0] = v4.x; cw[1] = v4.y; cw[WPC - 2] = v4.z; cw[WPC - 1] = v4.w;
+      } else {
+        const uint2 v2 = __ldg((const uint2 *)pc);
+        cw[0] = v2.x; cw[WPC - 1] = v2.y;
       }
-      for (int64_t t = 0; t < ntiles; t++) {
-        unsigned mpre = 0;
-        if (wt < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[qb + wt]];  // lands during the tile
-        const int c_t = (int)(t & 1) * kTcCodes + wt;
-        const int64_t g_t = c0g + (t >> 1);
-        const uint32_t vb_t = __ldg(a.valid + g_t * 32 + (c_t >> 3));  // read only by the survivor path
-        // ---- expand this thread's code into its A row; fetch the next tile's row ----
-        if (!(a.dbg & 2)) tc_expand_cm<MC>(t_a, cw);
-        if (t + 1 < ntiles) {
-          const uint32_t *p = a.codes_cm + ((size_t)(c0g + ((t + 1) >> 1)) * kChunkCodes +
-                                            (int)((t + 1) & 1) * kTcCodes + wt) * WPC;
-          if (WPC == 4) {
-            const uint4 v4 = __ldg((const uint4 *)p);
-            cw[0] = v4.x; cw[1] = v4.y; cw[WPC - 2] = v4.z; cw[WPC - 1] = v4.w;
-          } else {
-            const uint2 v2 = __ldg((const uint2 *)p);
-            cw[0] = v2.x; cw[WPC - 1] = v2.y;
+      auto run = [&](auto nm_c) {
+        constexpr int NM = decltype(nm_c)::value;  // MMA N: 16 or 32 query columns
+        for (int t = 0; t < (int)ntiles; t++) {
+          unsigned mpre = 0;
+          if (wt < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[qb + wt]];  // lands during the tile
+          const uint32_t vb_t = __ldg(pv);  // read only by the survivor path
+          pv += kTcCodes / 8;
+          // ---- expand this thread's code into its A row; fetch the next tile's row ----
+          if (!(a.dbg & 2)) tc_expand_cm<MC>(t_a, cw);
+          pc += kTcCodes * WPC;
+          if (t + 1 < (int)ntiles) {
+            if (WPC == 4) {
+              const uint4 v4 = __ldg((const uint4 *)pc);
+              cw[0] = v4.x; cw[1] = v4.y; cw[WPC - 2] = v4.z; cw[WPC - 1] = v4.w;
+            } else {
+              const uint2 v2 = __ldg((const uint2 *)pc);
+              cw[0] = v2.x; cw[WPC - 1] = v2.y;
+            }
+            if (lane == 0 && t + 4 < (int)ntiles)  // the warp's 32 rows of tile t + 4 into L2
+              prefetch_l2(pc + 3 * kTcCodes * WPC, 128u * WPC);
           }
-          if (lane == 0 && t + 4 < ntiles)  // the warp's 32 rows of tile t + 4 into L2
-            prefetch_l2(a.codes_cm + ((size_t)(c0g + ((t + 4) >> 1)) * kChunkCodes +
-                                      (int)((t + 4) & 1) * kTcCodes + (wt & ~31)) * WPC, 128u * WPC);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // A row written, D row zeroed
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        wg_sync();
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (lane == 0 && !(a.dbg & 128)) {
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // A row written, D row zeroed
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          wg_sync();
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (!(a.dbg & 128)) {
+            if (tc_elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < K / 32; ks++) {
-            if ((ks & 3) != wq) continue;
-            const uint32_t ta = a_mma + ks * 8;  // A from TMEM (K = 32 bytes = 8 columns)
-            const uint64_t db = tc_smem_desc(sB_a + ks * 256, SBO);
+              for (int i = 0; i < K / 128; i++)
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_mma),
+                    "r"(ta_w + 32u * i), "l"(db_w + 64ull * i), "r"(idesc), "r"(1u));
+              asm volatile(
+                  "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
+                  : "memory");
+            }
+            __syncwarp();
+            if (a.dbg & 256) tc_wait(mbar, ph);
+            else tc_wait_spin(mbar, ph);
+            ph ^= 1;
+          }
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          // ---- this code's sums: read, zero, test ----
+          uint32_t v[NM / 2];
+          if (NM == 32) {
             asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_mma),
-                "r"(ta), "l"(db), "r"(idesc), "r"(1u));
+                "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+                "%12,%13,%14,%15}, [%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                  "=r"(v[7]), "=r"(v[NM / 2 - 8]), "=r"(v[NM / 2 - 7]), "=r"(v[NM / 2 - 6]),
+                  "=r"(v[NM / 2 - 5]), "=r"(v[NM / 2 - 4]), "=r"(v[NM / 2 - 3]), "=r"(v[NM / 2 - 2]),
+                  "=r"(v[NM / 2 - 1])
+                : "r"(t_d));
+          } else {
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                  "=r"(v[7])
+                : "r"(t_d));
           }
-          asm volatile(
-              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
-              : "memory");
-        }
-        __syncwarp();
-        if (!(a.dbg & 128)) {
-          if (a.dbg & 256) tc_wait(mbar, ph);
-          else tc_wait_spin(mbar, ph);
-          ph ^= 1;
-        }
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        // ---- this code's sums: read, zero, test ----
-        uint32_t v[32];
-        tc_ldp(t_d, n_mma / 2, v);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        {
-          const uint32_t z = 0;
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          {
+            const uint32_t z = 0;
 #pragma unroll
-          for (int c = 0; c < kTcwNQ; c += 16)
-            if (c < n_mma)
+            for (int c = 0; c < NM; c += 16)
               asm volatile(
                   "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
                   "%1,%1,%1,%1};" ::"r"(t_d + c), "r"(z)
                   : "memory");
-        }
-        const uint4 *T = (const uint4 *)&s.thr16[qb];
-        uint32_t any = 0;
+          }
+          const uint4 *T = (const uint4 *)&s.thr16[qb];
+          uint32_t any = 0;
 #pragma unroll
-        for (int i = 0; i < kTcwNQ / 2; i += 4) {
-          if (2 * i >= n_mma) break;
-          const uint4 tt = T[i / 4];
-          any |= (tt.x - v[i]) | (tt.y - v[i + 1]) | (tt.z - v[i + 2]) | (tt.w - v[i + 3]);
-        }
-        unsigned todo = __ballot_sync(kFull, (any & 0x80008000u) && ((vb_t >> (c_t & 7)) & 1u) &&
-                                                 !(a.dbg & 1));
-        if (todo) {
-          uint32_t *xf = s.xfer[w][0];
-          const int64_t pos0 = g_t * kChunkCodes + (int64_t)(c_t - lane);
-          while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            if (lane == src) {
+          for (int i = 0; i < NM / 2; i += 4) {
+            const uint4 tt = T[i / 4];
+            any |= (tt.x - v[i]) | (tt.y - v[i + 1]) | (tt.z - v[i + 2]) | (tt.w - v[i + 3]);
+          }
+          const int c_t = (t & 1) * kTcCodes + wt;
+          unsigned todo = __ballot_sync(kFull, (any & 0x80008000u) && ((vb_t >> (c_t & 7)) & 1u) &&
+                                                   !(a.dbg & 1));
+          if (todo) {
+            uint32_t *xf = s.xfer[w][0];
+            const int64_t pos0 = pos_w + (int64_t)t * kTcCodes;
+            while (todo) {
+              const int src = __ffs(todo) - 1;
+              todo &= todo - 1;
+              if (lane == src) {
 #pragma unroll
-              for (int i = 0; i < kTcwNQ / 2; i += 4)
-                *(uint4 *)&xf[i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                for (int i = 0; i < NM / 2; i += 4)
+                  *(uint4 *)&xf[i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+              }
+              __syncwarp();
+              const uint32_t vv = lane < NM / 2 ? xf[lane] : 0u;
+              const int q = qb + 2 * (lane & (NM / 2 - 1));
+              const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
+              __syncwarp();
+              const bool on = lane < NM / 2;
+              tc_hit_warp(a, on && (x & 0x8000u) != 0, on && (x & 0x80000000u) != 0, q, vv, pos0 + src);
             }
-            __syncwarp();
-            const uint32_t vv = lane < kTcwNQ / 2 ? xf[lane] : 0u;
-            const int q = qb + 2 * (lane & (kTcwNQ / 2 - 1));
-            const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
-            __syncwarp();
-            const bool on = lane < n_mma / 2;
-            tc_hit_warp(a, on && (x & 0x8000u) != 0, on && (x & 0x80000000u) != 0, q, vv, pos0 + src);
+          }
+          if (wt < nq && mpre < s.mc[qb + wt]) {  // bounds tightened by the flusher or other CTAs
+            s.mc[qb + wt] = mpre;
+            const int th = q_threshold(__uint_as_float(mpre), s.qmin[qb + wt], s.delta[qb + wt]);
+            if (th + 0x8000 < (int)s.thr16[qb + wt]) s.thr16[qb + wt] = (uint16_t)(th + 0x8000);
           }
         }
-        if (wt < nq && mpre < s.mc[qb + wt]) {  // bounds tightened by the flusher or other CTAs
-          s.mc[qb + wt] = mpre;
-          const int th = q_threshold(__uint_as_float(mpre), s.qmin[qb + wt], s.delta[qb + wt]);
-          if (th + 0x8000 < (int)s.thr16[qb + wt]) s.thr16[qb + wt] = (uint16_t)(th + 0x8000);
-        }
-      }
+      };
+      if (n_mma == 16) run(std::integral_constant<int, 16>{});
+      else run(std::integral_constant<int, 32>{});
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       wg_sync();  // end of item: every tile read, g_tcw.item holds the next item
     }
