@@ -676,7 +676,51 @@ def run_b200(args):
                 "peak_G_lane_instr": round(peak[0] / 1e9, 2),
                 "frac": round(lookups / scan_s / peak[0], 4),
                 "alu_pipe_peak_G": round(peak[1] / 1e9, 2)}
-    if res.stats.get("scan_tc"):
+    if res.stats.get("scan_tc") == 2:
+        # k_scan_tcw (IVF lists probed by a few queries each): every list is
+        # scanned ceil(pairs / 32) times; a pass expands each code of the
+        # list into its one-hot A row (4 m PRMT per code on the ALU pipe) and
+        # runs m / 2 MMAs of N = 16 or 32 per 128-code tile. Three ceilings:
+        # executed int8 MMA ops vs the measured tensor peak (the contract's
+        # "tensor" bound), the expansion's PRMTs vs the measured ALU-pipe
+        # rate, and the code bytes vs HBM; plus north_star's integer-issue
+        # view (lookups / R_int), which this kernel may exceed because the
+        # lookups run on the tensor pipe.
+        mma = np.zeros(1, np.float64)
+        _native.check(lib.qadc_b200_mma_peak(mma.ctypes.data_as(_native._f64p)), "mma_peak")
+        cells_l = index.tables(q_dev, R, ma=ma, init=init)["cells"].cpu().numpy().ravel()
+        sizes_l = np.diff(row_off.cpu().numpy())
+        pl = np.bincount(cells_l, minlength=sizes_l.size)
+        tiles = 2 * ((sizes_l + 255) // 256)
+        full, rem = pl // 32, pl % 32
+        ncols = 32 * full + np.where(rem > 16, 32, np.where(rem > 0, 16, 0))
+        passes = full + (rem > 0)
+        ops_exec = float((tiles * ncols).sum()) * 128 * 16 * pq.m * 2
+        ops_useful = pairs * 16 * pq.m * 2
+        code_passes = float((tiles * passes).sum()) * 128
+        prmt = code_passes * 4 * pq.m
+        cm_bytes = code_passes * pq.m / 2
+        hbm_peak = pk.get("hbm_gbs", 6650.0) * 1e9
+        t_tensor, t_alu, t_hbm = ops_exec / mma[0], prmt / peak[1], cm_bytes / hbm_peak
+        roof = {"bound": "tensor", "achieved": round(ops_exec / scan_s / 1e12, 2),
+                "peak": round(mma[0] / 1e12, 2),
+                "unit": "TOP/s int8 (executed one-hot MMA ops: 128 codes x N in {16, 32} query "
+                        "columns x 16 m per tile and pass) vs measured tcgen05.mma.kind::i8 peak "
+                        "(qadc_b200_mma_peak)",
+                "frac": round(t_tensor / scan_s, 4),
+                "useful_ops_frac": round(ops_useful / scan_s / mma[0], 4),
+                "alu_expansion_view": {"prmt_lane_instr": int(prmt),
+                                       "alu_pipe_peak_G": int_view["alu_pipe_peak_G"],
+                                       "frac": round(t_alu / scan_s, 4)},
+                "roof_ms": {"tensor": round(t_tensor * 1e3, 2), "alu_expansion": round(t_alu * 1e3, 2),
+                            "hbm_code_major": round(t_hbm * 1e3, 2),
+                            "north_star_int_issue": round(lookups / peak[0] * 1e3, 2)},
+                "frac_of_slowest_ceiling": round(max(t_tensor, t_alu, t_hbm) / scan_s, 4),
+                "list_passes": {"code_passes": int(code_passes), "mean_passes_per_scanned_code":
+                                round(code_passes / max(1.0, float((tiles * (pl > 0)).sum()) * 128), 3)},
+                "int_issue_view": int_view}
+        hbm_bytes = cm_bytes
+    elif res.stats.get("scan_tc"):
         # int8 tcgen05 one-hot GEMM: 16 m MACs (2 ops each) per (query, code)
         # pair; achieved = useful ops / launch time vs the measured int8 rate
         mma = np.zeros(1, np.float64)
@@ -695,7 +739,8 @@ def run_b200(args):
                         "lane-instr/s (PRMT+IMAD dual-pipe microbench, qadc_b200_int_peak)",
                 "frac": int_view["frac"], "alu_pipe_peak_G": int_view["alu_pipe_peak_G"]}
     roof.update({
-        "kernel": "k_scan_tc2" if res.stats.get("scan_tc") else "k_scan (PRMT)",
+        "kernel": {0: "k_scan (PRMT)", 1: "k_scan_tc2 / k_scan_tc", 2: "k_scan_tcw"}[
+            int(res.stats.get("scan_tc", 0))],
         "traffic": ncu_traffic(args.config),
         "scan_kernel_ms": round(scan_s * 1e3, 3),
         "algorithmic_units_per_launch": {"pairs": int(pairs), "lookups": int(lookups)},

@@ -1094,15 +1094,16 @@ template <int MH>
 __device__ __forceinline__ void tc_expand_cm(uint32_t a_col, const uint32_t (&cw)[(MH + 7) / 8]) {
 #pragma unroll
   for (int gi = 0; gi < MH / 4; gi++) {
+    // The pool constant sits in PRMT's second source (bytes 4..7), where SASS
+    // takes an immediate; as first source ptxas re-materialises it from a
+    // uniform register before every PRMT (64 extra moves per code). Entries
+    // whose pool byte would be 0..3 flip bit 2 of every selector nibble
+    // instead, so four selector variants serve the 16 entries.
     const uint32_t sel = (gi & 1) ? (cw[gi / 2] >> 16) : cw[gi / 2];
-    const uint32_t selx = sel ^ 0x8888u;
+    const uint32_t sv[4] = {sel ^ 0x4444u, sel, sel ^ 0xccccu, sel ^ 0x8888u};
     uint32_t r[16];
 #pragma unroll
-    for (int e = 0; e < 16; e++) {
-      const uint32_t one = 1u << (8 * (e & 3));
-      const uint32_t sx = e < 8 ? sel : selx;
-      r[e] = (e & 4) ? prmt(0u, one, sx) : prmt(one, 0u, sx);
-    }
+    for (int e = 0; e < 16; e++) r[e] = prmt(0u, 1u << (8 * (e & 3)), sv[e >> 2]);
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
         "%13,%14,%15,%16};" ::"r"(a_col + 16 * gi),
@@ -1520,14 +1521,72 @@ k_scan_tc(const __grid_constant__ ScanArgs a) {
 // TMEM per warpgroup: D (32 columns) + A (4 m columns), single-buffered.
 constexpr int kWG = 3;        // warpgroups per CTA (3 x (32 + 128) <= 512 TMEM columns)
 constexpr int kTcwNQ = 32;    // queries per item (MMA N = 16 or 32)
+constexpr int kTcwSlots = 8;  // survivor slots per compute warp
+// A code with at least one surviving (query, code) pair: its packed sums go
+// through the compute warp's own single-producer ring to the filter warp,
+// which runs the per-pair test, midpoints and the push to the candidate ring
+// (tc_hit_warp). A compute warp spends ~25 instructions on a survivor
+// instead of the per-pair path (configs[4]: ~10^7 survivors per batch cost
+// 5.5 of 21.9 ms while compute warps handled them inline).
+struct __align__(16) TcwEnt {
+  uint32_t sums[kTcwNQ / 2];  // packed pairs: query 2 i (low half), 2 i + 1 (high)
+  int64_t pos;                // code position (chunk * 256 + code)
+};
 struct TcwSmem {
-  uint64_t mbar[kWG];
+  uint64_t mbar[kWG][2];         // MMAs of half 0 / half 1 of the warpgroup's tile
   int item[kWG];
+  int nm2[kWG];                  // packed sum registers of the warpgroup's current item (N / 2)
+  unsigned head[4 * kWG];        // slots published by compute warp w (monotone)
+  unsigned tail[4 * kWG];        // slots consumed by the filter warp
+  __align__(16) TcwEnt ent[4 * kWG][kTcwSlots];
 };
 __shared__ TcwSmem g_tcw;
 
+// Filter warp f of k_scan_tcw serves the four compute warps of warpgroup f:
+// two ring entries per round (lanes 0-15 / 16-31 take one packed pair each),
+// the entries' tails released once per round.
+__device__ __forceinline__ void tcw_filter(const ScanArgs &a, int f) {
+  const int lane = threadIdx.x & 31;
+  const int qb = f * kTcwNQ;
+  unsigned tail = 0;  // lane l < 4: of ring 4 f + l
+  for (;;) {
+    unsigned head = 0;
+    if (lane < 4) head = *(volatile unsigned *)&g_tcw.head[4 * f + lane];
+    const unsigned busy = __ballot_sync(kFull, head != tail);
+    if (!busy) {
+      // a compute warp publishes its entries before it reports done: re-check once
+      if (*(volatile int *)&g_tc.done >= kWG) {
+        if (lane < 4) head = *(volatile unsigned *)&g_tcw.head[4 * f + lane];
+        if (!__ballot_sync(kFull, head != tail)) break;
+        continue;
+      }
+      __nanosleep(100);
+      continue;
+    }
+    __threadfence_block();  // entries written before the heads read above
+    const int rl = __ffs(busy) - 1, r = 4 * f + rl;
+    const unsigned h = __shfl_sync(kFull, head, rl), t0 = __shfl_sync(kFull, tail, rl);
+    const unsigned n = min(h - t0, 2u);
+    const int nm2 = *(volatile int *)&g_tcw.nm2[f];
+    const int half = lane >> 4, pl = lane & 15;
+    const TcwEnt &e = g_tcw.ent[r][(t0 + (unsigned)half) % kTcwSlots];
+    const bool on = (unsigned)half < n && pl < nm2;
+    const uint32_t vv = on ? e.sums[pl] : 0u;
+    const int64_t pos = e.pos;
+    const int q = qb + 2 * pl;
+    const uint32_t x = *(const uint32_t *)&g_tc.thr16[q] - vv;
+    tc_hit_warp(a, on && (x & 0x8000u) != 0, on && (x & 0x80000000u) != 0, q, vv, pos);
+    if (lane == rl) {
+      tail = t0 + n;
+      __threadfence_block();  // the entries were read before their slots are released
+      *(volatile unsigned *)&g_tcw.tail[r] = tail;
+    }
+    __syncwarp();
+  }
+}
+
 template <int MC>
-__global__ void __launch_bounds__(128 * kWG + 32, 1) k_scan_tcw(const __grid_constant__ ScanArgs a) {
+__global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const __grid_constant__ ScanArgs a) {
   constexpr int K = 16 * MC, SBO = 8 * K, WPC = MC / 8;
   constexpr uint32_t kCols = 512, kWgCols = kTcwNQ + K / 4;
   static_assert(kWG * kWgCols <= kCols, "TMEM budget");
@@ -1542,32 +1601,40 @@ __global__ void __launch_bounds__(128 * kWG + 32, 1) k_scan_tcw(const __grid_con
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int g = 0; g < kWG; g++)
+    for (int g = 0; g < 2 * kWG; g++)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(
-          (uint32_t)__cvta_generic_to_shared(&g_tcw.mbar[g])));
+          (uint32_t)__cvta_generic_to_shared(&g_tcw.mbar[g >> 1][g & 1])));
     asm volatile("fence.mbarrier_init.release.cluster;");
     s.done = 0;
     s.head = 0;
     s.tail = 0;
+  }
+  if (tid < 4 * kWG) {
+    g_tcw.head[tid] = 0;
+    g_tcw.tail[tid] = 0;
   }
   for (int i = tid; i < kRing; i += blockDim.x) s.ring[i].query = -1;
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (w == 4 * kWG) {
-    tc_flusher(a, kWG);
+    tc_flusher(a, 2 * kWG);
+  } else if (w > 4 * kWG) {
+    tcw_filter(a, w - (4 * kWG + 1));
+    if (lane == 0) atomicAdd(&s.done, 1);  // this filter's survivors are in the candidate ring
   } else {
     const int wg = w >> 2, wt = tid & 127, wq = w & 3;  // warpgroup, thread in it, warp in it
     const int qb = wg * kTcwNQ;                          // the warpgroup's slice of the query-state arrays
     uint8_t *sB = dsm + (size_t)wg * kTcwNQ * K;
     const uint32_t sB_a = (uint32_t)__cvta_generic_to_shared(sB);
-    const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&g_tcw.mbar[wg]);
+    const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&g_tcw.mbar[wg][0]);
     const uint32_t tmem = s.tmem;
     const uint32_t t_d = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)wg * kWgCols;  // this thread's D row
     const uint32_t t_a = t_d + kTcwNQ;                                                  // its A row
     const uint32_t d_mma = tmem + (uint32_t)wg * kWgCols, a_mma = d_mma + kTcwNQ;
     const int n_items = *a.n_items;
     uint32_t ph = 0;
+    unsigned rh = 0;  // this warp's survivor ring: slots published
     {  // D starts zeroed (every MMA accumulates)
       const uint32_t z = 0;
 #pragma unroll
@@ -1634,6 +1701,7 @@ __global__ void __launch_bounds__(128 * kWG + 32, 1) k_scan_tcw(const __grid_con
         }
         s.thr16[qb + q] = (uint16_t)(thr + 0x8000);
         s.mc[qb + q] = mb;
+        if (q == 0) g_tcw.nm2[wg] = n_mma / 2;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       wg_sync();  // B and the query state are staged; everyone has read g_tcw.item
@@ -1648,58 +1716,87 @@ __global__ void __launch_bounds__(128 * kWG + 32, 1) k_scan_tcw(const __grid_con
       const uint32_t *pc = a.codes_cm + ((size_t)c0g * kChunkCodes + wt) * WPC;  // this thread's row of tile 0
       const uint8_t *pv = a.valid + c0g * 32 + (wt >> 3);
       const int64_t pos_w = c0g * kChunkCodes + (wt - lane);  // position of the warp's first code in tile 0
-      uint32_t cw[WPC];
-      if (WPC == 4) {
-        const uint4 v4 = __ldg((const uint4 *)pc);
-        cw[0] = v4.x; cw[1] = v4.y; cw[WPC - 2] = v4.z; cw[WPC - 1] = v4.w;
-      } else {
-        const uint2 v2 = __ldg((const uint2 *)pc);
-        cw[0] = v2.x; cw[WPC - 1] = v2.y;
-      }
+      uint32_t vb_next = __ldg(pv);  // valid byte of this thread's code, one tile ahead
+      // code-major rows of tiles t, t + 1 and t + 2 (the row of tile t + 2 is
+      // requested a whole tile before its first use)
+      uint32_t cw[WPC], cn[WPC], cf[WPC];
+      auto load_row = [&](const uint32_t *p, uint32_t (&dst)[WPC]) {
+        if (WPC == 4) {
+          const uint4 v4 = __ldg((const uint4 *)p);
+          dst[0] = v4.x; dst[1] = v4.y; dst[WPC - 2] = v4.z; dst[WPC - 1] = v4.w;
+        } else {
+          const uint2 v2 = __ldg((const uint2 *)p);
+          dst[0] = v2.x; dst[WPC - 1] = v2.y;
+        }
+      };
+      load_row(pc, cw);
+      if (ntiles > 1) load_row(pc + kTcCodes * WPC, cn);
+      // Half h of a tile = sub-quantizers [h m / 2, (h + 1) m / 2): its own A
+      // columns and its own MMAs (k-steps [h m / 4, (h + 1) m / 4), this warp:
+      // wq, wq + 4, ... of them), committed to mbarrier h.
+      constexpr int HW = WPC / 2, HCOLS = 2 * MC, HM = K / 256;  // words, A columns, MMAs per warp of a half
+      auto expand_half = [&](int h, const uint32_t (&row)[WPC]) {
+        if (a.dbg & 2) return;
+        uint32_t hw[HW];
+#pragma unroll
+        for (int i = 0; i < HW; i++) hw[i] = row[h * HW + i];
+        tc_expand_cm<MC / 2>(t_a + (uint32_t)(h * HCOLS), hw);
+      };
+      auto issue_half = [&](int h) {
+        // A row halves written and D zeroed by every thread of the warpgroup
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        wg_sync();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (a.dbg & 128) return;
+        if (tc_elect_one()) {
+#pragma unroll
+          for (int i = 0; i < HM; i++)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_mma),
+                "r"(ta_w + 32u * (uint32_t)(h * HM + i)), "l"(db_w + 64ull * (uint64_t)(h * HM + i)),
+                "r"(idesc), "r"(1u));
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                  mbar + 8u * (uint32_t)h)
+              : "memory");
+        }
+        __syncwarp();
+      };
+      // Software pipeline of one warpgroup (A and D single-buffered, A in two
+      // halves): the MMAs of half 0 run while half 1 is expanded, those of
+      // half 1 while half 0 of the NEXT tile is expanded, and the threshold
+      // test of tile t runs after half 0 of tile t + 1 has been issued: the
+      // warpgroup never waits for an MMA it has just issued.
+      expand_half(0, cw);
+      issue_half(0);
       auto run = [&](auto nm_c) {
         constexpr int NM = decltype(nm_c)::value;  // MMA N: 16 or 32 query columns
         for (int t = 0; t < (int)ntiles; t++) {
+          const bool more = t + 1 < (int)ntiles;
           unsigned mpre = 0;
           if (wt < nq) mpre = *(volatile unsigned *)&a.M_bits[s.query[qb + wt]];  // lands during the tile
-          const uint32_t vb_t = __ldg(pv);  // read only by the survivor path
+          const uint32_t vb_t = vb_next;  // read only by the survivor path
           pv += kTcCodes / 8;
-          // ---- expand this thread's code into its A row; fetch the next tile's row ----
-          if (!(a.dbg & 2)) tc_expand_cm<MC>(t_a, cw);
-          pc += kTcCodes * WPC;
-          if (t + 1 < (int)ntiles) {
-            if (WPC == 4) {
-              const uint4 v4 = __ldg((const uint4 *)pc);
-              cw[0] = v4.x; cw[1] = v4.y; cw[WPC - 2] = v4.z; cw[WPC - 1] = v4.w;
-            } else {
-              const uint2 v2 = __ldg((const uint2 *)pc);
-              cw[0] = v2.x; cw[WPC - 1] = v2.y;
-            }
-            if (lane == 0 && t + 4 < (int)ntiles)  // the warp's 32 rows of tile t + 4 into L2
-              prefetch_l2(pc + 3 * kTcCodes * WPC, 128u * WPC);
+          if (more) vb_next = __ldg(pv);
+          // ---- half 1 of tile t ----
+          expand_half(1, cw);
+          pc += kTcCodes * WPC;  // row of tile t + 1
+          if (t + 2 < (int)ntiles) {
+            load_row(pc + kTcCodes * WPC, cf);
+            if (lane == 0 && t + 5 < (int)ntiles)  // the warp's 32 rows of tile t + 5 into L2
+              prefetch_l2(pc + 4 * kTcCodes * WPC, 128u * WPC);
           }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");  // A row written, D row zeroed
-          asm volatile("tcgen05.fence::before_thread_sync;");
-          wg_sync();
+          issue_half(1);
+          // ---- half 0 of tile t + 1 (its A columns are free once the MMAs of half 0 of tile t are done) ----
+          if (!(a.dbg & 128)) tc_wait_spin(mbar, ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          if (!(a.dbg & 128)) {
-            if (tc_elect_one()) {
-#pragma unroll
-              for (int i = 0; i < K / 128; i++)
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_mma),
-                    "r"(ta_w + 32u * i), "l"(db_w + 64ull * i), "r"(idesc), "r"(1u));
-              asm volatile(
-                  "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
-                  : "memory");
-            }
-            __syncwarp();
-            if (a.dbg & 256) tc_wait(mbar, ph);
-            else tc_wait_spin(mbar, ph);
-            ph ^= 1;
-          }
+          if (more) expand_half(0, cn);
+          // ---- tile t: read this code's sums, zero them ----
+          if (!(a.dbg & 128)) tc_wait_spin(mbar + 8, ph);
+          ph ^= 1;
           asm volatile("tcgen05.fence::after_thread_sync;");
-          // ---- this code's sums: read, zero, test ----
           uint32_t v[NM / 2];
           if (NM == 32) {
             asm volatile(
@@ -1727,6 +1824,8 @@ __global__ void __launch_bounds__(128 * kWG + 32, 1) k_scan_tcw(const __grid_con
                   "%1,%1,%1,%1};" ::"r"(t_d + c), "r"(z)
                   : "memory");
           }
+          if (more) issue_half(0);  // tile t + 1 starts on the tensor pipe before tile t is tested
+          // ---- tile t: threshold test ----
           const uint4 *T = (const uint4 *)&s.thr16[qb];
           uint32_t any = 0;
 #pragma unroll
@@ -1738,23 +1837,21 @@ __global__ void __launch_bounds__(128 * kWG + 32, 1) k_scan_tcw(const __grid_con
           unsigned todo = __ballot_sync(kFull, (any & 0x80008000u) && ((vb_t >> (c_t & 7)) & 1u) &&
                                                    !(a.dbg & 1));
           if (todo) {
-            uint32_t *xf = s.xfer[w][0];
             const int64_t pos0 = pos_w + (int64_t)t * kTcCodes;
             while (todo) {
               const int src = __ffs(todo) - 1;
               todo &= todo - 1;
+              while (rh - *(volatile unsigned *)&g_tcw.tail[w] >= (unsigned)kTcwSlots) __nanosleep(40);
               if (lane == src) {
+                TcwEnt &e = g_tcw.ent[w][rh % kTcwSlots];
 #pragma unroll
                 for (int i = 0; i < NM / 2; i += 4)
-                  *(uint4 *)&xf[i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                  *(uint4 *)&e.sums[i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                e.pos = pos0 + src;
+                __threadfence_block();
+                *(volatile unsigned *)&g_tcw.head[w] = rh + 1;
               }
-              __syncwarp();
-              const uint32_t vv = lane < NM / 2 ? xf[lane] : 0u;
-              const int q = qb + 2 * (lane & (NM / 2 - 1));
-              const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
-              __syncwarp();
-              const bool on = lane < NM / 2;
-              tc_hit_warp(a, on && (x & 0x8000u) != 0, on && (x & 0x80000000u) != 0, q, vv, pos0 + src);
+              rh++;
             }
           }
           if (wt < nq && mpre < s.mc[qb + wt]) {  // bounds tightened by the flusher or other CTAs
@@ -1762,10 +1859,18 @@ __global__ void __launch_bounds__(128 * kWG + 32, 1) k_scan_tcw(const __grid_con
             const int th = q_threshold(__uint_as_float(mpre), s.qmin[qb + wt], s.delta[qb + wt]);
             if (th + 0x8000 < (int)s.thr16[qb + wt]) s.thr16[qb + wt] = (uint16_t)(th + 0x8000);
           }
+#pragma unroll
+          for (int i = 0; i < WPC; i++) {
+            cw[i] = cn[i];
+            cn[i] = cf[i];
+          }
         }
       };
       if (n_mma == 16) run(std::integral_constant<int, 16>{});
       else run(std::integral_constant<int, 32>{});
+      // the filter warp reads this item's thresholds and query state: drain
+      // the warp's ring before the next item is staged
+      while (*(volatile unsigned *)&g_tcw.tail[w] != rh) __nanosleep(40);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       wg_sync();  // end of item: every tile read, g_tcw.item holds the next item
     }
@@ -1781,7 +1886,7 @@ template <int MC>
 void launch_tcw(const ScanArgs &a, int nsm, cudaStream_t st) {
   const size_t smem = (size_t)kWG * kTcwNQ * 16 * MC;
   cudaFuncSetAttribute(k_scan_tcw<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_scan_tcw<MC><<<nsm, 128 * kWG + 32, smem, st>>>(a);
+  k_scan_tcw<MC><<<nsm, 128 * kWG + 32 + 32 * kWG, smem, st>>>(a);
 }
 
 
