@@ -1522,6 +1522,12 @@ k_scan_tc(const __grid_constant__ ScanArgs a) {
 constexpr int kWG = 3;        // warpgroups per CTA (3 x (32 + 128) <= 512 TMEM columns)
 constexpr int kTcwNQ = 32;    // queries per item (MMA N = 16 or 32)
 constexpr int kTcwSlots = 8;  // survivor slots per compute warp
+// timing experiments (QADC_B200_TC_DEBUG bits 1 / 2 / 128: no survivors / no
+// expansion / no MMAs) are compiled in only with -DQADC_TCW_DEBUG=1
+#ifndef QADC_TCW_DEBUG
+#define QADC_TCW_DEBUG 0
+#endif
+constexpr bool kTcwDbg = QADC_TCW_DEBUG != 0;
 // A code with at least one surviving (query, code) pair: its packed sums go
 // through the compute warp's own single-producer ring to the filter warp,
 // which runs the per-pair test, midpoints and the push to the candidate ring
@@ -1602,7 +1608,7 @@ __global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const
   }
   if (tid == 0) {
     for (int g = 0; g < 2 * kWG; g++)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
           (uint32_t)__cvta_generic_to_shared(&g_tcw.mbar[g >> 1][g & 1])));
     asm volatile("fence.mbarrier_init.release.cluster;");
     s.done = 0;
@@ -1635,17 +1641,7 @@ __global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const
     const int n_items = *a.n_items;
     uint32_t ph = 0;
     unsigned rh = 0;  // this warp's survivor ring: slots published
-    {  // D starts zeroed (every MMA accumulates)
-      const uint32_t z = 0;
-#pragma unroll
-      for (int c = 0; c < kTcwNQ; c += 16)
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
-            "%1,%1,%1,%1};" ::"r"(t_d + c), "r"(z)
-            : "memory");
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
-    auto wg_sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(wg + 1) : "memory"); };
+    auto wg_sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(3 * wg + 1) : "memory"); };
     if (wt == 0) g_tcw.item[wg] = atomicAdd(a.item_counter, 1);
     wg_sync();
     for (;;) {
@@ -1708,11 +1704,11 @@ __global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const
       if (wt == 0) g_tcw.item[wg] = atomicAdd(a.item_counter, 1);  // claimed ahead (read after the item's last barrier)
       const uint32_t idesc =
           (2u << 4) | ((uint32_t)(n_mma >> 3) << 17) | ((uint32_t)(kTcCodes >> 4) << 24);
-      // this warp's MMAs: k-steps wq, wq + 4, ... (operands of step i are the
-      // step-0 operands plus compile-time offsets: one register-to-uniform
-      // move per operand and tile instead of one per MMA)
-      const uint32_t ta_w = a_mma + (uint32_t)wq * 8;  // A from TMEM (K = 32 bytes = 8 columns)
-      const uint64_t db_w = tc_smem_desc(sB_a + (uint32_t)wq * 256, SBO);
+      // operands of k-step i = the step-0 operands plus compile-time offsets
+      // (A from TMEM: 8 columns per step; B: 256 bytes per step): no
+      // per-MMA register-to-uniform moves, so ONE warp issues at the tensor
+      // pipe's own rate (N / 2 cycles per MMA, tools/tc_kind_bench)
+      const uint64_t db_0 = tc_smem_desc(sB_a, SBO);
       const uint32_t *pc = a.codes_cm + ((size_t)c0g * kChunkCodes + wt) * WPC;  // this thread's row of tile 0
       const uint8_t *pv = a.valid + c0g * 32 + (wt >> 3);
       const int64_t pos_w = c0g * kChunkCodes + (wt - lane);  // position of the warp's first code in tile 0
@@ -1734,29 +1730,41 @@ __global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const
       // Half h of a tile = sub-quantizers [h m / 2, (h + 1) m / 2): its own A
       // columns and its own MMAs (k-steps [h m / 4, (h + 1) m / 4), this warp:
       // wq, wq + 4, ... of them), committed to mbarrier h.
-      constexpr int HW = WPC / 2, HCOLS = 2 * MC, HM = K / 256;  // words, A columns, MMAs per warp of a half
+      constexpr int HW = WPC / 2, HCOLS = 2 * MC, HK = K / 64;  // words, A columns, MMAs (K = 32 steps) of a half
       auto expand_half = [&](int h, const uint32_t (&row)[WPC]) {
-        if (a.dbg & 2) return;
+        if (kTcwDbg && (a.dbg & 2)) return;
         uint32_t hw[HW];
 #pragma unroll
         for (int i = 0; i < HW; i++) hw[i] = row[h * HW + i];
         tc_expand_cm<MC / 2>(t_a + (uint32_t)(h * HCOLS), hw);
       };
       auto issue_half = [&](int h) {
-        // A row halves written and D zeroed by every thread of the warpgroup
+        // this thread's A row half is written (and, for half 0, its D row read)
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
-        wg_sync();
+        if (wq != 0) {  // only the issuing warp waits for the warpgroup
+          asm volatile("bar.arrive %0, 128;" ::"r"(3 * wg + 2 + h) : "memory");
+          return;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(3 * wg + 2 + h) : "memory");
         asm volatile("tcgen05.fence::after_thread_sync;");
-        if (a.dbg & 128) return;
+        if (kTcwDbg && (a.dbg & 128)) return;
         if (tc_elect_one()) {
 #pragma unroll
-          for (int i = 0; i < HM; i++)
-            asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_mma),
-                "r"(ta_w + 32u * (uint32_t)(h * HM + i)), "l"(db_w + 64ull * (uint64_t)(h * HM + i)),
-                "r"(idesc), "r"(1u));
+          for (int i = 0; i < HK; i++) {
+            // the tile's first MMA overwrites D, the others accumulate
+            if (h == 0 && i == 0)
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_mma),
+                  "r"(a_mma), "l"(db_0), "r"(idesc), "r"(0u));
+            else
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_mma),
+                  "r"(a_mma + 8u * (uint32_t)(h * HK + i)), "l"(db_0 + 16ull * (uint64_t)(h * HK + i)),
+                  "r"(idesc), "r"(1u));
+          }
           asm volatile(
               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                   mbar + 8u * (uint32_t)h)
@@ -1790,11 +1798,11 @@ __global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const
           }
           issue_half(1);
           // ---- half 0 of tile t + 1 (its A columns are free once the MMAs of half 0 of tile t are done) ----
-          if (!(a.dbg & 128)) tc_wait_spin(mbar, ph);
+          if (!(kTcwDbg && (a.dbg & 128))) tc_wait_spin(mbar, ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (more) expand_half(0, cn);
           // ---- tile t: read this code's sums, zero them ----
-          if (!(a.dbg & 128)) tc_wait_spin(mbar + 8, ph);
+          if (!(kTcwDbg && (a.dbg & 128))) tc_wait_spin(mbar + 8, ph);
           ph ^= 1;
           asm volatile("tcgen05.fence::after_thread_sync;");
           uint32_t v[NM / 2];
@@ -1815,15 +1823,6 @@ __global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const
                 : "r"(t_d));
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          {
-            const uint32_t z = 0;
-#pragma unroll
-            for (int c = 0; c < NM; c += 16)
-              asm volatile(
-                  "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
-                  "%1,%1,%1,%1};" ::"r"(t_d + c), "r"(z)
-                  : "memory");
-          }
           if (more) issue_half(0);  // tile t + 1 starts on the tensor pipe before tile t is tested
           // ---- tile t: threshold test ----
           const uint4 *T = (const uint4 *)&s.thr16[qb];
@@ -1835,13 +1834,30 @@ __global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const
           }
           const int c_t = (t & 1) * kTcCodes + wt;
           unsigned todo = __ballot_sync(kFull, (any & 0x80008000u) && ((vb_t >> (c_t & 7)) & 1u) &&
-                                                   !(a.dbg & 1));
+                                                   !(kTcwDbg && (a.dbg & 1)));
           if (todo) {
             const int64_t pos0 = pos_w + (int64_t)t * kTcCodes;
             while (todo) {
               const int src = __ffs(todo) - 1;
               todo &= todo - 1;
-              while (rh - *(volatile unsigned *)&g_tcw.tail[w] >= (unsigned)kTcwSlots) __nanosleep(40);
+              if (rh - *(volatile unsigned *)&g_tcw.tail[w] >= (unsigned)kTcwSlots) {
+                // ring full (a burst under a still loose bound): this warp
+                // runs the per-pair path itself instead of waiting
+                uint32_t *xf = s.xfer[w][0];
+                if (lane == src) {
+#pragma unroll
+                  for (int i = 0; i < NM / 2; i += 4)
+                    *(uint4 *)&xf[i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                }
+                __syncwarp();
+                const bool on = lane < NM / 2;
+                const uint32_t vv = on ? xf[lane] : 0u;
+                const int q = qb + 2 * (lane & (NM / 2 - 1));
+                const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
+                __syncwarp();
+                tc_hit_warp(a, on && (x & 0x8000u) != 0, on && (x & 0x80000000u) != 0, q, vv, pos0 + src);
+                continue;
+              }
               if (lane == src) {
                 TcwEnt &e = g_tcw.ent[w][rh % kTcwSlots];
 #pragma unroll

@@ -89,5 +89,19 @@ if os.environ.get("KNOB_COMPARE") == "1":  # tensor-core vs PRMT scan on the sam
     print(f"compare: prmt scan {a[3]:.2f} ms ({a[4]:.0f} cand/q), {os.environ.get("KNOB_COMPARE_MODE", "auto")} scan {b[3]:.2f} ms ({b[4]:.0f} cand/q); "
           f"ids exact {int(ok_i.sum())}/{qs.shape[0]}, dist bits exact {int(ok_d.sum())}/{qs.shape[0]}, "
           f"counts equal {bool((a[2] == b[2]).all())}", file=sys.stderr)
+if os.environ.get("KNOB_PROFILE") == "1":  # per-kernel device time of one search (torch profiler)
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(3):
+            index.search(qs, cfg.R, ma=cfg.nprobe, init=cfg.init)
+        torch.cuda.synchronize()
+    rows = {}
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA:
+            t = rows.setdefault(ev.name, [0.0, 0])
+            t[0] += ev.device_time
+            t[1] += 1
+    for k, (us, c) in sorted(rows.items(), key=lambda kv: -kv[1][0])[:24]:
+        print(f"  {us / 3 / 1e3:8.3f} ms  x{c // 3:<3d} {k[:100]}", file=sys.stderr)
 print(json.dumps({"step_ms": round(e0.elapsed_time(e1) / 5, 3), "scan_ms": round(scan / 5e3, 3),
                   "cand_per_query": round(cand / 5 / qs.shape[0], 1)}))

@@ -130,6 +130,72 @@ __global__ void __launch_bounds__(128, 1) k_multi(int NW, int N, int ksteps, lon
   if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// One warp, 16 MMAs per tile with operands = loop-invariant bases + compile-time
+// offsets (no per-MMA register-to-uniform moves): the issue rate of clean code.
+__global__ void __launch_bounds__(128, 1) k_clean(int N, long long *cyc) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, K = 512;
+  for (int i = tid; i < (128 + N) * K / 16; i += 128) ((uint4 *)sm)[i] = make_uint4(0, 0, 0, 0);
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_slot;
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm) + 128 * K;
+  const uint32_t idesc = ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24) | (2u << 4);
+  const uint32_t a_t = tmem + 256;
+  const uint64_t db0 = desc(sb, 8 * K);
+  long long t0 = clock64();
+  if (tid < 32) {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    if (pred) {
+      for (int t = 0; t < kTiles; t++) {
+#pragma unroll
+        for (int ks = 0; ks < 16; ks++)
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+              "r"(a_t + ks * 8), "l"(db0 + 16ull * ks), "r"(idesc), "r"(1u));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb) : "memory");
+      wait_mb(mb, 0);
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (tid == 0 && blockIdx.x == 0) cyc[0] = t1 - t0;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+void run_clean(int N, int sms) {
+  long long *d;
+  cudaMalloc(&d, 1024);
+  const size_t smem = (size_t)(128 + N) * 512;
+  cudaFuncSetAttribute(k_clean, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_clean<<<sms, 128, smem>>>(N, d);
+  k_clean<<<sms, 128, smem>>>(N, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long c = 0;
+  cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+  printf("i8 one warp, uniform operands, N %3d: %6.1f cycles per mma  %s\n", N, (double)c / kTiles / 16,
+         cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 void run_multi(int NW, int N, int sms) {
   const int ksteps = 16;
   long long *d;
@@ -167,6 +233,7 @@ void run(int M, int N, int sms) {
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run_clean(16, sms); run_clean(32, sms); run_clean(64, sms); run_clean(128, sms);
   for (int nw = 1; nw <= 4; nw++) { run_multi(nw, 16, sms); run_multi(nw, 64, sms); }
   const int ns[6] = {16, 32, 64, 96, 128, 256};
   if (sms > 0) return 0;
