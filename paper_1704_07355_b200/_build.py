@@ -22,7 +22,7 @@ SOURCES = ["layout.cu", "lut.cu", "probe_tc.cu", "scan.cu", "select.cu", "simple
            "peak.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-                     "-I" + str(ROOT / "include")]
+                     "-I" + str(ROOT / "include")] + os.environ.get("QADC_NVCC_EXTRA", "").split()
 
 
 def _nvcc() -> str:

@@ -1090,8 +1090,11 @@ __device__ __forceinline__ void tc_flusher(const ScanArgs &a, int done_target = 
 // shift / add instructions per cell when the one-hot bytes are built from
 // the interleaved words. The K order this produces — byte (16 (4 g) + 4 e +
 // i) = entry e of sub-quantizer 4 g + i — is matched by the B staging.
+// (mode: timing experiments of k_scan_tcw only: 1 = stores without the PRMTs,
+// 2 = PRMTs without the stores)
 template <int MH>
-__device__ __forceinline__ void tc_expand_cm(uint32_t a_col, const uint32_t (&cw)[(MH + 7) / 8]) {
+__device__ __forceinline__ void tc_expand_cm(uint32_t a_col, const uint32_t (&cw)[(MH + 7) / 8],
+                                             int mode = 0) {
 #pragma unroll
   for (int gi = 0; gi < MH / 4; gi++) {
     // The pool constant sits in PRMT's second source (bytes 4..7), where SASS
@@ -1103,7 +1106,14 @@ __device__ __forceinline__ void tc_expand_cm(uint32_t a_col, const uint32_t (&cw
     const uint32_t sv[4] = {sel ^ 0x4444u, sel, sel ^ 0xccccu, sel ^ 0x8888u};
     uint32_t r[16];
 #pragma unroll
-    for (int e = 0; e < 16; e++) r[e] = prmt(0u, 1u << (8 * (e & 3)), sv[e >> 2]);
+    for (int e = 0; e < 16; e++) r[e] = mode == 1 ? sv[e >> 2] : prmt(0u, 1u << (8 * (e & 3)), sv[e >> 2]);
+    if (mode == 2) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int e = 0; e < 16; e++) asm volatile("" ::"r"(r[e]));
+      (void)x;
+      continue;
+    }
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
         "%13,%14,%15,%16};" ::"r"(a_col + 16 * gi),
@@ -1209,16 +1219,16 @@ __device__ __forceinline__ void tc_sync(int t) {
 //    named barrier (all compute threads expanded it, finished reading D and
 //    zeroed it), then one elected lane per warp issues its share of the m/2
 //    MMAs (k-steps mw, mw + kMmaWarps, ...; N = the item's queries, up to
-//    256) and commits to the mbarrier (one arrival per MMA warp). ONE warp
-//    issues at most one tcgen05.mma per ~70-78 cycles whatever its shape
-//    (tools/tc_kind_bench: every kind, M 64 / 128, N 16..128, A in TMEM or
-//    SMEM), while the tensor pipe needs N / 2 cycles: with few queries per
-//    list (IVF) a single issuing warp is the bottleneck (16 x 78 cycles per
-//    128 codes); four issuing warps reach the pipe's own rate from N = 64
-//    (32 cycles per MMA) and 19.5 cycles at N = 16. The MMAs of a tile come
-//    from several warps in no fixed order, so all of them ACCUMULATE into a
-//    D the compute threads zeroed after reading the previous tile (int32
-//    sums: order-independent).
+//    256) and commits to the mbarrier (one arrival per MMA warp). As compiled
+//    here an issuing warp spends ~70 cycles per MMA (its operands are moved
+//    from vector to uniform registers for every instruction), which matters
+//    only below N = 128 (the tensor pipe needs N / 2 cycles): four issuing
+//    warps hide it. (k_scan_tcw, the kernel for lists with few queries,
+//    issues from ONE warp with loop-invariant uniform operands at the pipe's
+//    own rate: tools/tc_kind_bench.) The MMAs of a tile come from several
+//    warps in no fixed order, so all of them ACCUMULATE into a D the compute
+//    threads zeroed after reading the previous tile (int32 sums:
+//    order-independent).
 //  D is single-buffered at N = 256: one MMA instruction costs ~77 cycles of
 //  issue for any N <= 128 but 128 cycles of execution at N = 256
 //  (tools/tc_mma_bench: 3.79 vs 4.59 POP/s back to back), so 256 queries per
@@ -1499,26 +1509,33 @@ k_scan_tc(const __grid_constant__ ScanArgs a) {
 //
 // IVF batches put 10-40 (query, list) pairs on a list (configs[4]: 93 % of
 // the scanned codes sit in lists probed by <= 32 queries of the batch), so
-// the MMA itself is short (N = 16 or 32: 8-16 cycles per K = 32 step) and the
-// tile's cost is the one-hot expansion and the latency of the expand -> MMA
-// -> read chain. k_scan_tc runs ONE tile at a time on all its warps, so
-// every thread repeats the tile's fixed work (addresses, barriers, bound
-// refresh) for a quarter of a code; here a CTA holds kWG independent
-// warpgroups, each scanning its own work item (list, <= 32 queries, chunk
-// range) tile by tile:
+// the MMA itself is short (N = 16 or 32: 8-16 cycles per K = 32 step) and a
+// tile's cost is the one-hot expansion of its codes on the ALU pipe plus the
+// latency of the expand -> MMA -> read chain. k_scan_tc runs ONE tile at a
+// time on all its warps, so every thread repeats the tile's fixed work
+// (addresses, barriers, bound refresh) for a quarter of a code; here a CTA
+// holds kWG independent warpgroups, each scanning its own work item (list,
+// <= 32 queries, chunk range) tile by tile:
 //   * thread = one code of the 128-code tile: ONE 16-byte load of its
-//     code-major row (coalesced 512 B per warp), m / 4 x 16 PRMT one-hot
-//     words written to its TMEM lane (tc_expand_cm);
-//   * warpgroup barrier; each of the 4 warps issues m / 8 of the tile's
-//     m / 2 MMAs (a single warp cannot issue faster than one MMA per ~70
-//     cycles; all MMAs accumulate into the zeroed D) and commits to the
-//     warpgroup's mbarrier;
-//   * every thread reads its code's N sums (16-bit packed), zeroes them and
-//     runs the SWAR threshold test; survivors go through the shared ring to
-//     the flusher warp (tc_hit_warp / tc_flusher, as k_scan_tc).
-// While one warpgroup waits for its MMAs the others expand: the ALU pipe
-// (PRMT) and the tensor pipe overlap without any cross-warpgroup barrier.
-// TMEM per warpgroup: D (32 columns) + A (4 m columns), single-buffered.
+//     code-major row (coalesced 512 B per warp, requested two tiles ahead),
+//     m / 4 x 16 PRMT one-hot words written to its TMEM lane (tc_expand_cm);
+//   * the tile is expanded and multiplied in two halves of m / 2
+//     sub-quantizers: warp 0 of the warpgroup waits on the half's named
+//     barrier (the others only arrive and go on), issues its m / 4 MMAs from
+//     loop-invariant uniform operands (the first MMA of a tile overwrites D,
+//     the rest accumulate) and commits to the half's mbarrier. The MMAs of
+//     half 0 run while half 1 is expanded, those of half 1 while half 0 of
+//     the NEXT tile is expanded, so no thread waits for an MMA just issued;
+//   * every thread reads its code's N sums (16-bit packed) and runs the SWAR
+//     threshold test after the next tile's first half has been issued;
+//     a code with survivors is handed (its packed sums) through the warp's
+//     own ring to the warpgroup's filter warp, which runs the per-pair test,
+//     midpoints and the push to the candidate ring (tc_hit_warp) drained by
+//     the flusher warp (tc_flusher, as k_scan_tc).
+// While one warpgroup waits (barrier, MMA) the others expand: the ALU pipe
+// (PRMT), the tensor pipe and the survivor path overlap without any
+// cross-warpgroup barrier. TMEM per warpgroup: D (32 columns) + A (4 m
+// columns), single-buffered.
 constexpr int kWG = 3;        // warpgroups per CTA (3 x (32 + 128) <= 512 TMEM columns)
 constexpr int kTcwNQ = 32;    // queries per item (MMA N = 16 or 32)
 constexpr int kTcwSlots = 8;  // survivor slots per compute warp
@@ -1736,7 +1753,8 @@ __global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const
         uint32_t hw[HW];
 #pragma unroll
         for (int i = 0; i < HW; i++) hw[i] = row[h * HW + i];
-        tc_expand_cm<MC / 2>(t_a + (uint32_t)(h * HCOLS), hw);
+        tc_expand_cm<MC / 2>(t_a + (uint32_t)(h * HCOLS), hw,
+                             kTcwDbg ? ((a.dbg >> 9) & 3) : 0);
       };
       auto issue_half = [&](int h) {
         // this thread's A row half is written (and, for half 0, its D row read)
@@ -1859,12 +1877,16 @@ __global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const
                 continue;
               }
               if (lane == src) {
-                TcwEnt &e = g_tcw.ent[w][rh % kTcwSlots];
+                // No fence between the entry and its publication: one
+                // thread's shared-memory stores are performed in program
+                // order (in-order LSU, nothing cached between an SM's warps
+                // and its shared memory); the volatile accesses and the asm
+                // barrier keep the compiler from reordering them.
+                volatile TcwEnt &e = g_tcw.ent[w][rh % kTcwSlots];
 #pragma unroll
-                for (int i = 0; i < NM / 2; i += 4)
-                  *(uint4 *)&e.sums[i] = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                for (int i = 0; i < NM / 2; i++) e.sums[i] = v[i];
                 e.pos = pos0 + src;
-                __threadfence_block();
+                asm volatile("" ::: "memory");
                 *(volatile unsigned *)&g_tcw.head[w] = rh + 1;
               }
               rh++;

@@ -101,7 +101,8 @@ if os.environ.get("KNOB_PROFILE") == "1":  # per-kernel device time of one searc
             t = rows.setdefault(ev.name, [0.0, 0])
             t[0] += ev.device_time
             t[1] += 1
-    for k, (us, c) in sorted(rows.items(), key=lambda kv: -kv[1][0])[:24]:
-        print(f"  {us / 3 / 1e3:8.3f} ms  x{c // 3:<3d} {k[:100]}", file=sys.stderr)
+    for k, (us, c) in sorted(rows.items(), key=lambda kv: -kv[1][0])[:14]:
+        k = k.replace("qadc::(anonymous namespace)::", "").replace("void ", "")
+        print(f"  {us / 3 / 1e3:8.3f} ms x{c // 3:<2d} {k[:40]}", file=sys.stderr)
 print(json.dumps({"step_ms": round(e0.elapsed_time(e1) / 5, 3), "scan_ms": round(scan / 5e3, 3),
                   "cand_per_query": round(cand / 5 / qs.shape[0], 1)}))
