@@ -141,9 +141,9 @@ QADC_API int64_t qadc_b200_index_bytes(const qadc_b200_index *idx);
                                   shard but the owner of the global prefix) */
 #define QADC_B200_SCAN_PRMT 8u /* scan with the PRMT (CUDA-core) kernel even
                                   where the tensor-core scan applies */
-#define QADC_B200_SCAN_TC 16u  /* tensor-core scan (m = 16, 32) even with few
-                                  (query, list) pairs per list; default: the
-                                  tensor cores from 64 pairs per list on */
+#define QADC_B200_SCAN_TC 16u  /* the all-warps-on-one-tile tensor-core scan
+                                  (m = 16, 32; up to 256 queries per pass)
+                                  whatever the batch */
 #define QADC_B200_SCAN_TC1 32u /* with the tensor-core scan of one exhaustive
                                   list: one SM per tile instead of CTA pairs
                                   (cta_group::2, the default) */
@@ -156,8 +156,9 @@ QADC_API int64_t qadc_b200_index_bytes(const qadc_b200_index *idx);
  * adc.py:114-187 search(method="qadc") for nq queries at once:
  * probe (IVF) -> residual, rotation, float LUT -> qmax from the first
  * probed cell's first `init` codes -> per-cell qmin/delta and uint8 LUT ->
- * scan with streaming thresholds (int8 tcgen05 one-hot GEMM for m = 16, 32
- * with >= 64 pairs per list; interleaved PRMT lookups otherwise) -> exact top-R by
+ * scan with streaming thresholds (int8 tcgen05 one-hot GEMM for m = 16, 32:
+ * CTA pairs on an exhaustive list, warpgroup-pipelined passes of <= 32 queries
+ * over inverted lists; interleaved PRMT lookups otherwise) -> exact top-R by
  * (distance, id). Outputs (nq, R) ids / fp32 midpoint distances sorted
  * ascending, padded with -1 / +inf, and out_n (nq) = result count.
  * With QADC_B200_LUT_IN, lut_in (nq, ma, m, 16) fp32 and cells_in (nq, ma)
