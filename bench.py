@@ -615,6 +615,7 @@ def run_b200(args):
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        torch.cuda.nvtx.range_push("qadc_timed_region")  # ncu --nvtx --nvtx-include "qadc_timed_region/"
         e0.record(stream)
         for _ in range(args.steps):
             (gi, gd), res = step_device()
@@ -622,6 +623,7 @@ def run_b200(args):
                 st[k] += res.stats[k]
         e1.record(stream)
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
     barrier()
     ms_dev = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
@@ -678,7 +680,8 @@ def run_b200(args):
                 "alu_pipe_peak_G": round(peak[1] / 1e9, 2)}
     if res.stats.get("scan_tc") == 2:
         # k_scan_tcw (IVF lists probed by a few queries each): every list is
-        # scanned ceil(pairs / 32) times; a pass expands each code of the
+        # scanned ceil(pairs / tq) times (tq = 32 queries per pass); a pass
+        # expands each code of the
         # list into its one-hot A row (4 m PRMT per code on the ALU pipe) and
         # runs m / 2 MMAs of N = 16 or 32 per 128-code tile. Three ceilings:
         # executed int8 MMA ops vs the measured tensor peak (the contract's
@@ -692,8 +695,9 @@ def run_b200(args):
         sizes_l = np.diff(row_off.cpu().numpy())
         pl = np.bincount(cells_l, minlength=sizes_l.size)
         tiles = 2 * ((sizes_l + 255) // 256)
-        full, rem = pl // 32, pl % 32
-        ncols = 32 * full + np.where(rem > 16, 32, np.where(rem > 0, 16, 0))
+        tq = int(res.stats.get("scan_tile_q") or 32)  # queries per pass over a list
+        full, rem = pl // tq, pl % tq
+        ncols = tq * full + ((rem + 15) // 16) * 16  # MMA N of the last pass: rounded to 16
         passes = full + (rem > 0)
         ops_exec = float((tiles * ncols).sum()) * 128 * 16 * pq.m * 2
         ops_useful = pairs * 16 * pq.m * 2
@@ -704,8 +708,8 @@ def run_b200(args):
         t_tensor, t_alu, t_hbm = ops_exec / mma[0], prmt / peak[1], cm_bytes / hbm_peak
         roof = {"bound": "tensor", "achieved": round(ops_exec / scan_s / 1e12, 2),
                 "peak": round(mma[0] / 1e12, 2),
-                "unit": "TOP/s int8 (executed one-hot MMA ops: 128 codes x N in {16, 32} query "
-                        "columns x 16 m per tile and pass) vs measured tcgen05.mma.kind::i8 peak "
+                "unit": "TOP/s int8 (executed one-hot MMA ops: 128 codes x N (queries of the pass, "
+                        "rounded to 16) x 16 m per tile and pass) vs measured tcgen05.mma.kind::i8 peak "
                         "(qadc_b200_mma_peak)",
                 "frac": round(t_tensor / scan_s, 4),
                 "useful_ops_frac": round(ops_useful / scan_s / mma[0], 4),
@@ -716,7 +720,8 @@ def run_b200(args):
                             "hbm_code_major": round(t_hbm * 1e3, 2),
                             "north_star_int_issue": round(lookups / peak[0] * 1e3, 2)},
                 "frac_of_slowest_ceiling": round(max(t_tensor, t_alu, t_hbm) / scan_s, 4),
-                "list_passes": {"code_passes": int(code_passes), "mean_passes_per_scanned_code":
+                "list_passes": {"queries_per_pass": tq, "code_passes": int(code_passes),
+                                "mean_passes_per_scanned_code":
                                 round(code_passes / max(1.0, float((tiles * (pl > 0)).sum()) * 128), 3)},
                 "int_issue_view": int_view}
         hbm_bytes = cm_bytes

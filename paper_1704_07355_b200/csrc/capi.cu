@@ -113,6 +113,7 @@ struct SearchStats {
   int64_t codes = 0, cands = 0, reruns = 0, scan_launches = 0, launches = 0;
   double scan_us = 0.0;
   int scan_tc = 0;  // the scan ran on the tensor cores
+  int scan_tile_q = 0;  // queries per work item (per pass over a list) of the scan kernel
   // device time per phase of the first pass (adc.py:140-179's Index /
   // Tables / Scan split; the work list and the exact top-R are the GPU's
   // own phases), CUDA events on the search stream
@@ -266,14 +267,25 @@ int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int in
   static const int tcw_min = scan_env_int("QADC_B200_TCW_MIN_PAIRS", 6);
   static const int tcw_max = scan_env_int("QADC_B200_TCW_MAX_PAIRS", 1 << 20);
   const int nl = idx->nlists;
-  bool tcw = false;
+  int tcw = 0;
   if (!prmt && !force_tc && !one_sm && idx->K > 0 && scan_use_tc(m, false)) {
     const double load = (double)npairs / nl;
     const double per_probed = load / std::max(1e-9, 1.0 - std::exp(-load));
-    tcw = force_tcw || (tcw_env && nl > 1 && per_probed >= tcw_min && load <= tcw_max);
+    // (a 2-warpgroup shape with <= 128 queries per pass was measured for the
+    // lists of configs[2]: 32.2 / 23.7 ms at nprobe 16 / 64 against 5.9 /
+    // 11.7 ms here: its survivor entries are 4x wider and two filter warps
+    // do not keep up)
+    if (force_tcw || (tcw_env && nl > 1 && per_probed >= tcw_min && load <= tcw_max)) tcw = 1;
+    // the code-major copy (m / 2 more bytes per code) may not fit next to a
+    // very large index: the heuristic choice then stays on the PRMT scan
+    if (tcw && ensure_code_major(idx, st) != kOk) {
+      if (force_tcw) return kErrCuda;
+      cudaGetLastError();
+      tcw = 0;
+    }
   }
   if (!tcw && !force_tc && npairs < (int64_t)tc_min_pairs * std::max(idx->nlists, 1)) prmt = true;
-  const int qt_tile = scan_tile_queries(m, prmt, tcw);
+  const int qt_tile = scan_tile_queries(m, prmt, tcw != 0);
 
   DevBuf<float> cand_mid, hist_w;
   DevBuf<unsigned> cand_n, hist;
@@ -371,7 +383,7 @@ int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int in
   ScanArgs a;
   a.codes = idx->codes;
   a.codes_cm = nullptr;
-  a.tcw = tcw ? 1 : 0;
+  a.tcw = tcw;
   if (scan_use_tc(m, prmt) && !pair_cta) {  // k_scan_tc / k_scan_tcw expand from the code-major copy
     if ((rc = ensure_code_major(idx, st))) return rc;
     a.codes_cm = idx->codes_cm;
@@ -410,6 +422,7 @@ int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int in
     tc_stats_dump();
   }
   ss.scan_tc = scan_use_tc(m, prmt) ? (tcw ? 2 : 1) : 0;
+  if (level == 0) ss.scan_tile_q = qt_tile;
   QADC_CUDA(cudaGetLastError());
   cudaEventRecord(e1, st);
   ss.scan_launches++;
@@ -582,12 +595,13 @@ void write_stats(const SearchStats &ss, int64_t *stats) {
   stats[3] = ss.scan_launches;
   stats[4] = ss.launches;
   stats[5] = (int64_t)llround(ss.scan_us);
-  stats[6] = ss.scan_tc;  // scan kernel: 1 = int8 tensor-core, 0 = PRMT
+  stats[6] = ss.scan_tc;  // scan kernel: 0 = PRMT, 1 = int8 tensor-core, 2 = warpgroup-pipelined int8 tensor-core
   stats[7] = (int64_t)llround(ss.probe_us);
   stats[8] = (int64_t)llround(ss.tables_us);
   stats[9] = (int64_t)llround(ss.work_us);
   stats[10] = (int64_t)llround(ss.select_us);
-  for (int i = 11; i < 16; i++) stats[i] = 0;
+  stats[11] = ss.scan_tile_q;
+  for (int i = 12; i < 16; i++) stats[i] = 0;
 }
 
 }  // namespace

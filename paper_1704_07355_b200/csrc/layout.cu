@@ -154,13 +154,19 @@ int ensure_code_major(qadc_b200_index *idx, cudaStream_t st) {
   const int64_t tc = std::max<int64_t>(idx->total_chunks, 1);
   const size_t bytes = (size_t)tc * kChunkCodes * (idx->m / 8) * 4;
   uint32_t *p = nullptr;
-  QADC_CUDA(cudaMalloc(&p, bytes));
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("code-major copy of the codes: out of device memory");
+    return kErrCuda;
+  }
   if (idx->total_chunks > 0)
     k_code_major<<<grid_for(idx->total_chunks * kChunkCodes * (idx->m / 8)), 256, 0, st>>>(
         idx->codes, idx->m, idx->total_chunks, p);
   else
     cudaMemsetAsync(p, 0, bytes, st);
   QADC_CUDA(cudaGetLastError());
+  // one-time: the copy is complete before any stream can see the pointer
+  QADC_CUDA(cudaStreamSynchronize(st));
   idx->codes_cm = p;
   idx->bytes += (int64_t)bytes;
   return kOk;

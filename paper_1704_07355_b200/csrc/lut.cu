@@ -634,21 +634,46 @@ __global__ void __launch_bounds__(256) k_quantize(const float *__restrict__ lut,
     __syncwarp();
   }
   const float *t = lut + (size_t)pair * m * 16;
+  // m <= 32: the pair's table (<= 512 floats) is read once, 4 float4 per
+  // lane, and both passes (minimum, bins) run from registers
+  const bool in_regs = m <= 32;
+  float4 tv[4];
+  if (in_regs) {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int w = lane + 32 * i;
+      tv[i] = w < m * 4 ? *(const float4 *)(t + w * 4) : make_float4(FLT_MAX, FLT_MAX, FLT_MAX, FLT_MAX);
+    }
+  }
   double qmin, qmax;
   if (qmin_in) {
     qmin = qmin_in[pair];
     qmax = qmax_in[pair];
   } else {
     float mn = FLT_MAX;
-    for (int e = lane; e < m * 16; e += 32) mn = fminf(mn, t[e]);
+    if (in_regs) {
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        mn = fminf(mn, fminf(fminf(tv[i].x, tv[i].y), fminf(tv[i].z, tv[i].w)));
+    } else {
+      for (int e = lane; e < m * 16; e += 32) mn = fminf(mn, t[e]);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     qmax = (double)qmax_q[pair / nslots];
     qmin = fmin((double)mn, qmax);
   }
   const double delta = __ddiv_rn(__dsub_rn(qmax, qmin), (double)kQuantBins);
-  for (int w = lane; w < m * 4; w += 32) {
-    const float4 v4 = *(const float4 *)(t + w * 4);
+  // floor(fl(x / delta)) without a float64 division per entry (software
+  // division: ~10 % of this kernel at configs[4]): k = floor(x *
+  // fl(1 / delta)) is accepted when the exactly rounded residuals x - k delta
+  // >= margin and x - (k + 1) delta <= -margin (margin = 2^-40 delta, far
+  // above the spacing of doubles below 128): then k < x / delta < k + 1 -
+  // 2^-41, so the rounded quotient lies in [k, k + 1) too. Anything else
+  // (quotients within 2^-40 of an integer, overflow, NaN) takes the division.
+  const double rdelta = delta > 0 ? __ddiv_rn(1.0, delta) : 0.0;
+  const double marg = delta * 0x1p-40;
+  auto quant_word = [&](int w, const float4 v4) {
     const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
     uint32_t word = 0;
 #pragma unroll
@@ -656,7 +681,10 @@ __global__ void __launch_bounds__(256) k_quantize(const float *__restrict__ lut,
       const double v = (double)vv[b];
       double qq;
       if (delta > 0) {
-        qq = floor(__ddiv_rn(__dsub_rn(v, qmin), delta));
+        const double x = __dsub_rn(v, qmin);
+        qq = floor(__dmul_rn(x, rdelta));
+        const double r0 = __fma_rn(-qq, delta, x), r1 = __fma_rn(-(qq + 1.0), delta, x);
+        if (!(r0 >= marg && r1 <= -marg)) qq = floor(__ddiv_rn(x, delta));
         qq = fmin(fmax(qq, 0.0), (double)kQuantBins);
       } else {
         qq = v <= qmin ? 0.0 : (double)kQuantBins;
@@ -670,6 +698,13 @@ __global__ void __launch_bounds__(256) k_quantize(const float *__restrict__ lut,
       const uint32_t mx = __vmaxu4(word, word >> 16);
       atomicMax(&rmax[w >> 2], max(mx & 255u, (mx >> 8) & 255u));
     }
+  };
+  if (in_regs) {
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      if (lane + 32 * i < m * 4) quant_word(lane + 32 * i, tv[i]);
+  } else {
+    for (int w = lane; w < m * 4; w += 32) quant_word(w, *(const float4 *)(t + w * 4));
   }
   if (pair_depth) {
     // byte-sum depth of this pair's scan: the largest D in {16, 8, 4, 2}
@@ -733,6 +768,10 @@ __global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ cod
   for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&whist[0][0])[i] = 0;
   __syncthreads();
   for (int s = 0; s < nslots; s++) {
+    // later cells matter only while fewer than R valid lanes have been seen
+    // (s_seen is stable here: last written before a barrier); without this
+    // exit every query staged the tables of all its probed cells
+    if (s > 0 && s_seen >= R) break;
     const int pair = q * nslots + s;
     const int64_t L = cells ? cells[pair] : 0;
     const int64_t c0 = chunk_off[L], n = lanes[L];

@@ -31,7 +31,7 @@ def _np(a, dtype):
 
 class DeviceIndex:
     STAT_KEYS = ("codes", "candidates", "reruns", "scan_launches", "launches", "scan_us",
-                 "scan_tc", "probe_us", "tables_us", "work_us", "select_us")
+                 "scan_tc", "probe_us", "tables_us", "work_us", "select_us", "scan_tile_q")
 
     def __init__(self, handle: int, d: int, m: int, K: int, nlists: int, ncodes: int):
         self._h = handle

@@ -542,13 +542,15 @@ def test_ivf_search_vs_oracle_at_scale(gpu, ma):
     assert np.array_equal(_bits(nat.distances), _bits(nd))
 
 @pytest.mark.parametrize("m,K,n,nq,ma,R", [(32, 48, 60_000, 150, 12, 50), (16, 20, 30_000, 64, 5, 100),
-                                           (32, 300, 40_000, 400, 20, 10)])
+                                           (32, 300, 40_000, 400, 20, 10), (16, 24, 30_000, 200, 8, 100),
+                                           (32, 16, 50_000, 300, 10, 100)])
 def test_warpgroup_tensor_core_scan_vs_oracle(gpu, m, K, n, nq, ma, R):
-    """k_scan_tcw (IVF lists probed by a few queries each: <= 32 queries per
-    pass, code-major one-hot expansion, MMAs issued by four warps into a
-    zeroed accumulator): ids, fp32 distance bits and counts equal the oracle's
-    and the PRMT scan's on lists of 0..~3000 codes with 1..~40 pairs each
-    (lists with more than 32 pairs take several passes)."""
+    """k_scan_tcw (IVF lists probed by a few queries each: code-major one-hot
+    expansion, one issuing warp per warpgroup, survivors through per-warp
+    rings): ids, fp32 distance bits and counts equal the oracle's and the PRMT
+    scan's on lists of 0..~3000 codes with 1..~200 pairs each (<= 32 queries
+    per pass: lists with more pairs take several passes, MMA N = 16 and
+    32)."""
     import torch
 
     from paper_1704_07355_b200 import datagen
