@@ -966,8 +966,12 @@ __device__ __forceinline__ void tc_put(const ScanArgs &a, int query, float mid, 
 // claim per warp. Each warp checks the ring's room before reserving and has
 // at most one reservation (<= 32 slots) in flight, so 16 x 32 = 512 slots of
 // slack make the reservation safe; a full ring falls back to direct appends.
+// (slack: slots kept free for reservations in flight — every warp that can
+// push may hold one of up to 64 slots between its check and its claim;
+// k_scan_tcw passes 640 = 12 compute warps x 32 + 3 filter warps x 64 + a
+// margin, which makes its ring overflow-free by construction.)
 __device__ __forceinline__ void tc_hit_warp(const ScanArgs &a, bool w0, bool w1, int q,
-                                            uint32_t vv, int64_t pos) {
+                                            uint32_t vv, int64_t pos, unsigned slack = 512) {
   const int lane = threadIdx.x & 31;
   float mid0 = 0.f, mid1 = 0.f;
   if (w0) {
@@ -984,7 +988,7 @@ __device__ __forceinline__ void tc_hit_warp(const ScanArgs &a, bool w0, bool w1,
   unsigned base = 0xffffffffu;
   if (lane == leader) {
     const unsigned h = *(volatile unsigned *)&g_tc.head, t = *(volatile unsigned *)&g_tc.tail;
-    if (h - t < (unsigned)(kRing - 512))
+    if (h - t < (unsigned)kRing - slack)
       base = atomicAdd(&g_tc.head, (unsigned)(__popc(b0) + __popc(b1)));
   }
   base = __shfl_sync(kFull, base, leader);
@@ -1598,7 +1602,7 @@ __device__ __forceinline__ void tcw_filter(const ScanArgs &a, int f) {
     const int64_t pos = e.pos;
     const int q = qb + 2 * pl;
     const uint32_t x = *(const uint32_t *)&g_tc.thr16[q] - vv;
-    tc_hit_warp(a, on && (x & 0x8000u) != 0, on && (x & 0x80000000u) != 0, q, vv, pos);
+    tc_hit_warp(a, on && (x & 0x8000u) != 0, on && (x & 0x80000000u) != 0, q, vv, pos, 640u);
     if (lane == rl) {
       tail = t0 + n;
       __threadfence_block();  // the entries were read before their slots are released
@@ -1873,7 +1877,7 @@ __global__ void __launch_bounds__(128 * kWG + 32 + 32 * kWG, 1) k_scan_tcw(const
                 const int q = qb + 2 * (lane & (NM / 2 - 1));
                 const uint32_t x = *(const uint32_t *)&s.thr16[q] - vv;
                 __syncwarp();
-                tc_hit_warp(a, on && (x & 0x8000u) != 0, on && (x & 0x80000000u) != 0, q, vv, pos0 + src);
+                tc_hit_warp(a, on && (x & 0x8000u) != 0, on && (x & 0x80000000u) != 0, q, vv, pos0 + src, 640u);
                 continue;
               }
               if (lane == src) {
