@@ -752,6 +752,7 @@ __global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ cod
                                                 const float *__restrict__ delta_f,
                                                 const int64_t *__restrict__ cells, int m,
                                                 int nslots, int R, int init, int bound_prefix,
+                                                int prefix_div,
                                                 unsigned *__restrict__ M_bits, int *__restrict__ fsat_n,
                                                 float *__restrict__ fsat_mid,
                                                 int64_t *__restrict__ fsat_id) {
@@ -779,7 +780,7 @@ __global__ void __launch_bounds__(256) k_prefix(const uint32_t *__restrict__ cod
     // bound prefix of cell 0: at least init codes, and up to kBoundPrefix
     // (at most 1/64 of the list) so the initial bound starts near the
     // R/prefix quantile without costing more than ~2% of the scan
-    int64_t want = n / 64 < bound_prefix ? n / 64 : bound_prefix;
+    int64_t want = n / prefix_div < bound_prefix ? n / prefix_div : bound_prefix;
     if (want < init) want = init;
     const int64_t pref = (s == 0) ? (want < n ? want : n) : 0;
     for (int e = threadIdx.x; e < m * 4; e += blockDim.x)
@@ -994,9 +995,15 @@ void launch_prefix(const qadc_b200_index *idx, const uint32_t *qt, const float *
   if (nq <= 0) return;
   // codes of the first cell's prefix behind the initial bound (tuning knob)
   static const int bound_prefix = std::max(256, scan_env_int("QADC_B200_BOUND_PREFIX", kBoundPrefix));
+  // share of the first cell behind the initial bound: 1/64 of an exhaustive
+  // list (~2 % of the scan); an inverted list is one of many, so all of it
+  // (up to bound_prefix codes) — the streaming candidate count of an exact
+  // top-R is ~R ln(n / prefix)
+  static const int div_env = scan_env_int("QADC_B200_BOUND_PREFIX_DIV", 0);
+  const int prefix_div = div_env > 0 ? div_env : (idx->K && nslots > 1 ? 1 : 64);
   k_prefix<<<nq, 256, 0, st>>>(idx->pcodes, idx->pchunk_off, idx->planes, idx->pids, qt, qmin_f,
                                delta_f, idx->K ? cells : nullptr, idx->m, nslots, R, init,
-                               bound_prefix, M_bits,
+                               bound_prefix, prefix_div, M_bits,
                                fsat_n, fsat_mid, fsat_id);
 }
 
