@@ -150,7 +150,7 @@ QADC_API int64_t qadc_b200_index_bytes(const qadc_b200_index *idx);
 #define QADC_B200_SCAN_TCW 64u /* IVF index, m = 16, 32: the warpgroup-
                                   pipelined tensor-core scan (<= 32 queries
                                   per pass over a list) whatever the batch;
-                                  default: from ~6 queries per probed list */
+                                  default: from ~4 queries per probed list */
 
 /*
  * adc.py:114-187 search(method="qadc") for nq queries at once:

@@ -261,10 +261,13 @@ int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int in
   // pipelined tensor-core scan (k_scan_tcw, <= 32 queries per pass over a
   // list). Its cost per code is the one-hot expansion, whatever the number
   // of queries, so the PRMT kernel keeps the batches that put fewer than
-  // ~6 queries on a probed list (expected probed lists under uniform
+  // ~4 queries on a probed list (expected probed lists under uniform
   // probing: nl (1 - exp(-npairs / nl))). QADC_B200_TCW=0 disables it.
   static const int tcw_env = scan_env_int("QADC_B200_TCW", 1);
-  static const int tcw_min = scan_env_int("QADC_B200_TCW_MIN_PAIRS", 6);
+  // (measured at configs[4] with smaller batches: Q = 2000 PRMT 10.2 ms vs
+  // 15.1 ms, Q = 4000 16.9 vs 15.9 ms, Q = 6000 23.8 vs ~16.5 ms, Q = 10^4
+  // 37.4 vs 17.9 ms: the kernels cross at ~3.8 by this estimate)
+  static const int tcw_min = scan_env_int("QADC_B200_TCW_MIN_PAIRS", 4);
   static const int tcw_max = scan_env_int("QADC_B200_TCW_MAX_PAIRS", 1 << 20);
   const int nl = idx->nlists;
   int tcw = 0;
@@ -275,7 +278,7 @@ int scan_impl(qadc_b200_index *idx, const Prep &p, int nq, int R, int ma, int in
     // lists of configs[2]: 32.2 / 23.7 ms at nprobe 16 / 64 against 5.9 /
     // 11.7 ms here: its survivor entries are 4x wider and two filter warps
     // do not keep up)
-    if (force_tcw || (tcw_env && nl > 1 && per_probed >= tcw_min && load <= tcw_max)) tcw = 1;
+    if (force_tcw || (tcw_env && nl > 1 && per_probed >= 0.95 * tcw_min && load <= tcw_max)) tcw = 1;
     // the code-major copy (m / 2 more bytes per code) may not fit next to a
     // very large index: the heuristic choice then stays on the PRMT scan
     if (tcw && ensure_code_major(idx, st) != kOk) {

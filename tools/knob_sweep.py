@@ -50,6 +50,8 @@ d = torch.load(cache)
 index = make_ivf_index(pq, coarse, d["rows"].cuda(), d["ids"].cuda(), d["row_off"].cuda())
 del d
 qs = torch.from_numpy(queries(cfg)).cuda()
+if os.environ.get("KNOB_Q"):  # a smaller batch (the scan-kernel heuristic depends on queries per list)
+    qs = qs[:int(os.environ["KNOB_Q"])].contiguous()
 if os.environ.get("KNOB_LIST_STATS") == "1":  # (query, list) pairs per list, weighted by scanned codes
     import numpy as np
     ro = torch.load(cache)["row_off"].numpy()
